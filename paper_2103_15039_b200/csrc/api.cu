@@ -1,0 +1,455 @@
+// C ABI of liblsgcpd.so (see include/lsgcpd.h for the contract of every entry point).
+#include <dlfcn.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+#define LSG_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace lsg {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    set_error("CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+    return LSGCPD_ECUDA;
+}
+
+static bool finite_vec(const double* v, int n) {
+    for (int i = 0; i < n; ++i)
+        if (!isfinite(v[i])) return false;
+    return true;
+}
+
+static bool is_rotation(const double* R) {
+    if (!finite_vec(R, 9)) return false;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 3; ++k) s += R[3 * k + i] * R[3 * k + j];
+            if (fabs(s - (i == j ? 1.0 : 0.0)) > 1e-6) return false;
+        }
+    const double det = R[0] * (R[4] * R[8] - R[5] * R[7]) - R[1] * (R[3] * R[8] - R[5] * R[6]) +
+                       R[2] * (R[3] * R[7] - R[4] * R[6]);
+    return det > 0.0;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---------------------------------------------------------------------------------------------
+// NCCL, loaded at run time (the library does not link it; torch's libnccl.so.2 is reused if loaded)
+// ---------------------------------------------------------------------------------------------
+typedef int ncclResult_t;
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+    char internal[128];
+} ncclUniqueId;
+enum { kNcclFloat64 = 8, kNcclSum = 0 };
+
+struct Nccl {
+    bool loaded = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+static Nccl g_nccl;
+static std::mutex g_nccl_mu;
+
+static int nccl_load() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.loaded) return 0;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    LSG_CHECK(h != nullptr, LSGCPD_ENCCL, "cannot load libnccl.so.2: %s", dlerror());
+    g_nccl.GetUniqueId = (ncclResult_t(*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (ncclResult_t(*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
+    g_nccl.AllReduce =
+        (ncclResult_t(*)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
+    g_nccl.CommDestroy = (ncclResult_t(*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
+    g_nccl.GetErrorString = (const char* (*)(ncclResult_t))dlsym(h, "ncclGetErrorString");
+    LSG_CHECK(g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy, LSGCPD_ENCCL,
+              "libnccl.so.2 lacks required symbols");
+    g_nccl.loaded = true;
+    return 0;
+}
+
+static int nccl_fail(ncclResult_t r, const char* what) {
+    set_error("NCCL error %d (%s) in %s", r, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?", what);
+    return LSGCPD_ENCCL;
+}
+
+struct Comm {
+    ncclComm_t nc;
+    int rank, world;
+};
+
+// ---------------------------------------------------------------------------------------------
+// Workspace layouts
+// ---------------------------------------------------------------------------------------------
+struct EstepLayout {
+    size_t state, part, total;
+};
+static int estep_layout(int64_t M_pad, int64_t N, EstepLayout* L, Sched* sc) {
+    const int rc = estep_plan(M_pad, N, sc);
+    if (rc) return rc;
+    size_t o = 0;
+    L->state = o; o += al(sizeof(IterState));
+    L->part = o; o += al(estep_partial_bytes(*sc));
+    L->total = o;
+    return 0;
+}
+
+struct RegLayout {
+    size_t state, mom, sums, blockpart, counters, nll, sig2, iters, part, rec, total;
+};
+static int reg_layout(int64_t M_pad, int64_t N, int max_iters, RegLayout* L, Sched* sc) {
+    const int rc = estep_plan(M_pad, N, sc);
+    if (rc) return rc;
+    size_t o = 0;
+    L->state = o; o += al(sizeof(IterState));
+    L->mom = o; o += al(sizeof(double) * 80);
+    L->sums = o; o += al(sizeof(double) * 4);
+    L->blockpart = o; o += al(sizeof(double) * kMomentBlocks * kMomentCount);
+    L->counters = o; o += al(sizeof(unsigned) * 8);
+    L->nll = o; o += al(sizeof(double) * (max_iters + 1));
+    L->sig2 = o; o += al(sizeof(double) * (max_iters + 2));
+    L->iters = o; o += al(sizeof(int) * 4);
+    L->part = o; o += al(estep_partial_bytes(*sc));
+    L->rec = o; o += al(sizeof(float) * LSGCPD_REC * (size_t)N);
+    L->total = o;
+    return 0;
+}
+
+static int read_header(const void* d_target, int64_t M, TargetHeader* h, cudaStream_t stream) {
+    LSG_CUDA(cudaMemcpyAsync(h, d_target, sizeof(TargetHeader), cudaMemcpyDeviceToHost, stream));
+    LSG_CUDA(cudaStreamSynchronize(stream));
+    LSG_CHECK(h->magic == kTargetMagic, LSGCPD_EINVAL, "d_target is not a prepared target (bad magic)");
+    LSG_CHECK(h->M == M, LSGCPD_EINVAL, "M=%lld does not match the prepared target (M=%lld)", (long long)M,
+              (long long)h->M);
+    return 0;
+}
+
+// One EM iteration (async): E step → moments → [all-reduce] → Newton + σ².
+static int enqueue_iteration(const void* d_target, const float* d_src, int64_t N, char* ws, const RegLayout& L,
+                             const Sched& sc, const RegParams& rp, Comm* comm, cudaStream_t stream) {
+    IterState* st = reinterpret_cast<IterState*>(ws + L.state);
+    double* mom = reinterpret_cast<double*>(ws + L.mom);
+    float* rec = reinterpret_cast<float*>(ws + L.rec);
+    estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), rec, rp.consistent, stream);
+    moments_launch(rec, d_src, N, st, reinterpret_cast<double*>(ws + L.blockpart), mom,
+                   reinterpret_cast<unsigned*>(ws + L.counters), stream);
+    if (comm) {
+        const ncclResult_t r = g_nccl.AllReduce(mom, mom, kMomentCount, kNcclFloat64, kNcclSum, comm->nc, stream);
+        if (r != 0) return nccl_fail(r, "ncclAllReduce(moments)");
+    }
+    newton_launch(st, mom, rp, reinterpret_cast<double*>(ws + L.nll), reinterpret_cast<double*>(ws + L.sig2),
+                  reinterpret_cast<int*>(ws + L.iters), stream);
+    return 0;
+}
+
+}  // namespace lsg
+
+using namespace lsg;
+
+// =============================================================================================
+// exported C ABI
+// =============================================================================================
+LSG_EXPORT int lsgcpd_version(void) { return 10000; }
+LSG_EXPORT const char* lsgcpd_last_error(void) { return g_err; }
+
+LSG_EXPORT void lsgcpd_prep_params_default(lsgcpd_prep_params* p) {
+    if (!p) return;
+    p->alpha_max = 50.0f;
+    p->lambda = 0.5f;
+    p->knn_k = 10;
+    p->volume_margin = 0.1;
+}
+
+LSG_EXPORT void lsgcpd_em_params_default(lsgcpd_em_params* p) {
+    if (!p) return;
+    p->w = 0.1;
+    p->max_iters = 50;
+    p->newton_max = 10;
+    p->consistent_normalizer = 1;
+    p->sigma2_init = 0.0;
+    p->sigma2_floor_rel = 1e-12;
+    p->tol = 0.0;
+}
+
+LSG_EXPORT size_t lsgcpd_target_bytes(int64_t M) {
+    if (M < 0) return 0;
+    return kHeaderBytes + (size_t)pad_targets(M) * kTgtFloats * sizeof(float);
+}
+
+LSG_EXPORT size_t lsgcpd_prepare_workspace_bytes(int64_t M, int knn_k) {
+    (void)knn_k;
+    if (M < 0) return 0;
+    return prepare_ws_bytes(M);
+}
+
+LSG_EXPORT size_t lsgcpd_pack_workspace_bytes(int64_t M) {
+    if (M < 0) return 0;
+    return pack_ws_bytes(M);
+}
+
+LSG_EXPORT int lsgcpd_prepare_target(const float* d_xyz, int64_t M, const lsgcpd_prep_params* params, void* d_target,
+                                     void* d_ws, size_t ws_bytes, lsgcpd_target_info* h_info,
+                                     const lsgcpd_annotations* annotations, lsgcpd_stream_t stream) {
+    lsgcpd_prep_params p;
+    lsgcpd_prep_params_default(&p);
+    if (params) p = *params;
+    LSG_CHECK(d_xyz && d_target && d_ws, LSGCPD_EINVAL, "null pointer argument");
+    LSG_CHECK(aligned16(d_target), LSGCPD_EINVAL, "d_target must be 16-byte aligned");
+    LSG_CHECK(M >= 3 && M < (int64_t)1 << 30, LSGCPD_EINVAL, "M=%lld out of range [3, 2^30)", (long long)M);
+    LSG_CHECK(p.knn_k >= 3 && p.knn_k <= 32 && p.knn_k <= M, LSGCPD_EINVAL, "knn_k=%d out of range [3, min(32, M)]",
+              p.knn_k);
+    LSG_CHECK(isfinite(p.alpha_max) && p.alpha_max >= 0.f && isfinite(p.lambda) && p.lambda > 0.f, LSGCPD_EINVAL,
+              "alpha_max must be >= 0 and lambda > 0");
+    LSG_CHECK(isfinite(p.volume_margin) && p.volume_margin >= 0.0, LSGCPD_EINVAL, "volume_margin must be >= 0");
+    LSG_CHECK(ws_bytes >= prepare_ws_bytes(M), LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes,
+              prepare_ws_bytes(M));
+    return prepare_target_impl(d_xyz, M, p, d_target, d_ws, h_info, annotations, (cudaStream_t)stream);
+}
+
+LSG_EXPORT int lsgcpd_pack_target(const float* d_xyz, const float* d_normals, const float* d_alpha, int64_t M,
+                                  double volume_margin, void* d_target, void* d_ws, size_t ws_bytes,
+                                  lsgcpd_target_info* h_info, lsgcpd_stream_t stream) {
+    LSG_CHECK(d_xyz && d_normals && d_alpha && d_target && d_ws, LSGCPD_EINVAL, "null pointer argument");
+    LSG_CHECK(aligned16(d_target), LSGCPD_EINVAL, "d_target must be 16-byte aligned");
+    LSG_CHECK(M >= 1 && M < (int64_t)1 << 30, LSGCPD_EINVAL, "M=%lld out of range", (long long)M);
+    LSG_CHECK(isfinite(volume_margin) && volume_margin >= 0.0, LSGCPD_EINVAL, "volume_margin must be >= 0");
+    LSG_CHECK(ws_bytes >= pack_ws_bytes(M), LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes,
+              pack_ws_bytes(M));
+    const int rc = pack_target_impl(d_xyz, d_normals, d_alpha, M, volume_margin, d_target, d_ws, h_info,
+                                    (cudaStream_t)stream);
+    if (rc == LSGCPD_EDEGENERATE && h_info && !isfinite(h_info->extent)) {
+        set_error("non-finite coordinate in d_xyz");
+        return LSGCPD_EINVAL;
+    }
+    return rc;
+}
+
+LSG_EXPORT size_t lsgcpd_estep_workspace_bytes(int64_t M, int64_t N) {
+    if (M < 1 || N < 1) return 0;
+    EstepLayout L;
+    Sched sc;
+    if (estep_layout(pad_targets(M), N, &L, &sc)) return 0;
+    return L.total;
+}
+
+LSG_EXPORT int lsgcpd_estep(const void* d_target, int64_t M, const float* d_src, int64_t N, const double R[9],
+                            const double t[3], double sigma2, double w, double volume, int consistent_normalizer,
+                            float* d_record, void* d_ws, size_t ws_bytes, lsgcpd_stream_t stream) {
+    LSG_CHECK(d_target && d_src && d_record && d_ws && R && t, LSGCPD_EINVAL, "null pointer argument");
+    LSG_CHECK(aligned16(d_target) && aligned16(d_record) && aligned16(d_ws), LSGCPD_EINVAL,
+              "d_target, d_record and d_ws must be 16-byte aligned");
+    LSG_CHECK(M >= 1 && N >= 1 && M < (int64_t)1 << 30 && N < (int64_t)1 << 34, LSGCPD_EINVAL,
+              "M=%lld N=%lld out of range", (long long)M, (long long)N);
+    LSG_CHECK(isfinite(sigma2) && sigma2 > 0.0, LSGCPD_EINVAL, "sigma2 must be finite and > 0");
+    LSG_CHECK(isfinite(w) && w >= 0.0 && w < 1.0, LSGCPD_EINVAL, "w must be in [0, 1)");
+    LSG_CHECK(isfinite(volume) && volume > 0.0, LSGCPD_EINVAL, "volume must be finite and > 0");
+    LSG_CHECK(is_rotation(R), LSGCPD_EINVAL, "R is not a rotation matrix (to 1e-6)");
+    LSG_CHECK(finite_vec(t, 3), LSGCPD_EINVAL, "t must be finite");
+    EstepLayout L;
+    Sched sc;
+    int rc = estep_layout(pad_targets(M), N, &L, &sc);
+    if (rc) return rc;
+    LSG_CHECK(ws_bytes >= L.total, LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
+    cudaStream_t s = (cudaStream_t)stream;
+    char* ws = static_cast<char*>(d_ws);
+    IterState* st = reinterpret_cast<IterState*>(ws + L.state);
+    estep_launch_setup(st, d_target, R, t, sigma2, w, volume, M, consistent_normalizer ? 1 : 0, s);
+    estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), d_record,
+                 consistent_normalizer ? 1 : 0, s);
+    LSG_CUDA(cudaGetLastError());
+    return 0;
+}
+
+LSG_EXPORT int lsgcpd_comm_unique_id(void* h_out128) {
+    LSG_CHECK(h_out128, LSGCPD_EINVAL, "null pointer argument");
+    int rc = nccl_load();
+    if (rc) return rc;
+    ncclUniqueId id;
+    const ncclResult_t r = g_nccl.GetUniqueId(&id);
+    if (r != 0) return nccl_fail(r, "ncclGetUniqueId");
+    memcpy(h_out128, &id, sizeof(id));
+    return 0;
+}
+
+LSG_EXPORT int lsgcpd_comm_init(int rank, int world_size, const void* h_id128, void** comm_out) {
+    LSG_CHECK(h_id128 && comm_out, LSGCPD_EINVAL, "null pointer argument");
+    LSG_CHECK(world_size >= 1 && rank >= 0 && rank < world_size, LSGCPD_EINVAL, "bad rank/world_size");
+    int rc = nccl_load();
+    if (rc) return rc;
+    ncclUniqueId id;
+    memcpy(&id, h_id128, sizeof(id));
+    Comm* c = new Comm();
+    c->rank = rank;
+    c->world = world_size;
+    const ncclResult_t r = g_nccl.CommInitRank(&c->nc, world_size, id, rank);
+    if (r != 0) {
+        delete c;
+        return nccl_fail(r, "ncclCommInitRank");
+    }
+    *comm_out = c;
+    return 0;
+}
+
+LSG_EXPORT int lsgcpd_comm_destroy(void* comm) {
+    if (!comm) return 0;
+    Comm* c = static_cast<Comm*>(comm);
+    ncclResult_t r = 0;
+    if (g_nccl.loaded) r = g_nccl.CommDestroy(c->nc);
+    delete c;
+    if (r != 0) return nccl_fail(r, "ncclCommDestroy");
+    return 0;
+}
+
+LSG_EXPORT size_t lsgcpd_register_workspace_bytes(int64_t M, int64_t N_local, int max_iters) {
+    if (M < 1 || N_local < 1 || max_iters < 0) return 0;
+    RegLayout L;
+    Sched sc;
+    if (reg_layout(pad_targets(M), N_local, max_iters, &L, &sc)) return 0;
+    return L.total;
+}
+
+LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, const float* d_src_local,
+                               int64_t N_local, const lsgcpd_em_params* params, const double R0[9], const double t0[3],
+                               double R_out[9], double t_out[3], double* sigma2_out, int* iters_out,
+                               double* nll_trace, double* sigma2_trace, void* comm, void* d_ws, size_t ws_bytes,
+                               lsgcpd_stream_t stream) {
+    lsgcpd_em_params p;
+    lsgcpd_em_params_default(&p);
+    if (params) p = *params;
+    LSG_CHECK(d_target && d_src_local && d_ws && R_out && t_out && sigma2_out && iters_out, LSGCPD_EINVAL,
+              "null pointer argument");
+    LSG_CHECK(aligned16(d_target) && aligned16(d_ws), LSGCPD_EINVAL, "d_target and d_ws must be 16-byte aligned");
+    LSG_CHECK(M >= 1 && N_local >= 1 && M < (int64_t)1 << 30 && N_local < (int64_t)1 << 34, LSGCPD_EINVAL,
+              "M=%lld N_local=%lld out of range", (long long)M, (long long)N_local);
+    LSG_CHECK(isfinite(p.w) && p.w >= 0.0 && p.w < 1.0, LSGCPD_EINVAL, "w must be in [0, 1)");
+    LSG_CHECK(p.max_iters >= 0 && p.max_iters <= 100000, LSGCPD_EINVAL, "max_iters out of range");
+    LSG_CHECK(p.newton_max >= 0 && p.newton_max <= 1000, LSGCPD_EINVAL, "newton_max out of range");
+    LSG_CHECK(isfinite(p.sigma2_floor_rel) && p.sigma2_floor_rel >= 0.0, LSGCPD_EINVAL, "bad sigma2_floor_rel");
+    LSG_CHECK(isfinite(p.sigma2_init) && isfinite(p.tol), LSGCPD_EINVAL, "sigma2_init and tol must be finite");
+    double Rid[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, tid[3] = {0, 0, 0};
+    const double* R = R0 ? R0 : Rid;
+    const double* t = t0 ? t0 : tid;
+    LSG_CHECK(is_rotation(R), LSGCPD_EINVAL, "R0 is not a rotation matrix (to 1e-6)");
+    LSG_CHECK(finite_vec(t, 3), LSGCPD_EINVAL, "t0 must be finite");
+    cudaStream_t s = (cudaStream_t)stream;
+    TargetHeader h;
+    int rc = read_header(d_target, M, &h, s);
+    if (rc) return rc;
+    const double V = volume > 0.0 ? volume : h.volume;
+    LSG_CHECK(isfinite(V) && V > 0.0, LSGCPD_EINVAL, "volume must be finite and > 0");
+    RegLayout L;
+    Sched sc;
+    rc = reg_layout(h.M_pad, N_local, p.max_iters, &L, &sc);
+    if (rc) return rc;
+    LSG_CHECK(ws_bytes >= L.total, LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
+    Comm* c = static_cast<Comm*>(comm);
+    if (c) {
+        rc = nccl_load();
+        if (rc) return rc;
+    }
+
+    char* ws = static_cast<char*>(d_ws);
+    IterState* st = reinterpret_cast<IterState*>(ws + L.state);
+    double* mom = reinterpret_cast<double*>(ws + L.mom);
+    double* sums = reinterpret_cast<double*>(ws + L.sums);
+    RegParams rp;
+    rp.w = p.w;
+    rp.V = V;
+    rp.floor = p.sigma2_floor_rel * h.extent * h.extent;
+    rp.tol = p.tol;
+    rp.omega_ref_target = h.omega_ref;
+    rp.M = M;
+    rp.newton_max = p.newton_max;
+    rp.consistent = p.consistent_normalizer ? 1 : 0;
+    rp.max_iters = p.max_iters;
+
+    LSG_CUDA(cudaMemsetAsync(ws + L.counters, 0, sizeof(unsigned) * 8, s));
+    LSG_CUDA(cudaMemsetAsync(ws + L.iters, 0, sizeof(int) * 4, s));
+    LSG_CUDA(cudaMemsetAsync(ws + L.nll, 0, sizeof(double) * (p.max_iters + 1), s));
+    LSG_CUDA(cudaMemsetAsync(ws + L.sig2, 0, sizeof(double) * (p.max_iters + 2), s));
+    // initial pose, then σ²₀ (CPD closed form over all ranks' points)
+    estep_launch_setup(st, d_target, R, t, 1.0, p.w, V, M, rp.consistent, s);
+    sigma2_sums_launch(d_src_local, N_local, st, d_target, reinterpret_cast<double*>(ws + L.blockpart), sums,
+                       reinterpret_cast<unsigned*>(ws + L.counters), s);
+    if (c) {
+        const ncclResult_t r = g_nccl.AllReduce(sums, sums, 2, kNcclFloat64, kNcclSum, c->nc, s);
+        if (r != 0) return nccl_fail(r, "ncclAllReduce(sigma2 sums)");
+    }
+    sigma2_init_launch(st, d_target, sums, rp, p.sigma2_init, reinterpret_cast<double*>(ws + L.sig2), mom + 75, s);
+    LSG_CUDA(cudaGetLastError());
+
+    // EM iterations: captured once into a CUDA graph and replayed (no host sync per iteration)
+    const char* env = getenv("LSGCPD_NO_GRAPH");
+    const bool use_graph = p.max_iters > 1 && !(env && env[0] == '1');
+    if (use_graph) {
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        cudaStream_t cs;
+        LSG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaEvent_t ev;
+        LSG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        LSG_CUDA(cudaEventRecord(ev, s));
+        LSG_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+        LSG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        rc = enqueue_iteration(d_target, d_src_local, N_local, ws, L, sc, rp, c, cs);
+        cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        if (rc) return rc;
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+        LSG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        for (int k = 0; k < p.max_iters; ++k) LSG_CUDA(cudaGraphLaunch(exec, cs));
+        LSG_CUDA(cudaEventRecord(ev, cs));
+        LSG_CUDA(cudaStreamWaitEvent(s, ev, 0));
+        LSG_CUDA(cudaStreamSynchronize(s));
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+        cudaEventDestroy(ev);
+        cudaStreamDestroy(cs);
+    } else {
+        for (int k = 0; k < p.max_iters; ++k) {
+            rc = enqueue_iteration(d_target, d_src_local, N_local, ws, L, sc, rp, c, s);
+            if (rc) return rc;
+        }
+        LSG_CUDA(cudaGetLastError());
+    }
+
+    IterState fin;
+    int iters = 0;
+    LSG_CUDA(cudaMemcpyAsync(&fin, st, sizeof(fin), cudaMemcpyDeviceToHost, s));
+    LSG_CUDA(cudaMemcpyAsync(&iters, ws + L.iters, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (nll_trace && p.max_iters > 0)
+        LSG_CUDA(cudaMemcpyAsync(nll_trace, ws + L.nll, sizeof(double) * p.max_iters, cudaMemcpyDeviceToHost, s));
+    if (sigma2_trace)
+        LSG_CUDA(cudaMemcpyAsync(sigma2_trace, ws + L.sig2, sizeof(double) * (p.max_iters + 1), cudaMemcpyDeviceToHost,
+                                 s));
+    LSG_CUDA(cudaStreamSynchronize(s));
+    LSG_CUDA(cudaGetLastError());
+    for (int i = 0; i < 9; ++i) R_out[i] = fin.R[i];
+    for (int i = 0; i < 3; ++i) t_out[i] = fin.t[i];
+    *sigma2_out = fin.sigma2;
+    *iters_out = iters;
+    if (fin.status == LSGCPD_ENOMASS) {
+        set_error("no inlier mass (sum P <= 1e-12 N) for 3 consecutive iterations");
+        return LSGCPD_ENOMASS;
+    }
+    return 0;
+}

@@ -1,0 +1,176 @@
+// Shared definitions for the LSG-CPD sm_100a library (product path; no oracle code).
+// Paper citations: P:<line> of arXiv 2103.15039's LaTeX source.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/lsgcpd.h"
+
+namespace lsg {
+
+// ------------------------------------------------------------------------------------------
+// Error reporting (thread-local message, C ABI codes)
+// ------------------------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define LSG_CUDA(call)                                               \
+    do {                                                             \
+        cudaError_t _e = (call);                                     \
+        if (_e != cudaSuccess) return ::lsg::cuda_fail(_e, #call);   \
+    } while (0)
+
+#define LSG_CHECK(cond, code, ...)                                   \
+    do {                                                             \
+        if (!(cond)) {                                               \
+            ::lsg::set_error(__VA_ARGS__);                           \
+            return (code);                                           \
+        }                                                            \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------
+// Prepared target: header + per-target 16-float record (64 B), padded to a tile multiple.
+//   f[0..3]   y_x, y_y, y_z, ω̄_m = ½log2(1+α_m) - ω_ref   (log-determinant weight, ≤ 0)
+//   f[4..7]   ñ_x, ñ_y, ñ_z (ñ = √α n), W_xx          (W = α n nᵀ)
+//   f[8..11]  W_xy, W_xz, W_yy, W_yz
+//   f[12..15] W_zz, b_x, b_y, b_z                      (b = α (n·y) n)
+// Padding targets have ω̄ = -inf (zero weight) and zero geometry.
+// ------------------------------------------------------------------------------------------
+constexpr int kTgtFloats = 16;
+constexpr int kTgtPadMultiple = 256;
+constexpr size_t kHeaderBytes = 256;
+
+struct TargetHeader {
+    int64_t M, M_pad;
+    double omega_ref;        // max_m ½log2(1+α_m)
+    double volume, extent;
+    double aabb_lo[3], aabb_hi[3];
+    double ybar[3];          // centroid
+    double syy;              // Σ_m ||y_m - ȳ||²
+    double alpha_sum;
+    int64_t n_degenerate;
+    uint32_t magic;
+    uint32_t pad_[3];
+};
+static_assert(sizeof(TargetHeader) <= kHeaderBytes, "header too big");
+constexpr uint32_t kTargetMagic = 0x4c534743u;  // "LSGC"
+
+inline int64_t pad_targets(int64_t M) { return (M + kTgtPadMultiple - 1) / kTgtPadMultiple * kTgtPadMultiple; }
+inline const float* target_body(const void* t) { return reinterpret_cast<const float*>(static_cast<const char*>(t) + kHeaderBytes); }
+inline float* target_body(void* t) { return reinterpret_cast<float*>(static_cast<char*>(t) + kHeaderBytes); }
+
+// ------------------------------------------------------------------------------------------
+// Per-E-step constants, computed in FP64 on the device (setup kernel or the Newton kernel),
+// read by the E-step kernels.  See DESIGN.md "E-step arithmetic".
+//   l̄_mn = ω̄_m - k2 τ_mn,  τ = ||r||² + (ñ·r)²,  k2 = log2(e)/(2σ²)      (base-2 log weights)
+//   outlier log2 weight relative to ω_ref:  Lo = log2(w/V) - C1/ln2 - ω_ref
+//   C1 = ln((1-w)/M) - 1.5 ln(2πσ²);  ln p(x̂) = C1 + ln2 (ω_ref + μ + log2 Σ 2^{l̄-μ})
+// fixed = 1 when Lo ≥ -50 (w > 0): then the constant max μ ≡ 0 is safe (all l̄ ≤ 0).
+// ------------------------------------------------------------------------------------------
+struct IterState {
+    double R[9], t[3];       // E-step pose g_old
+    double sigma2;
+    double w, volume;
+    double C1;
+    double omega_ref;        // 0 in the Eq. 9-10 literal mode
+    double Lo;               // -inf when w == 0
+    double extent;
+    float k2;
+    int fixed;
+    int active;              // 0: EM finished (kernels return immediately)
+    int iter;                // EM iteration index of this E step
+    int status;              // 0 or LSGCPD_ENOMASS
+    int no_mass;             // consecutive iterations with Σ P ≈ 0
+    double last_step_rot, last_step_trans;
+};
+
+__host__ __device__ inline void make_state(IterState& s, const double* R, const double* t, double sigma2, double w,
+                                           double V, int64_t M, double omega_ref_target, int consistent) {
+    for (int i = 0; i < 9; ++i) s.R[i] = R[i];
+    for (int i = 0; i < 3; ++i) s.t[i] = t[i];
+    s.sigma2 = sigma2;
+    s.w = w;
+    s.volume = V;
+    const double ln2 = 0.69314718055994530942;
+    s.omega_ref = consistent ? omega_ref_target : 0.0;
+    s.C1 = log((1.0 - w) / (double)M) - 1.5 * log(2.0 * 3.14159265358979323846 * sigma2);
+    if (w > 0.0) {
+        s.Lo = (log(w / V) - s.C1) / ln2 - s.omega_ref;
+    } else {
+        s.Lo = -INFINITY;
+    }
+    s.k2 = (float)(1.4426950408889634074 / (2.0 * sigma2));
+    s.fixed = (w > 0.0 && s.Lo >= -50.0) ? 1 : 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// Device helpers
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Deterministic grid reduction: entries [0, KMAX) by max, [KMAX, K) by sum.  Each block writes a
+// partial; the last block to finish (atomic ticket) combines the partials in block order and
+// writes `out`, then re-arms the counter.  blockDim.x must equal NT.
+template <int K, int KMAX, int NT>
+__device__ void block_reduce_store(double (&v)[K], double* blockpart, double* out, unsigned int* counter) {
+    __shared__ double sm[NT / 32][K];
+    __shared__ bool last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int f = 0; f < K; ++f) {
+        const double s = f < KMAX ? warp_max(v[f]) : warp_sum(v[f]);
+        if (lane == 0) sm[warp][f] = s;
+    }
+    __syncthreads();
+    for (int f = threadIdx.x; f < K; f += NT) {
+        double s = sm[0][f];
+        for (int w = 1; w < NT / 32; ++w) s = f < KMAX ? fmax(s, sm[w][f]) : s + sm[w][f];
+        blockpart[(int64_t)blockIdx.x * K + f] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        for (int f = threadIdx.x; f < K; f += NT) {
+            const volatile double* bp = blockpart;
+            double s = bp[f];
+            for (unsigned b = 1; b < gridDim.x; ++b) s = f < KMAX ? fmax(s, bp[(int64_t)b * K + f]) : s + bp[(int64_t)b * K + f];
+            out[f] = s;
+        }
+        if (threadIdx.x == 0) *counter = 0u;
+    }
+}
+
+// E-step stream-K schedule: units = (source block j, target tile i), u = j*T + i.
+// CTA g owns units [start(g), start(g+1)), start(g) = floor(g U / G).
+struct Sched {
+    int64_t U;        // total units
+    int64_t T;        // tiles per source block
+    int64_t G;        // CTAs
+    int64_t nblk;     // source blocks
+    int64_t kmax;     // max CTAs touching one source block (partial slots per block)
+};
+__host__ __device__ inline int64_t sched_start(const Sched& s, int64_t g) { return g * s.U / s.G; }
+__host__ __device__ inline int64_t sched_owner(const Sched& s, int64_t u) { return ((u + 1) * s.G - 1) / s.U; }
+
+}  // namespace lsg

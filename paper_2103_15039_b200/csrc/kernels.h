@@ -1,0 +1,43 @@
+// Host-side launchers shared between the translation units of liblsgcpd.so.
+#pragma once
+#include "common.cuh"
+
+namespace lsg {
+
+// Registration parameters passed by value to the device-side EM state machine.
+struct RegParams {
+    double w, V, floor, tol, omega_ref_target;
+    int64_t M;
+    int newton_max, consistent, max_iters;
+};
+
+// estep.cu
+int estep_plan(int64_t M_pad, int64_t N, Sched* sc);
+size_t estep_partial_bytes(const Sched& s);
+size_t estep_partial_bytes_bound(int64_t M_pad, int64_t N, int64_t max_ctas);
+void estep_launch_setup(IterState* st, const void* d_target, const double* R, const double* t, double sigma2,
+                        double w, double V, int64_t M, int consistent, cudaStream_t stream);
+void estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
+                  float* part, float* rec, int consistent, cudaStream_t stream);
+
+// mstep.cu
+constexpr int kMomentCount = 75;          // G 60, U 12, σ²ΣD, ΣP, Σ ln p
+constexpr int kMomentBlocks = 256;
+void moments_launch(const float* rec, const float* src, int64_t N, const IterState* st, double* blockpart,
+                    double* out, unsigned int* counter, cudaStream_t stream);
+void sigma2_sums_launch(const float* src, int64_t N, const IterState* st, const void* d_target, double* blockpart,
+                        double* out, unsigned int* counter, cudaStream_t stream);
+void sigma2_init_launch(IterState* st, const void* d_target, const double* sums, const RegParams& rp,
+                        double sigma2_user, double* sigma2_trace, double* ntot_out, cudaStream_t stream);
+void newton_launch(IterState* st, const double* mom, const RegParams& rp, double* nll_trace, double* sigma2_trace,
+                   int* iters_done, cudaStream_t stream);
+
+// target.cu
+size_t prepare_ws_bytes(int64_t M);
+size_t pack_ws_bytes(int64_t M);
+int pack_target_impl(const float* d_xyz, const float* d_nrm, const float* d_alpha, int64_t M, double margin,
+                     void* d_target, void* d_ws, lsgcpd_target_info* info, cudaStream_t stream);
+int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p, void* d_target, void* d_ws,
+                        lsgcpd_target_info* info, const lsgcpd_annotations* ann, cudaStream_t stream);
+
+}  // namespace lsg

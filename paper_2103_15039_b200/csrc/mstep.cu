@@ -1,0 +1,391 @@
+// LSG-CPD M step for sm_100a: per-point FP64 moments (K3), damped SE(3) Newton + σ² (K4),
+// and the σ²₀ reduction.
+//
+// Moment form of the frozen-P objective: with H_n = P_n I + A_n,
+// g_n = Σ_m P_mn y_m + b_n, u_n = H_n x̂_n - g_n and x̃_n = (x_n, 1), for any pose Θ' = [R'|t']
+//   q(Θ') = σ² Σ_n D_n + 2⟨ΔΘ, U⟩ + Σ ΔΘ_ia ΔΘ_jb G_{ij,ab},   ΔΘ = Θ' - Θ_E,
+//   U = Σ_n u_n x̃_nᵀ (12 numbers),  G = Σ_n H_n ⊗ x̃_n x̃_nᵀ (6 × 10 unique numbers).
+// 75 FP64 numbers (G 60, U 12, σ²ΣD, ΣP, Σ ln p) determine every Newton iterate and σ²_new, so one
+// all-reduce per EM iteration suffices across GPUs.  K4 differentiates q(Θ̃ exp(ξ^)) by the chain
+// rule (right derivatives, Eq. 11-12) and takes damped Newton steps (Eq. 13 P:337-339,
+// readings R11-R13).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lsg {
+
+constexpr int kMom = 75;
+constexpr int kMomBlocks = 256;   // fixed grid: the reduction order does not depend on the device
+constexpr int kMomThreads = 128;
+
+__device__ __forceinline__ int s3(int i, int j) {  // symmetric 3×3 index
+    if (i > j) { int t = i; i = j; j = t; }
+    return i == 0 ? j : (i == 1 ? 2 + j : 5);
+}
+__device__ __forceinline__ int s4(int a, int b) {  // symmetric 4×4 index
+    if (a > b) { int t = a; a = b; b = t; }
+    return a == 0 ? b : (a == 1 ? 3 + b : (a == 2 ? 5 + b : 9));
+}
+
+// K3: per-point moments from the E-step record.
+__global__ void __launch_bounds__(kMomThreads)
+    moments_kernel(const float* __restrict__ rec, const float* __restrict__ src, int64_t N,
+                   const IterState* __restrict__ st, double* blockpart, double* out, unsigned int* counter) {
+    if (!st->active) return;
+    double R[9], t[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = st->R[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) t[i] = st->t[i];
+    const double s2 = st->sigma2;
+    double m[kMom];
+#pragma unroll
+    for (int f = 0; f < kMom; ++f) m[f] = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += stride) {
+        const float4* r4 = reinterpret_cast<const float4*>(rec + n * LSGCPD_REC);
+        const float4 a0 = r4[0], a1 = r4[1], a2 = r4[2], a3 = r4[3];
+        const double P = a0.x;
+        const double H[6] = {P + (double)a1.x, (double)a1.y, (double)a1.z, P + (double)a1.w, (double)a2.x,
+                             P + (double)a2.y};
+        const double gv[3] = {(double)a0.y + (double)a2.z, (double)a0.z + (double)a2.w, (double)a0.w + (double)a3.x};
+        const double x[4] = {(double)src[3 * n], (double)src[3 * n + 1], (double)src[3 * n + 2], 1.0};
+        double xh[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) xh[i] = fma(R[3 * i], x[0], fma(R[3 * i + 1], x[1], fma(R[3 * i + 2], x[2], t[i])));
+        double u[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            u[i] = H[s3(i, 0)] * xh[0] + H[s3(i, 1)] * xh[1] + H[s3(i, 2)] * xh[2] - gv[i];
+        // G_{ij,ab} += H_ij x̃_a x̃_b
+        double xx[10];
+        int k = 0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = a; b < 4; ++b) xx[k++] = x[a] * x[b];
+#pragma unroll
+        for (int ij = 0; ij < 6; ++ij)
+#pragma unroll
+            for (int ab = 0; ab < 10; ++ab) m[ij * 10 + ab] = fma(H[ij], xx[ab], m[ij * 10 + ab]);
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int a = 0; a < 4; ++a) m[60 + 4 * i + a] = fma(u[i], x[a], m[60 + 4 * i + a]);
+        m[72] = fma(s2, (double)a3.y, m[72]);
+        m[73] += P;
+        m[74] += (double)a3.z;
+    }
+    block_reduce_store<kMom, 0, kMomThreads>(m, blockpart, out, counter);
+}
+
+// σ²₀ partial sums: [Σ_n ||x̂_n - ȳ||², N_local]  (x̂ at the initial pose in st).
+__global__ void __launch_bounds__(kMomThreads)
+    sigma2_sums_kernel(const float* __restrict__ src, int64_t N, const IterState* __restrict__ st,
+                       const TargetHeader* __restrict__ hdr, double* blockpart, double* out, unsigned int* counter) {
+    double R[9], t[3], yb[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = st->R[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) { t[i] = st->t[i]; yb[i] = hdr->ybar[i]; }
+    double v[2] = {0.0, 0.0};
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += stride) {
+        const double x0 = src[3 * n], x1 = src[3 * n + 1], x2 = src[3 * n + 2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double d = fma(R[3 * i], x0, fma(R[3 * i + 1], x1, fma(R[3 * i + 2], x2, t[i]))) - yb[i];
+            v[0] = fma(d, d, v[0]);
+        }
+        v[1] += 1.0;
+    }
+    block_reduce_store<2, 0, kMomThreads>(v, blockpart, out, counter);
+}
+
+// σ²₀ (CPD closed form, exact): (M Σ_n||x̂_n-ȳ||² + N Σ_m||y_m-ȳ||²)/(3MN); sets up iteration 0.
+__global__ void sigma2_init_kernel(IterState* st, const TargetHeader* hdr, const double* sums, RegParams rp,
+                                   double sigma2_user, double* sigma2_trace, double* ntot_out) {
+    IterState s = *st;
+    const double N = sums[1];
+    double s2 = sigma2_user;
+    if (!(s2 > 0.0)) s2 = ((double)rp.M * sums[0] + N * hdr->syy) / (3.0 * (double)rp.M * N);
+    const double floor = rp.floor;
+    if (s2 < floor) s2 = floor;
+    make_state(s, s.R, s.t, s2, rp.w, rp.V, rp.M, rp.omega_ref_target, rp.consistent);
+    s.extent = hdr->extent;
+    s.active = 1;
+    s.iter = 0;
+    s.status = 0;
+    s.no_mass = 0;
+    s.last_step_rot = s.last_step_trans = 0.0;
+    *st = s;
+    sigma2_trace[0] = s2;
+    *ntot_out = N;
+}
+
+// ---------------------------------------------------------------------------------------------
+// K4: Newton on SE(3) from the moments (single thread, FP64).
+// ---------------------------------------------------------------------------------------------
+struct Mom {
+    double GG[12][12];   // 𝔾 over θ = vec(Θ) (row-major Θ: θ[4i+a] = Θ_ia)
+    double U[12];
+};
+
+__device__ inline void build_mom(Mom& mo, const double* m) {
+    for (int i = 0; i < 3; ++i)
+        for (int a = 0; a < 4; ++a) {
+            mo.U[4 * i + a] = m[60 + 4 * i + a];
+            for (int j = 0; j < 3; ++j)
+                for (int b = 0; b < 4; ++b) mo.GG[4 * i + a][4 * j + b] = m[s3(i, j) * 10 + s4(a, b)];
+        }
+}
+
+// q(Θ') - q(Θ_E) = 2 Δθ·U + Δθᵀ𝔾Δθ
+__device__ inline double q_rel(const Mom& mo, const double* dth) {
+    double q = 0.0;
+    for (int r = 0; r < 12; ++r) {
+        double gr = 0.0;
+        for (int c = 0; c < 12; ++c) gr = fma(mo.GG[r][c], dth[c], gr);
+        q = fma(dth[r], 2.0 * mo.U[r] + gr, q);
+    }
+    return q;
+}
+
+__device__ inline void theta_of(const double* R, const double* t, double* th) {
+    for (int i = 0; i < 3; ++i) {
+        for (int a = 0; a < 3; ++a) th[4 * i + a] = R[3 * i + a];
+        th[4 * i + 3] = t[i];
+    }
+}
+
+// se(3) basis E_k (4×4, row-major): k = 0..2 rotations about x, y, z; 3..5 translations.
+__device__ inline void basis4(int k, double* E) {
+    for (int i = 0; i < 16; ++i) E[i] = 0.0;
+    if (k == 0) { E[1 * 4 + 2] = -1.0; E[2 * 4 + 1] = 1.0; }
+    else if (k == 1) { E[0 * 4 + 2] = 1.0; E[2 * 4 + 0] = -1.0; }
+    else if (k == 2) { E[0 * 4 + 1] = -1.0; E[1 * 4 + 0] = 1.0; }
+    else E[(k - 3) * 4 + 3] = 1.0;
+}
+
+__device__ inline void mat4mul(const double* A, const double* B, double* C) {
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 4; ++k) s = fma(A[i * 4 + k], B[k * 4 + j], s);
+            C[i * 4 + j] = s;
+        }
+}
+
+// exp of a twist δ = (ω, v): rotation (Rodrigues) and V·v; series for small |ω|.
+__device__ inline void se3_exp(const double* d, double* dR, double* dt) {
+    const double wx = d[0], wy = d[1], wz = d[2];
+    const double th2 = wx * wx + wy * wy + wz * wz;
+    double A, B, C;
+    if (th2 < 1e-8) {
+        A = 1.0 - th2 / 6.0 + th2 * th2 / 120.0;
+        B = 0.5 - th2 / 24.0 + th2 * th2 / 720.0;
+        C = 1.0 / 6.0 - th2 / 120.0 + th2 * th2 / 5040.0;
+    } else {
+        const double th = sqrt(th2);
+        A = sin(th) / th;
+        B = (1.0 - cos(th)) / th2;
+        C = (th - sin(th)) / (th2 * th);
+    }
+    const double K[9] = {0.0, -wz, wy, wz, 0.0, -wx, -wy, wx, 0.0};
+    double K2[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) K2[3 * i + j] = K[3 * i] * K[j] + K[3 * i + 1] * K[3 + j] + K[3 * i + 2] * K[6 + j];
+    double Vm[9];
+    for (int i = 0; i < 9; ++i) {
+        const double I = (i % 4 == 0) ? 1.0 : 0.0;
+        dR[i] = I + A * K[i] + B * K2[i];
+        Vm[i] = I + B * K[i] + C * K2[i];
+    }
+    for (int i = 0; i < 3; ++i) dt[i] = Vm[3 * i] * d[3] + Vm[3 * i + 1] * d[4] + Vm[3 * i + 2] * d[5];
+}
+
+// Cholesky solve (A + μI) x = b, 6×6.  Returns false if not positive definite.
+__device__ inline bool chol_solve6(const double* A, double mu, const double* b, double* x) {
+    double L[36];
+    for (int i = 0; i < 36; ++i) L[i] = 0.0;
+    for (int j = 0; j < 6; ++j) {
+        double s = A[j * 6 + j] + mu;
+        for (int k = 0; k < j; ++k) s -= L[j * 6 + k] * L[j * 6 + k];
+        if (!(s > 0.0)) return false;
+        const double d = sqrt(s);
+        L[j * 6 + j] = d;
+        for (int i = j + 1; i < 6; ++i) {
+            double v = A[i * 6 + j];
+            for (int k = 0; k < j; ++k) v -= L[i * 6 + k] * L[j * 6 + k];
+            L[i * 6 + j] = v / d;
+        }
+    }
+    double y[6];
+    for (int i = 0; i < 6; ++i) {
+        double v = b[i];
+        for (int k = 0; k < i; ++k) v -= L[i * 6 + k] * y[k];
+        y[i] = v / L[i * 6 + i];
+    }
+    for (int i = 5; i >= 0; --i) {
+        double v = y[i];
+        for (int k = i + 1; k < 6; ++k) v -= L[k * 6 + i] * x[k];
+        x[i] = v / L[i * 6 + i];
+    }
+    return true;
+}
+
+__global__ void newton_kernel(IterState* st, const double* __restrict__ mom, RegParams rp, double* nll_trace,
+                              double* sigma2_trace, int* iters_done) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    IterState s = *st;
+    if (!s.active) return;
+    __shared__ Mom mo;
+    build_mom(mo, mom);
+    const double sig2D = mom[72], sumP = mom[73], sumlnp = mom[74];
+    const double ntot = mom[75];  // total source points (appended by the host-side layout)
+    double th_E[12];
+    theta_of(s.R, s.t, th_E);
+    double R[9], t[3];
+    for (int i = 0; i < 9; ++i) R[i] = s.R[i];
+    for (int i = 0; i < 3; ++i) t[i] = s.t[i];
+    double q_cur = 0.0;
+    double E[6][16];
+    for (int k = 0; k < 6; ++k) basis4(k, E[k]);
+    double step_rot = 0.0, step_trans = 0.0;
+
+    for (int itn = 0; itn < rp.newton_max; ++itn) {
+        double th[12], dth[12], v[12];
+        theta_of(R, t, th);
+        for (int r = 0; r < 12; ++r) dth[r] = th[r] - th_E[r];
+        for (int r = 0; r < 12; ++r) {
+            double gr = 0.0;
+            for (int c = 0; c < 12; ++c) gr = fma(mo.GG[r][c], dth[c], gr);
+            v[r] = mo.U[r] + gr;                       // ½ ∇_θ q
+        }
+        double Gt[16] = {R[0], R[1], R[2], t[0], R[3], R[4], R[5], t[1], R[6], R[7], R[8], t[2], 0, 0, 0, 1};
+        double J[6][12];                               // dθ/dξ_k = (Θ̃ E_k)[0:3,:]
+        for (int k = 0; k < 6; ++k) {
+            double P4[16];
+            mat4mul(Gt, E[k], P4);
+            for (int r = 0; r < 12; ++r) J[k][r] = P4[r];
+        }
+        double grad[6], H[36];
+        double GJ[6][12];
+        for (int k = 0; k < 6; ++k) {
+            double g = 0.0;
+            for (int r = 0; r < 12; ++r) g = fma(J[k][r], v[r], g);
+            grad[k] = g;
+            for (int r = 0; r < 12; ++r) {
+                double a = 0.0;
+                for (int c = 0; c < 12; ++c) a = fma(mo.GG[r][c], J[k][c], a);
+                GJ[k][r] = a;
+            }
+        }
+        for (int k = 0; k < 6; ++k)
+            for (int l = k; l < 6; ++l) {
+                double h = 0.0;
+                for (int r = 0; r < 12; ++r) h = fma(J[k][r], GJ[l][r], h);
+                // second-order term: v · (Θ̃ ½(E_k E_l + E_l E_k))[0:3,:]
+                double EE1[16], EE2[16], S4[16], P4[16];
+                mat4mul(E[k], E[l], EE1);
+                mat4mul(E[l], E[k], EE2);
+                for (int i = 0; i < 16; ++i) S4[i] = 0.5 * (EE1[i] + EE2[i]);
+                mat4mul(Gt, S4, P4);
+                for (int r = 0; r < 12; ++r) h = fma(v[r], P4[r], h);
+                H[k * 6 + l] = h;
+                H[l * 6 + k] = h;
+            }
+        double tr = fabs(H[0] + H[7] + H[14] + H[21] + H[28] + H[35]) / 6.0;
+        double mu = 0.0;
+        bool accepted = false, converged = false;
+        for (int tries = 0; tries < 20; ++tries) {
+            double delta[6], mg[6];
+            for (int k = 0; k < 6; ++k) mg[k] = -grad[k];
+            if (!chol_solve6(H, mu, mg, delta)) {
+                mu = fmax(10.0 * mu, 1e-6 * tr);
+                continue;
+            }
+            const double nr = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]);
+            const double nt = sqrt(delta[3] * delta[3] + delta[4] * delta[4] + delta[5] * delta[5]);
+            if (nr < 1e-10 && nt < 1e-10 * s.extent) {
+                converged = true;
+                break;
+            }
+            double dR[9], dt[3], Rn[9], tn[3];
+            se3_exp(delta, dR, dt);
+            for (int i = 0; i < 3; ++i) {
+                for (int j = 0; j < 3; ++j)
+                    Rn[3 * i + j] = R[3 * i] * dR[j] + R[3 * i + 1] * dR[3 + j] + R[3 * i + 2] * dR[6 + j];
+                tn[i] = R[3 * i] * dt[0] + R[3 * i + 1] * dt[1] + R[3 * i + 2] * dt[2] + t[i];
+            }
+            double thn[12], dthn[12];
+            theta_of(Rn, tn, thn);
+            for (int r = 0; r < 12; ++r) dthn[r] = thn[r] - th_E[r];
+            const double qn = q_rel(mo, dthn);
+            if (qn < q_cur) {
+                for (int i = 0; i < 9; ++i) R[i] = Rn[i];
+                for (int i = 0; i < 3; ++i) t[i] = tn[i];
+                q_cur = qn;
+                accepted = true;
+                step_rot += nr;
+                step_trans += nt;
+                break;
+            }
+            mu = fmax(10.0 * mu, 1e-6 * tr);
+        }
+        if (converged || !accepted) break;
+    }
+
+    // σ² at the new pose: q(g_new) / (3 Σ P), floored; unchanged without mass.
+    const int k = s.iter;
+    nll_trace[k] = -sumlnp;
+    double s2 = s.sigma2;
+    const bool has_mass = sumP > 1e-12 * ntot;
+    if (has_mass) {
+        s2 = (sig2D + q_cur) / (3.0 * sumP);
+        if (!(s2 >= rp.floor)) s2 = rp.floor;
+    }
+    const double s2_old = s.sigma2;
+    IterState nx = s;
+    make_state(nx, R, t, s2, rp.w, rp.V, rp.M, rp.omega_ref_target, rp.consistent);
+    nx.extent = s.extent;
+    nx.iter = k + 1;
+    nx.no_mass = has_mass ? 0 : s.no_mass + 1;
+    nx.status = s.status;
+    nx.active = 1;
+    nx.last_step_rot = step_rot;
+    nx.last_step_trans = step_trans;
+    if (nx.no_mass >= 3) {
+        nx.status = LSGCPD_ENOMASS;
+        nx.active = 0;
+    }
+    if (rp.tol > 0.0 && fabs(s2 - s2_old) <= rp.tol * s2_old && step_rot <= rp.tol && step_trans <= rp.tol * s.extent)
+        nx.active = 0;
+    if (nx.iter >= rp.max_iters) nx.active = 0;
+    sigma2_trace[k + 1] = s2;
+    *iters_done = k + 1;
+    *st = nx;
+}
+
+// ---- host launchers ----------------------------------------------------------------------------
+void moments_launch(const float* rec, const float* src, int64_t N, const IterState* st, double* blockpart,
+                    double* out, unsigned int* counter, cudaStream_t stream) {
+    moments_kernel<<<kMomBlocks, kMomThreads, 0, stream>>>(rec, src, N, st, blockpart, out, counter);
+}
+void sigma2_sums_launch(const float* src, int64_t N, const IterState* st, const void* d_target, double* blockpart,
+                        double* out, unsigned int* counter, cudaStream_t stream) {
+    sigma2_sums_kernel<<<kMomBlocks, kMomThreads, 0, stream>>>(src, N, st,
+                                                               reinterpret_cast<const TargetHeader*>(d_target),
+                                                               blockpart, out, counter);
+}
+void sigma2_init_launch(IterState* st, const void* d_target, const double* sums, const RegParams& rp,
+                        double sigma2_user, double* sigma2_trace, double* ntot_out, cudaStream_t stream) {
+    sigma2_init_kernel<<<1, 1, 0, stream>>>(st, reinterpret_cast<const TargetHeader*>(d_target), sums, rp,
+                                             sigma2_user, sigma2_trace, ntot_out);
+}
+void newton_launch(IterState* st, const double* mom, const RegParams& rp, double* nll_trace, double* sigma2_trace,
+                   int* iters_done, cudaStream_t stream) {
+    newton_kernel<<<1, 32, 0, stream>>>(st, mom, rp, nll_trace, sigma2_trace, iters_done);
+}
+
+}  // namespace lsg

@@ -1,0 +1,449 @@
+// Target preparation for sm_100a: exact grid kNN (FP64 distances),
+// centred scatter, FP64 Jacobi eigen-decomposition → n_m, κ_m, α_m (Eq. 3), working volume V, and
+// the packed 64-B-per-target model the E step streams through TMA.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lsg {
+
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 148;
+constexpr int kMaxK = 32;
+
+// ---- reductions over the raw cloud -------------------------------------------------------------
+// stats1: [max(-x), max(-y), max(-z), max x, max y, max z, Σx, Σy, Σz]
+__global__ void __launch_bounds__(kRedThreads)
+    cloud_stats_kernel(const float* __restrict__ xyz, int64_t M, double* blockpart, double* out, unsigned* counter) {
+    double v[9] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0, 0.0, 0.0};
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double c = xyz[3 * m + a];
+            v[a] = fmax(v[a], -c);
+            v[3 + a] = fmax(v[3 + a], c);
+            v[6 + a] += c;
+        }
+    }
+    block_reduce_store<9, 6, kRedThreads>(v, blockpart, out, counter);
+}
+
+// stats2 (after the model is built): [max ω, Σ α, Σ ||y - ȳ||², Σ nn-distance, n_degenerate]
+__global__ void __launch_bounds__(kRedThreads)
+    model_stats_kernel(const float* __restrict__ xyz, const float* __restrict__ alpha, const float* __restrict__ nnd,
+                       const int* __restrict__ degen, int64_t M, const double* __restrict__ stats1, double* blockpart,
+                       double* out, unsigned* counter) {
+    double v[5] = {-INFINITY, 0.0, 0.0, 0.0, 0.0};
+    const double yb[3] = {stats1[6] / M, stats1[7] / M, stats1[8] / M};
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
+        const double a = alpha[m];
+        v[0] = fmax(v[0], 0.5 * log2(1.0 + a));
+        v[1] += a;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double d = (double)xyz[3 * m + i] - yb[i];
+            v[2] = fma(d, d, v[2]);
+        }
+        if (nnd) v[3] += nnd[m];
+        if (degen) v[4] += degen[m];
+    }
+    block_reduce_store<5, 1, kRedThreads>(v, blockpart, out, counter);
+}
+
+// Header: AABB, centroid, V (margin per side; a zero-extent axis is floored at the mean
+// nearest-neighbour spacing when known, else at sqrt(area/M) of the other two axes), extent.
+__global__ void header_kernel(TargetHeader* hdr, int64_t M, const double* stats1, const double* stats2,
+                              double margin, int have_nn) {
+    TargetHeader h;
+    h.M = M;
+    h.M_pad = ((M + kTgtPadMultiple - 1) / kTgtPadMultiple) * kTgtPadMultiple;
+    h.omega_ref = stats2[0];
+    double ext[3], e2 = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        h.aabb_lo[a] = -stats1[a];
+        h.aabb_hi[a] = stats1[3 + a];
+        ext[a] = h.aabb_hi[a] - h.aabb_lo[a];
+        e2 += ext[a] * ext[a];
+        h.ybar[a] = stats1[6 + a] / (double)M;
+    }
+    h.extent = sqrt(e2);
+    double floor_s;
+    if (have_nn) {
+        floor_s = stats2[3] / (double)M;
+    } else {
+        double area = 1.0;
+        int nz = 0;
+        for (int a = 0; a < 3; ++a)
+            if (ext[a] > 0.0) { area *= ext[a]; ++nz; }
+        floor_s = nz >= 2 ? sqrt(area / (double)M) : (nz == 1 ? area / (double)M : 1.0);
+    }
+    double V = 1.0;
+    for (int a = 0; a < 3; ++a) V *= (ext[a] > 0.0 ? ext[a] : floor_s) * (1.0 + 2.0 * margin);
+    h.volume = V;
+    h.syy = stats2[2];
+    h.alpha_sum = stats2[1];
+    h.n_degenerate = (int64_t)stats2[4];
+    h.magic = kTargetMagic;
+    h.pad_[0] = h.pad_[1] = h.pad_[2] = 0;
+    *hdr = h;
+}
+
+// Packed per-target record (FP64 arithmetic, FP32 storage); padding targets contribute nothing.
+__global__ void pack_body_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm,
+                                 const float* __restrict__ alpha, int64_t M, int64_t M_pad,
+                                 const double* __restrict__ stats2, float* __restrict__ body) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M_pad) return;
+    float4* o = reinterpret_cast<float4*>(body + m * kTgtFloats);
+    if (m >= M) {
+        // far away (τ overflows to a huge value → weight 0 in both normaliser modes) and ω̄ = -inf
+        o[0] = make_float4(1e18f, 1e18f, 1e18f, -INFINITY);
+        o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        o[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+        o[3] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    const double y0 = xyz[3 * m], y1 = xyz[3 * m + 1], y2 = xyz[3 * m + 2];
+    const double n0 = nrm[3 * m], n1 = nrm[3 * m + 1], n2 = nrm[3 * m + 2];
+    const double a = alpha[m];
+    const double sa = sqrt(a);
+    const double ny = n0 * y0 + n1 * y1 + n2 * y2;
+    const double om = 0.5 * log2(1.0 + a) - stats2[0];
+    o[0] = make_float4((float)y0, (float)y1, (float)y2, (float)om);
+    o[1] = make_float4((float)(sa * n0), (float)(sa * n1), (float)(sa * n2), (float)(a * n0 * n0));
+    o[2] = make_float4((float)(a * n0 * n1), (float)(a * n0 * n2), (float)(a * n1 * n1), (float)(a * n1 * n2));
+    o[3] = make_float4((float)(a * n2 * n2), (float)(a * ny * n0), (float)(a * ny * n1), (float)(a * ny * n2));
+}
+
+// ---- grid kNN ------------------------------------------------------------------------------------
+struct Grid {
+    double lo[3];
+    double h;
+    int dim[3];
+};
+
+__device__ __forceinline__ int cell_coord(double p, double lo, double h, int dim) {
+    int c = (int)floor((p - lo) / h);
+    return c < 0 ? 0 : (c >= dim ? dim - 1 : c);
+}
+
+__global__ void cell_keys_kernel(const float* __restrict__ xyz, int64_t M, Grid g, int* keys, int* ids) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    const int cx = cell_coord(xyz[3 * m], g.lo[0], g.h, g.dim[0]);
+    const int cy = cell_coord(xyz[3 * m + 1], g.lo[1], g.h, g.dim[1]);
+    const int cz = cell_coord(xyz[3 * m + 2], g.lo[2], g.h, g.dim[2]);
+    keys[m] = (cx * g.dim[1] + cy) * g.dim[2] + cz;
+    ids[m] = (int)m;
+}
+
+__global__ void cell_ranges_kernel(const int* __restrict__ skeys, int64_t M, int* cstart, int* cend) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int k = skeys[i];
+    if (i == 0 || skeys[i - 1] != k) cstart[k] = (int)i;
+    if (i == M - 1 || skeys[i + 1] != k) cend[k] = (int)i + 1;
+}
+
+// One thread per target point: exact k nearest (self included), ties → lower id, by ring search
+// over grid cells until the k-th distance is below the distance to the unsearched region.
+// Then the centred scatter, a cyclic Jacobi eigen-solve (FP64) and α (Eq. 3, tanh form).
+__device__ inline void jacobi3(double A[3][3], double V[3][3]) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) V[i][j] = (i == j) ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 16; ++sweep) {
+        const double off = A[0][1] * A[0][1] + A[0][2] * A[0][2] + A[1][2] * A[1][2];
+        const double dia = A[0][0] * A[0][0] + A[1][1] * A[1][1] + A[2][2] * A[2][2];
+        if (!(off > 1e-36 * dia) ) break;
+        for (int p = 0; p < 2; ++p)
+            for (int q = p + 1; q < 3; ++q) {
+                const double apq = A[p][q];
+                if (apq == 0.0) continue;
+                const double theta = (A[q][q] - A[p][p]) / (2.0 * apq);
+                const double tt = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                const double c = 1.0 / sqrt(tt * tt + 1.0), s = tt * c;
+                for (int k = 0; k < 3; ++k) {  // A ← Jᵀ A J
+                    const double akp = A[k][p], akq = A[k][q];
+                    A[k][p] = c * akp - s * akq;
+                    A[k][q] = s * akp + c * akq;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    const double apk = A[p][k], aqk = A[q][k];
+                    A[p][k] = c * apk - s * aqk;
+                    A[q][k] = s * apk + c * aqk;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    const double vkp = V[k][p], vkq = V[k][q];
+                    V[k][p] = c * vkp - s * vkq;
+                    V[k][q] = s * vkp + c * vkq;
+                }
+            }
+    }
+}
+
+__global__ void __launch_bounds__(128)
+    knn_surface_kernel(const float* __restrict__ xyz, int64_t M, Grid g, const int* __restrict__ sids,
+                       const int* __restrict__ cstart, const int* __restrict__ cend, int k, float alpha_max,
+                       float lambda, float* __restrict__ nrm_out, float* __restrict__ kappa_out,
+                       float* __restrict__ alpha_out, int* __restrict__ knn_out, float* __restrict__ nnd_out,
+                       int* __restrict__ degen_out) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    const double p0 = xyz[3 * m], p1 = xyz[3 * m + 1], p2 = xyz[3 * m + 2];
+    const int c0 = cell_coord(p0, g.lo[0], g.h, g.dim[0]);
+    const int c1 = cell_coord(p1, g.lo[1], g.h, g.dim[1]);
+    const int c2 = cell_coord(p2, g.lo[2], g.h, g.dim[2]);
+    double bd[kMaxK];
+    int bi[kMaxK];
+    int cnt = 0;
+    for (int r = 0;; ++r) {
+        const int x0 = c0 - r, x1 = c0 + r, y0 = c1 - r, y1 = c1 + r, z0 = c2 - r, z1 = c2 + r;
+        for (int cx = max(x0, 0); cx <= min(x1, g.dim[0] - 1); ++cx)
+            for (int cy = max(y0, 0); cy <= min(y1, g.dim[1] - 1); ++cy) {
+                const bool edge_xy = (cx == x0 || cx == x1 || cy == y0 || cy == y1);
+                for (int cz = max(z0, 0); cz <= min(z1, g.dim[2] - 1); ++cz) {
+                    if (!edge_xy && cz != z0 && cz != z1) continue;  // only the shell of radius r
+                    const int key = (cx * g.dim[1] + cy) * g.dim[2] + cz;
+                    const int s = cstart[key];
+                    if (s < 0) continue;
+                    const int e = cend[key];
+                    for (int i = s; i < e; ++i) {
+                        const int j = sids[i];
+                        const double dx = (double)xyz[3 * (int64_t)j] - p0, dy = (double)xyz[3 * (int64_t)j + 1] - p1,
+                                     dz = (double)xyz[3 * (int64_t)j + 2] - p2;
+                        const double d = dx * dx + dy * dy + dz * dz;
+                        if (cnt == k && !(d < bd[k - 1] || (d == bd[k - 1] && j < bi[k - 1]))) continue;
+                        int pos = cnt < k ? cnt : k - 1;
+                        while (pos > 0 && (d < bd[pos - 1] || (d == bd[pos - 1] && j < bi[pos - 1]))) {
+                            bd[pos] = bd[pos - 1];
+                            bi[pos] = bi[pos - 1];
+                            --pos;
+                        }
+                        bd[pos] = d;
+                        bi[pos] = j;
+                        if (cnt < k) ++cnt;
+                    }
+                }
+            }
+        // distance from p to the unsearched region (sides that reach the grid border are closed)
+        double bound = INFINITY;
+        const double pc[3] = {p0, p1, p2};
+        const int cc[3] = {c0, c1, c2};
+        bool all_covered = true;
+        for (int a = 0; a < 3; ++a) {
+            if (cc[a] - r > 0) {
+                bound = fmin(bound, pc[a] - (g.lo[a] + (cc[a] - r) * g.h));
+                all_covered = false;
+            }
+            if (cc[a] + r < g.dim[a] - 1) {
+                bound = fmin(bound, g.lo[a] + (cc[a] + r + 1) * g.h - pc[a]);
+                all_covered = false;
+            }
+        }
+        if (all_covered) break;
+        if (cnt == k && bd[k - 1] < bound * bound) break;
+    }
+    // neighbour ids, nearest other point distance
+    double nn = 0.0;
+    for (int i = 0; i < k; ++i) {
+        if (knn_out) knn_out[m * k + i] = bi[i];
+        if (bi[i] != (int)m && nn == 0.0) nn = sqrt(bd[i]);
+    }
+    if (nn == 0.0) {
+        for (int i = 0; i < k; ++i)
+            if (bi[i] != (int)m) { nn = sqrt(bd[i]); break; }
+    }
+    nnd_out[m] = (float)nn;
+    // centred scatter of the k neighbours
+    double mean[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < k; ++i)
+        for (int a = 0; a < 3; ++a) mean[a] += (double)xyz[3 * (int64_t)bi[i] + a];
+    for (int a = 0; a < 3; ++a) mean[a] /= k;
+    double C[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    for (int i = 0; i < k; ++i) {
+        double d[3];
+        for (int a = 0; a < 3; ++a) d[a] = (double)xyz[3 * (int64_t)bi[i] + a] - mean[a];
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) C[a][b] += d[a] * d[b];
+    }
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) C[a][b] /= k;
+    const double trace = C[0][0] + C[1][1] + C[2][2];
+    double n[3] = {0.0, 0.0, 1.0};
+    double kappa = 1.0 / 3.0;
+    int degenerate = 1;
+    if (trace > 0.0) {
+        degenerate = 0;
+        double V[3][3];
+        jacobi3(C, V);
+        int imin = 0;
+        for (int a = 1; a < 3; ++a)
+            if (C[a][a] < C[imin][imin]) imin = a;
+        const double lmin = C[imin][imin];
+        const double tr2 = C[0][0] + C[1][1] + C[2][2];
+        kappa = lmin / tr2;
+        double nrm = 0.0;
+        for (int a = 0; a < 3; ++a) { n[a] = V[a][imin]; nrm += n[a] * n[a]; }
+        nrm = sqrt(nrm);
+        for (int a = 0; a < 3; ++a) n[a] /= nrm;
+    }
+    kappa = fmin(fmax(kappa, 1e-12), 1.0 / 3.0);
+    const double alpha = (double)alpha_max * tanh(0.5 * (double)lambda * (1.0 / kappa - 3.0));
+    for (int a = 0; a < 3; ++a) nrm_out[3 * m + a] = (float)n[a];
+    kappa_out[m] = (float)kappa;
+    alpha_out[m] = (float)alpha;
+    degen_out[m] = degenerate;
+}
+
+// ---- host side -------------------------------------------------------------------------------------
+struct PrepLayout {
+    size_t blockpart, stats1, stats2, counter, keys, ids, skeys, sids, cstart, cend, nrm, kappa, alpha, nnd,
+        degen, cub_tmp, cub_bytes, total;
+};
+static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+constexpr int64_t kMaxCells = 1 << 22;
+
+static size_t cub_sort_bytes(int64_t M) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int*)nullptr, (int*)nullptr, (const int*)nullptr,
+                                    (int*)nullptr, (int)M, 0, 22);
+    return bytes;
+}
+
+static PrepLayout prep_layout(int64_t M, bool with_knn) {
+    PrepLayout L;
+    size_t o = 0;
+    L.blockpart = o; o += al(sizeof(double) * kRedBlocks * 16);
+    L.stats1 = o; o += al(sizeof(double) * 16);
+    L.stats2 = o; o += al(sizeof(double) * 16);
+    L.counter = o; o += al(sizeof(unsigned) * 4);
+    L.nrm = o; o += al(sizeof(float) * 3 * M);
+    L.kappa = o; o += al(sizeof(float) * M);
+    L.alpha = o; o += al(sizeof(float) * M);
+    L.nnd = o; o += al(sizeof(float) * M);
+    L.degen = o; o += al(sizeof(int) * M);
+    if (with_knn) {
+        L.keys = o; o += al(sizeof(int) * M);
+        L.ids = o; o += al(sizeof(int) * M);
+        L.skeys = o; o += al(sizeof(int) * M);
+        L.sids = o; o += al(sizeof(int) * M);
+        L.cstart = o; o += al(sizeof(int) * kMaxCells);
+        L.cend = o; o += al(sizeof(int) * kMaxCells);
+        L.cub_bytes = cub_sort_bytes(M);
+        L.cub_tmp = o; o += al(L.cub_bytes);
+    } else {
+        L.keys = L.ids = L.skeys = L.sids = L.cstart = L.cend = L.cub_tmp = L.cub_bytes = 0;
+    }
+    L.total = o;
+    return L;
+}
+
+size_t prepare_ws_bytes(int64_t M) { return prep_layout(M, true).total; }
+size_t pack_ws_bytes(int64_t M) { return prep_layout(M, false).total; }
+
+static int finish_target(const float* d_xyz, const float* nrm, const float* alpha, const float* nnd, const int* degen,
+                         int64_t M, double margin, char* ws, const PrepLayout& L, void* d_target,
+                         lsgcpd_target_info* info, cudaStream_t stream) {
+    double* bp = reinterpret_cast<double*>(ws + L.blockpart);
+    double* st1 = reinterpret_cast<double*>(ws + L.stats1);
+    double* st2 = reinterpret_cast<double*>(ws + L.stats2);
+    unsigned* ctr = reinterpret_cast<unsigned*>(ws + L.counter);
+    model_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_xyz, alpha, nnd, degen, M, st1, bp, st2, ctr);
+    TargetHeader* hdr = reinterpret_cast<TargetHeader*>(d_target);
+    header_kernel<<<1, 1, 0, stream>>>(hdr, M, st1, st2, margin, nnd != nullptr ? 1 : 0);
+    const int64_t M_pad = pad_targets(M);
+    pack_body_kernel<<<(unsigned)((M_pad + 255) / 256), 256, 0, stream>>>(d_xyz, nrm, alpha, M, M_pad, st2,
+                                                                          target_body(d_target));
+    LSG_CUDA(cudaGetLastError());
+    TargetHeader h;
+    LSG_CUDA(cudaMemcpyAsync(&h, hdr, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    LSG_CUDA(cudaStreamSynchronize(stream));
+    if (info) {
+        info->volume = h.volume;
+        info->extent = h.extent;
+        for (int a = 0; a < 3; ++a) {
+            info->aabb_lo[a] = h.aabb_lo[a];
+            info->aabb_hi[a] = h.aabb_hi[a];
+        }
+        info->alpha_mean = h.alpha_sum / (double)M;
+        info->n_degenerate = h.n_degenerate;
+    }
+    LSG_CHECK(isfinite(h.extent), LSGCPD_EINVAL, "non-finite coordinate in the target cloud");
+    LSG_CHECK(h.extent > 0.0 || nnd == nullptr, LSGCPD_EDEGENERATE, "degenerate target: all points coincide");
+    LSG_CHECK(isfinite(h.volume) && h.volume > 0.0, LSGCPD_EDEGENERATE, "degenerate target: zero working volume");
+    return 0;
+}
+
+int pack_target_impl(const float* d_xyz, const float* d_nrm, const float* d_alpha, int64_t M, double margin,
+                     void* d_target, void* d_ws, lsgcpd_target_info* info, cudaStream_t stream) {
+    const PrepLayout L = prep_layout(M, false);
+    char* ws = static_cast<char*>(d_ws);
+    LSG_CUDA(cudaMemsetAsync(ws + L.counter, 0, sizeof(unsigned) * 4, stream));
+    cloud_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_xyz, M, reinterpret_cast<double*>(ws + L.blockpart),
+                                                              reinterpret_cast<double*>(ws + L.stats1),
+                                                              reinterpret_cast<unsigned*>(ws + L.counter));
+    return finish_target(d_xyz, d_nrm, d_alpha, nullptr, nullptr, M, margin, ws, L, d_target, info, stream);
+}
+
+int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p, void* d_target, void* d_ws,
+                        lsgcpd_target_info* info, const lsgcpd_annotations* ann, cudaStream_t stream) {
+    const PrepLayout L = prep_layout(M, true);
+    char* ws = static_cast<char*>(d_ws);
+    double* bp = reinterpret_cast<double*>(ws + L.blockpart);
+    double* st1 = reinterpret_cast<double*>(ws + L.stats1);
+    unsigned* ctr = reinterpret_cast<unsigned*>(ws + L.counter);
+    LSG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 4, stream));
+    cloud_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_xyz, M, bp, st1, ctr);
+    double s1[9];
+    LSG_CUDA(cudaMemcpyAsync(s1, st1, sizeof(s1), cudaMemcpyDeviceToHost, stream));
+    LSG_CUDA(cudaStreamSynchronize(stream));
+    // grid: cell size from the AABB volume per point (≈ 1 point per cell for a volume-filling cloud)
+    Grid g;
+    double ext[3], maxe = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        g.lo[a] = -s1[a];
+        ext[a] = s1[3 + a] + s1[a];
+        maxe = fmax(maxe, ext[a]);
+    }
+    LSG_CHECK(maxe > 0.0 && isfinite(maxe), LSGCPD_EDEGENERATE, "degenerate target: all points coincide");
+    const double floor_e = maxe * 1e-3;
+    double h = cbrt(fmax(ext[0], floor_e) * fmax(ext[1], floor_e) * fmax(ext[2], floor_e) / (double)M);
+    for (;;) {
+        int64_t cells = 1;
+        for (int a = 0; a < 3; ++a) {
+            g.dim[a] = (int)fmin(floor(ext[a] / h) + 1.0, 1024.0);
+            cells *= g.dim[a];
+        }
+        if (cells <= kMaxCells) break;
+        h *= 1.25;
+    }
+    g.h = h;
+    int* keys = reinterpret_cast<int*>(ws + L.keys);
+    int* ids = reinterpret_cast<int*>(ws + L.ids);
+    int* skeys = reinterpret_cast<int*>(ws + L.skeys);
+    int* sids = reinterpret_cast<int*>(ws + L.sids);
+    int* cstart = reinterpret_cast<int*>(ws + L.cstart);
+    int* cend = reinterpret_cast<int*>(ws + L.cend);
+    const unsigned nb = (unsigned)((M + 255) / 256);
+    cell_keys_kernel<<<nb, 256, 0, stream>>>(d_xyz, M, g, keys, ids);
+    size_t cub_bytes = L.cub_bytes;
+    LSG_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.cub_tmp, cub_bytes, keys, skeys, ids, sids, (int)M, 0, 22, stream));
+    const int64_t ncells = (int64_t)g.dim[0] * g.dim[1] * g.dim[2];
+    LSG_CUDA(cudaMemsetAsync(cstart, 0xff, sizeof(int) * ncells, stream));
+    LSG_CUDA(cudaMemsetAsync(cend, 0xff, sizeof(int) * ncells, stream));
+    cell_ranges_kernel<<<nb, 256, 0, stream>>>(skeys, M, cstart, cend);
+    float* nrm = ann && ann->d_normals ? ann->d_normals : reinterpret_cast<float*>(ws + L.nrm);
+    float* kap = ann && ann->d_kappa ? ann->d_kappa : reinterpret_cast<float*>(ws + L.kappa);
+    float* alp = ann && ann->d_alpha ? ann->d_alpha : reinterpret_cast<float*>(ws + L.alpha);
+    int* knn = ann ? ann->d_knn : nullptr;
+    float* nnd = reinterpret_cast<float*>(ws + L.nnd);
+    int* degen = reinterpret_cast<int*>(ws + L.degen);
+    knn_surface_kernel<<<(unsigned)((M + 127) / 128), 128, 0, stream>>>(d_xyz, M, g, sids, cstart, cend, p.knn_k,
+                                                                        p.alpha_max, p.lambda, nrm, kap, alp, knn,
+                                                                        nnd, degen);
+    LSG_CUDA(cudaGetLastError());
+    return finish_target(d_xyz, nrm, alp, nnd, degen, M, p.volume_margin, ws, L, d_target, info, stream);
+}
+
+}  // namespace lsg

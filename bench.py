@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark: LSG-CPD E-step pair evaluations/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config scale] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL)
+
+A step is one full registration of the workload through the library (lsgcpd_register: σ²₀, then
+`iters` EM iterations of E step → moments → NCCL all-reduce → SE(3) Newton + σ²) with the prepared
+target and the source shard already resident in HBM.  value = M·N·iters·K / (max over ranks of the
+device time of the K steps).  The source is sharded contiguously across ranks, the target is
+replicated (strong scaling: the total problem is fixed).
+
+`e2e` is the same metric through the public API from pinned HOST buffers: every step copies the
+target and source shard host→device, prepares the target (kNN/normals/α on the GPU), registers and
+returns R, t, σ² to the host.  `roofline` is for the dominant kernel (the fused E step), timed with
+CUDA events around lsgcpd_estep on the launching stream.  `cpu_baseline` / `--impl reference` time the
+FP64 CPU oracle (test infrastructure, never on the product path) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "E-step pair evals/s (M·N·iters/s) at 1/2/4/8 B200; % of MUFU/FP32 peak"
+UNIT = "pair-evals/s"
+SM_MAX_MHZ_FALLBACK = 1965.0
+FLOPS_PER_PAIR = 47.0     # SURVEY §8(d).2 algorithmic FP32 flops per (m, n) pair (FMA = 2), + 1 exp
+FP32_LANES_PER_SM = 128   # FP32 FMA lanes per SM per clock (B200)
+MUFU_EX2_PER_SM = 16      # MUFU.EX2 results per SM per clock (B200; measured 4.58e12/s, tools/microbench)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="scale")
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--skip-cpu", action="store_true", help="skip the cpu_baseline leg (profiling runs)")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--iters", type=int, default=0, help="override EM iterations per step (0 = config's)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def shard(n: int, rank: int, world: int):
+    """Contiguous, balanced source shard [lo, hi) of rank `rank` (paper_2103_15039_b200.dist)."""
+    from paper_2103_15039_b200.dist import shard_range
+    return shard_range(n, rank, world)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"sm_max_mhz": SM_MAX_MHZ_FALLBACK}, "fallback"
+
+
+def cpu_oracle_rate(wl, target_sample_pts: int = 0, budget_s: float = 12.0):
+    """FP64 oracle E step (C/OpenMP, all host cores) on a bounded sample of source points against the
+    full target; returns (pairs/s, cores, sample description)."""
+    import oracle
+    rng = np.random.default_rng(0)
+    tgt_n = rng.standard_normal(wl.target.shape)
+    tgt_n /= np.linalg.norm(tgt_n, axis=1, keepdims=True)
+    alpha = rng.uniform(0, 50, wl.M)
+    V, _ = oracle.working_volume(wl.target)
+    cores = int(oracle._lib.lib().ora_max_threads())
+    # calibrate on 8 points, then size the sample for ~budget_s of CPU work
+    idx = rng.choice(wl.N, 8, replace=False)
+    t0 = time.perf_counter()
+    oracle.estep(wl.target, tgt_n, alpha, wl.source[idx], wl.R_expected, wl.t_expected, 1e-3, wl.w, V)
+    dt = max(time.perf_counter() - t0, 1e-3)
+    n = int(np.clip(8 * budget_s / dt, 8, wl.N))
+    idx = rng.choice(wl.N, n, replace=False)
+    t0 = time.perf_counter()
+    oracle.estep(wl.target, tgt_n, alpha, wl.source[idx], wl.R_expected, wl.t_expected, 1e-3, wl.w, V)
+    dt = time.perf_counter() - t0
+    return n * wl.M / dt, cores, f"oracle E step (FP64, OpenMP) for {n} sampled source points x all {wl.M} targets", dt
+
+
+def run_reference(args, wl, rank):
+    """--impl reference: the FP64 CPU oracle (E step + M step on a source sample) as it stands."""
+    import oracle
+    if rank != 0:
+        return
+    rng = np.random.default_rng(1)
+    # seeded unit normals and α in [0, 50] (the annotation cost is not part of the E-step metric)
+    normals = rng.standard_normal(wl.target.shape)
+    normals /= np.linalg.norm(normals, axis=1, keepdims=True)
+    alpha = rng.uniform(0, 50, wl.M)
+    V, ext = oracle.working_volume(wl.target)
+    cores = int(oracle._lib.lib().ora_max_threads())
+    s = 256 if wl.M > 100000 else min(wl.N, 2048)
+    idx = np.sort(rng.choice(wl.N, s, replace=False))
+    X = wl.source[idx]
+    R, t, s2 = np.eye(3), np.zeros(3), oracle.sigma2_init(X, wl.target)
+
+    def step():
+        nonlocal R, t, s2
+        rec = oracle.estep(wl.target, normals, alpha, X, R, t, s2, wl.w, V)
+        R, t, s2, _ = oracle.mstep(X, rec, R, t, s2, ext, 10, 1e-12 * ext * ext)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = s * wl.M * args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.name, "M": wl.M, "N": wl.N, "w": wl.w, "sample_source_points": s},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"per step: oracle E step + M step for {s} sampled source points x all "
+                                       f"{wl.M} targets"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    import synth
+    wl = synth.make(args.config)
+    if args.impl == "reference":
+        return run_reference(args, wl, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2103_15039_b200 as lsg
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    iters = args.iters or wl.iters
+    lo, hi = shard(wl.N, rank, world)
+    n_local = hi - lo
+
+    # resident inputs
+    tgt_xyz = torch.from_numpy(wl.target).to(dev)
+    src = torch.from_numpy(np.ascontiguousarray(wl.source[lo:hi])).to(dev)
+    target = lsg.prepare_target(tgt_xyz, wl.knn_k)
+    comm = lsg.Comm(rank, world) if world > 1 else None
+    reg = lsg.Registrar(target, src, iters)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MiB > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def step():
+        return reg(w=wl.w, comm=comm)
+
+    for _ in range(args.warmup):
+        out = step()
+        flush.fill_(1)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters_done = []
+    barrier()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            out = step()
+            iters_done.append(out["iters"])
+            flush.fill_(1)
+        e1.record(stream)
+        barrier()
+    dev_s = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    pairs_per_step = float(wl.M) * float(wl.N) * iters
+    assert all(i == iters for i in iters_done), iters_done
+    value = pairs_per_step * args.steps / dev_s
+    clocks = clk.summary()
+
+    # ---- roofline of the dominant kernel: the fused E step (lsgcpd_estep on this stream) ----
+    runner = lsg.EstepRunner(target, src)
+    s2_probe = float(out["sigma2"])
+    for _ in range(2):
+        runner(out["R"], out["t"], s2_probe, wl.w)
+    nrep = 3
+    barrier()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for _ in range(nrep):
+        runner(out["R"], out["t"], s2_probe, wl.w)
+    k1.record(stream)
+    barrier()
+    t_launch = max_over_ranks(k0.elapsed_time(k1) / 1e3 / nrep)
+    pairs_launch = float(wl.M) * float(n_local)
+    peaks, peak_src = measured_peaks()
+    f_max = float(peaks.get("sm_max_mhz", SM_MAX_MHZ_FALLBACK)) * 1e6
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak_tflops = sms * FP32_LANES_PER_SM * 2 * f_max / 1e12
+    mufu_peak = sms * MUFU_EX2_PER_SM * f_max
+    achieved_tflops = FLOPS_PER_PAIR * pairs_launch / t_launch / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "estep_dram_bytes.json")
+    if os.path.exists(tfile):
+        try:
+            tj = json.load(open(tfile))
+            if tj.get("workload") == wl.name and tj.get("n_gpus") == world:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "achieved": achieved_tflops, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
+                "frac": achieved_tflops / fp32_peak_tflops, "traffic": traffic,
+                "kernel": "lsg::estep_kernel (+merge) via lsgcpd_estep",
+                "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 flop x {f_max/1e6:.0f} MHz "
+                               f"(sm_max_mhz {peak_src}, MEASURED_PEAKS.json); algorithmic "
+                               f"{FLOPS_PER_PAIR:.0f} flop/pair (SURVEY 8(d).2)",
+                "pairs_per_launch": pairs_launch, "launch_ms": t_launch * 1e3,
+                "mufu_ex2_frac": pairs_launch / t_launch / mufu_peak,
+                "pairs_per_s_per_gpu": pairs_launch / t_launch}
+
+    # ---- e2e: host buffers → public API → host results ----
+    e2e = None
+    if not args.skip_e2e:
+        h_tgt = torch.from_numpy(wl.target).pin_memory()
+        h_src = torch.from_numpy(np.ascontiguousarray(wl.source[lo:hi])).pin_memory()
+        d_tgt = torch.empty_like(h_tgt, device=dev)
+        d_src = torch.empty_like(h_src, device=dev)
+
+        def e2e_step():
+            d_tgt.copy_(h_tgt, non_blocking=True)
+            d_src.copy_(h_src, non_blocking=True)
+            tg = lsg.prepare_target(d_tgt, wl.knn_k)
+            return lsg.Registrar(tg, d_src, iters)(w=wl.w, comm=comm)
+
+        e2e_step()
+        flush.fill_(1)
+        ne = max(1, min(args.steps, 3))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(ne):
+            r = e2e_step()
+            flush.fill_(1)
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": pairs_per_step * ne / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(h_tgt.numel() * 4 + h_src.numel() * 4),
+               "d2h_bytes_per_step": int(9 * 8 + 3 * 8 + 8 + 4), "steps": ne,
+               "includes": "H2D target+source, lsgcpd_prepare_target, lsgcpd_register, R/t/sigma2 to host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        rate, cores, sample, secs = cpu_oracle_rate(wl)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+               "seconds": secs}
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        launches_per_step = 3 + 4 * iters
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl.name, "M": wl.M, "N": wl.N, "iters_per_step": iters, "w": wl.w,
+                       "knn_k": wl.knn_k, "step": "one full registration (lsgcpd_register)",
+                       "parallelism": f"source-sharded x{world}, target replicated, 75-double NCCL all-reduce "
+                                      f"per EM iteration",
+                       "l2": "flushed between steps (256 MiB write)"},
+            "registrations_per_s": args.steps / dev_s,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

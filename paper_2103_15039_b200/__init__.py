@@ -226,19 +226,14 @@ class Comm:
     """NCCL communicator wrapper (one process per GPU); the id is broadcast over torch.distributed."""
 
     def __init__(self, rank: int, world_size: int, group=None):
-        import torch
-        import torch.distributed as dist
-        idbuf = torch.zeros(128, dtype=torch.uint8)
+        from .dist import broadcast_bytes
+        blob = b""
         if rank == 0:
             raw = (ctypes.c_char * 128)()
             _check(lib().lsgcpd_comm_unique_id(ctypes.cast(raw, ctypes.c_void_p)))
-            idbuf = torch.frombuffer(bytearray(raw.raw), dtype=torch.uint8).clone()
-        if dist.is_initialized() and world_size > 1:
-            dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
-            idb = idbuf.to(dev)
-            dist.broadcast(idb, src=0, group=group)
-            idbuf = idb.cpu()
-        raw = (ctypes.c_char * 128).from_buffer_copy(bytes(idbuf.numpy().tobytes()))
+            blob = bytes(raw.raw)
+        blob = broadcast_bytes(blob, 0, group)
+        raw = (ctypes.c_char * 128).from_buffer_copy(blob)
         h = ctypes.c_void_p()
         _check(lib().lsgcpd_comm_init(rank, world_size, ctypes.cast(raw, ctypes.c_void_p), ctypes.byref(h)))
         self.handle = h

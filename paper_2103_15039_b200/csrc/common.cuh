@@ -2,6 +2,7 @@
 // Paper citations: P:<line> of arXiv 2103.15039's LaTeX source.
 #pragma once
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -32,6 +33,8 @@ int cuda_fail(cudaError_t e, const char* what);
 
 // ------------------------------------------------------------------------------------------
 // Prepared target: header + per-target 16-float record (64 B), padded to a tile multiple.
+// Stored pair-interleaved: targets (2i, 2i+1) form a 128-B pair block holding, for every field f,
+// {f of 2i, f of 2i+1} adjacent — one float2 per field for the f32x2 (FFMA2) E-step kernel.
 //   f[0..3]   y_x, y_y, y_z, ω̄_m = ½log2(1+α_m) - ω_ref   (log-determinant weight, ≤ 0)
 //   f[4..7]   ñ_x, ñ_y, ñ_z (ñ = √α n), W_xx          (W = α n nᵀ)
 //   f[8..11]  W_xy, W_xz, W_yy, W_yz
@@ -169,6 +172,8 @@ struct Sched {
     int64_t G;        // CTAs
     int64_t nblk;     // source blocks
     int64_t kmax;     // max CTAs touching one source block (partial slots per block)
+    int64_t B;        // source points per block
+    int variant;      // E-step kernel variant
 };
 __host__ __device__ inline int64_t sched_start(const Sched& s, int64_t g) { return g * s.U / s.G; }
 __host__ __device__ inline int64_t sched_owner(const Sched& s, int64_t u) { return ((u + 1) * s.G - 1) / s.U; }

@@ -14,7 +14,6 @@ struct RegParams {
 // estep.cu
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc);
 size_t estep_partial_bytes(const Sched& s);
-size_t estep_partial_bytes_bound(int64_t M_pad, int64_t N, int64_t max_ctas);
 void estep_launch_setup(IterState* st, const void* d_target, const double* R, const double* t, double sigma2,
                         double w, double V, int64_t M, int consistent, cudaStream_t stream);
 void estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,

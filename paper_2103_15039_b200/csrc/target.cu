@@ -95,25 +95,29 @@ __global__ void pack_body_kernel(const float* __restrict__ xyz, const float* __r
                                  const double* __restrict__ stats2, float* __restrict__ body) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M_pad) return;
-    float4* o = reinterpret_cast<float4*>(body + m * kTgtFloats);
+    // pair-interleaved layout: target m is slot (m & 1) of pair m >> 1; field f at pair*32 + 2f + slot
+    float* o = body + (m >> 1) * (2 * kTgtFloats) + (m & 1);
+    float f[kTgtFloats];
     if (m >= M) {
         // far away (τ overflows to a huge value → weight 0 in both normaliser modes) and ω̄ = -inf
-        o[0] = make_float4(1e18f, 1e18f, 1e18f, -INFINITY);
-        o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-        o[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-        o[3] = make_float4(0.f, 0.f, 0.f, 0.f);
-        return;
+        f[0] = f[1] = f[2] = 1e18f;
+        f[3] = -INFINITY;
+        for (int i = 4; i < kTgtFloats; ++i) f[i] = 0.f;
+    } else {
+        const double y0 = xyz[3 * m], y1 = xyz[3 * m + 1], y2 = xyz[3 * m + 2];
+        const double n0 = nrm[3 * m], n1 = nrm[3 * m + 1], n2 = nrm[3 * m + 2];
+        const double a = alpha[m];
+        const double sa = sqrt(a);
+        const double ny = n0 * y0 + n1 * y1 + n2 * y2;
+        f[0] = (float)y0; f[1] = (float)y1; f[2] = (float)y2;
+        f[3] = (float)(0.5 * log2(1.0 + a) - stats2[0]);
+        f[4] = (float)(sa * n0); f[5] = (float)(sa * n1); f[6] = (float)(sa * n2);
+        f[7] = (float)(a * n0 * n0); f[8] = (float)(a * n0 * n1); f[9] = (float)(a * n0 * n2);
+        f[10] = (float)(a * n1 * n1); f[11] = (float)(a * n1 * n2); f[12] = (float)(a * n2 * n2);
+        f[13] = (float)(a * ny * n0); f[14] = (float)(a * ny * n1); f[15] = (float)(a * ny * n2);
     }
-    const double y0 = xyz[3 * m], y1 = xyz[3 * m + 1], y2 = xyz[3 * m + 2];
-    const double n0 = nrm[3 * m], n1 = nrm[3 * m + 1], n2 = nrm[3 * m + 2];
-    const double a = alpha[m];
-    const double sa = sqrt(a);
-    const double ny = n0 * y0 + n1 * y1 + n2 * y2;
-    const double om = 0.5 * log2(1.0 + a) - stats2[0];
-    o[0] = make_float4((float)y0, (float)y1, (float)y2, (float)om);
-    o[1] = make_float4((float)(sa * n0), (float)(sa * n1), (float)(sa * n2), (float)(a * n0 * n0));
-    o[2] = make_float4((float)(a * n0 * n1), (float)(a * n0 * n2), (float)(a * n1 * n1), (float)(a * n1 * n2));
-    o[3] = make_float4((float)(a * n2 * n2), (float)(a * ny * n0), (float)(a * ny * n1), (float)(a * ny * n2));
+#pragma unroll
+    for (int i = 0; i < kTgtFloats; ++i) o[2 * i] = f[i];
 }
 
 // ---- grid kNN ------------------------------------------------------------------------------------

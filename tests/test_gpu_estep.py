@@ -51,7 +51,8 @@ def test_estep_parity_outlier_weight_and_normaliser(w, consistent):
         np.testing.assert_allclose(rec[:, 0] + rec[:, 15], 1.0, atol=2e-6)
 
 
-@pytest.mark.parametrize("M,N", [(1, 1), (3, 7), (63, 65), (64, 512), (257, 513), (1000, 1), (2, 5000)])
+@pytest.mark.parametrize("M,N", [(1, 1), (3, 7), (63, 65), (64, 512), (257, 513), (1000, 1), (2, 5000),
+                                 (130, 769)])
 def test_estep_ragged_and_tiny_sizes(M, N):
     rng = np.random.default_rng(M * 7919 + N)
     Y = rng.uniform(-1, 1, (M, 3)).astype(np.float32)
@@ -95,7 +96,8 @@ def test_estep_sampled_parity_at_full_scale():
         tgt = _gpu_target(Y, n32, a32)
         Xd = to_dev(wl.source)
         idx = np.sort(rng.choice(wl.N, 192, replace=False))
-        for s2 in (1e-3, 1e-5):
+        s2_0 = oracle.sigma2_init(wl.source, Y, wl.R_expected, wl.t_expected)
+        for s2 in (s2_0, 1e-3, 1e-5):     # σ²₀: every target contributes (longest FP32 sums)
             rec = lsg.estep(tgt, Xd, wl.R_expected, wl.t_expected, s2, wl.w, V).cpu().numpy()[idx]
             ora = oracle.estep(Y, n32.astype(np.float64), a32.astype(np.float64), wl.source[idx], wl.R_expected,
                                wl.t_expected, s2, wl.w, V)
@@ -115,3 +117,13 @@ def test_estep_invalid_arguments_raise():
         lsg.estep(tgt, X, 2 * np.eye(3), np.zeros(3), 1e-3, 0.1, V)
     with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
         lsg.estep(tgt, X, np.eye(3), np.array([np.nan, 0, 0]), 1e-3, 0.1, V)
+
+
+@pytest.mark.parametrize("variant", range(7))
+def test_estep_every_kernel_variant(variant, monkeypatch):
+    # every compiled kernel variant (scalar / packed f32x2, points per thread, warps) gives the same record
+    monkeypatch.setenv("LSGCPD_ESTEP_VARIANT", str(variant))
+    wl, n32, a32, V, ext = oracle_target32("tiny")
+    for w in (0.0, 0.1):
+        rec, ora = _run_pair(wl.target, n32, a32, wl.source, wl.R_expected, wl.t_expected, 1e-4, w, V)
+        assert_record_parity(rec, ora, wl.target, a32, what=f"variant {variant} w={w}")

@@ -193,7 +193,7 @@ LSG_EXPORT void lsgcpd_em_params_default(lsgcpd_em_params* p) {
 
 LSG_EXPORT size_t lsgcpd_target_bytes(int64_t M) {
     if (M < 0) return 0;
-    return kHeaderBytes + (size_t)pad_targets(M) * kTgtFloats * sizeof(float);
+    return target_total_bytes(pad_targets(M));
 }
 
 LSG_EXPORT size_t lsgcpd_prepare_workspace_bytes(int64_t M, int knn_k) {

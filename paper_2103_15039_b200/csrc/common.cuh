@@ -64,6 +64,23 @@ inline int64_t pad_targets(int64_t M) { return (M + kTgtPadMultiple - 1) / kTgtP
 inline const float* target_body(const void* t) { return reinterpret_cast<const float*>(static_cast<const char*>(t) + kHeaderBytes); }
 inline float* target_body(void* t) { return reinterpret_cast<float*>(static_cast<char*>(t) + kHeaderBytes); }
 
+// Tensor-core section (after the pair-interleaved body): per 64-target tile, 10 KB:
+//   [0, 2048)     core: 32 target pairs × 64 B, field f of targets (2i, 2i+1) adjacent, f = y0, y1, y2, ω̄,
+//                 ñ0, ñ1, ñ2, 0 (the CUDA-core part of the pair math, two targets per f32x2 instruction)
+//   [2048, 10240) 8 K-steps × 1024 B: the 32×8 B operand [F_hi; F_lo] of one K step, where
+//                 F[f][m] = (1, y, W, b, 0,0,0), F_hi = F rounded to TF32 (nearest), F_lo = F - F_hi
+//                 (exact in FP32, read as TF32 by the MMA); UMMA K-major, no swizzle:
+//                 core matrix = 8 rows × 16 B (4 targets); LBO = 128 B (next 4 targets),
+//                 SBO = 256 B (next 8 rows): byte(row r, j) = 1024 s + (r/8) 256 + (j/4) 128 + (r%8) 16 + (j%4) 4.
+constexpr int kTcTile = 64;
+constexpr int kTcTileBytes = 10240;
+constexpr int kTcCoreBytes = 2048;
+constexpr int kTcBOff = 2048;
+inline size_t tc_section_offset(int64_t M_pad) { return kHeaderBytes + (size_t)M_pad * kTgtFloats * sizeof(float); }
+inline size_t target_total_bytes(int64_t M_pad) { return tc_section_offset(M_pad) + (size_t)(M_pad / kTcTile) * kTcTileBytes; }
+inline const float* target_tc(const void* t, int64_t M_pad) { return reinterpret_cast<const float*>(static_cast<const char*>(t) + tc_section_offset(M_pad)); }
+inline float* target_tc(void* t, int64_t M_pad) { return reinterpret_cast<float*>(static_cast<char*>(t) + tc_section_offset(M_pad)); }
+
 // ------------------------------------------------------------------------------------------
 // Per-E-step constants, computed in FP64 on the device (setup kernel or the Newton kernel),
 // read by the E-step kernels.  See DESIGN.md "E-step arithmetic".

@@ -193,7 +193,7 @@ __global__ void estep_setup_kernel(IterState* st, const TargetHeader* hdr, doubl
 template <int PPT, int NCW, int MINB, bool PACKED, bool kLiteral>
 __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     estep_kernel(const float* __restrict__ tgt, const float* __restrict__ src, int64_t N,
-                 const IterState* __restrict__ st, Sched sc, float* __restrict__ part) {
+                 const IterState* __restrict__ st, Sched sc, float* __restrict__ part, int skip_fixed) {
     using T = typename std::conditional<PACKED, float2, float>::type;
     constexpr int W = PACKED ? 2 : 1;        // source points per register lane
     constexpr int NL = PPT / W;              // register lanes per thread
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     __shared__ __align__(8) uint64_t full_bar[kStages];
     __shared__ __align__(8) uint64_t empty_bar[kStages];
 
-    if (!st->active) return;
+    if (!st->active || (skip_fixed && st->fixed)) return;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t g = blockIdx.x;
@@ -384,6 +384,383 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     if (cur_blk >= 0) flush(cur_blk);
 }
 
+// ---- tensor-core (tcgen05) variant --------------------------------------------------------------
+// The 13 target-feature accumulations Σ_m p_mn F_m (F = 1, y, α n nᵀ, α(n·y)n) are a dense K = M
+// contraction D[points × 16] += P[points × K] · F[K × 16].  The CUDA cores compute p per pair (τ, e,
+// MUFU.EX2) and Σ p τ; p is split into TF32 hi + lo (p_hi = p with the low 13 mantissa bits cleared,
+// p_lo = p - p_hi exactly) and written to TMEM as the A operand; one elected thread per warpgroup
+// issues tcgen05.mma.kind::tf32 (A from TMEM, B = F_hi / F_lo from shared memory, D in TMEM):
+// D += A_hi F_hi + A_lo F_hi + A_hi F_lo (3×TF32 ≈ FP32 products).  D is drained to registers and
+// Kahan-folded after every 64-target tile (FP32 error independent of M).  Fixed-max mode only; the
+// running-max mode (w = 0 or tiny w) is served by the CUDA-core kernel.
+constexpr int kTcStages = 4;
+constexpr int kTcWG = 4;                      // consumer warpgroups (128 TMEM lanes each)
+constexpr int kTcNCW = 4 * kTcWG;
+constexpr int kTcMW = 2;                      // MMA-issuing warps (each serves kTcWG / kTcMW warpgroups)
+constexpr int kTcThreads = (kTcNCW + 1 + kTcMW) * 32;   // + TMA producer warp + MMA warps
+constexpr int kTcCols = 512;                  // TMEM columns allocated
+constexpr int kTcWGCols = 128;                // per warpgroup: D 2 row blocks × 32 + A 2 buffers × (2 × 16)
+constexpr int kTcChunk = 8;                   // targets per A buffer (one K step)
+// dynamic shared memory: target stages + Kahan running sums (R, C) of the 13 TC features per thread
+constexpr size_t kTcSmemRC = (size_t)26 * kTcNCW * 32 * sizeof(float2);
+constexpr size_t kTcSmem = kTcSmemRC;   // dynamic part (the stages are static shared memory)
+// instruction descriptors: D F32, A/B TF32, K-major A and B, M = 128, N = 32 ([hi | lo] features) or 16
+constexpr uint32_t kTcIdesc32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t kTcIdesc16 = (1u << 4) | (2u << 7) | (2u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t enable_d) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(enable_d)
+        : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n"
+        ".reg .pred P;\n"
+        "elect.sync _|P, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, P;\n"
+        "}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+// UMMA shared-memory descriptor: K-major, no swizzle, LBO = 128 B, SBO = 256 B, version 1 (sm_100).
+__device__ __forceinline__ uint64_t bdesc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128u >> 4) << 16) | ((uint64_t)(256u >> 4) << 32) |
+           ((uint64_t)1 << 46);
+}
+
+// Warp roles: 16 consumer warps (4 warpgroups × 128 TMEM lanes), 1 TMA producer warp, 2 MMA warps.
+// Per warpgroup mbarriers: afull[b] (4 warp arrivals: A buffer b written), aempty[b] (MMA commit: buffer
+// b consumed), dfull (commit after a tile's last MMAs: D ready), dfree (4 arrivals: D drained).
+// The running Kahan sums live in shared memory (touched once per tile), leaving registers for
+// in-flight pairs: the kernel is latency-bound on the τ → e → ex2 chain, so warps matter.
+template <bool kLiteral>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    estep_tc_kernel(const char* __restrict__ tc, const float* __restrict__ src, int64_t N,
+                    const IterState* __restrict__ st, Sched sc, float* __restrict__ part) {
+    constexpr int PPT = 2;
+    constexpr int kBlk = kTcNCW * 32 * PPT;   // 1024
+    constexpr int kChunks = kTcTile / kTcChunk;
+    // static shared memory for the TMA stages (link-time constant addresses: the MMA warp's B
+    // descriptors become immediates); dynamic shared memory for the Kahan running sums
+    __shared__ __align__(1024) char tiles_st[kTcStages][kTcTileBytes];
+    char* tiles = &tiles_st[0][0];
+    extern __shared__ __align__(16) char dsmem[];
+    float2* smRC = reinterpret_cast<float2*>(dsmem);   // [26][consumer threads]
+    __shared__ __align__(8) uint64_t full_bar[kTcStages];
+    __shared__ __align__(8) uint64_t empty_bar[kTcStages];
+    __shared__ __align__(8) uint64_t afull[kTcWG][2], aempty[kTcWG][2], dfull[kTcWG], dfree[kTcWG];
+    __shared__ uint32_t tmem_base_sh;
+
+    if (!st->active || !st->fixed) return;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t g = blockIdx.x;
+    const int64_t u0 = sched_start(sc, g), u1 = sched_start(sc, g + 1);
+    if (u0 >= u1) return;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"((uint32_t)kTcCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 32) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], kTcNCW);
+        }
+        for (int w = 0; w < kTcWG; ++w) {
+            mbar_init(&afull[w][0], 4);
+            mbar_init(&afull[w][1], 4);
+            mbar_init(&aempty[w][0], 1);
+            mbar_init(&aempty[w][1], 1);
+            mbar_init(&dfull[w], 1);
+            mbar_init(&dfree[w], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    if (tmem != 0u) __trap();   // 512 columns = the whole TMEM: the allocation must start at lane 0, column 0
+
+    if (warp == kTcNCW) {
+        // ---------------- producer warp: TMA bulk copies of 10-KB tensor-core tiles ----------------
+        if (lane == 0) {
+            int64_t it = 0;
+            for (int64_t u = u0; u < u1; ++u, ++it) {
+                const int s = (int)(it % kTcStages);
+                const uint32_t ph = (uint32_t)((it / kTcStages) & 1);
+                mbar_wait_sleep(&empty_bar[s], ph ^ 1);
+                const int64_t tile = u % sc.T;
+                mbar_arrive_expect_tx(&full_bar[s], kTcTileBytes);
+                bulk_g2s(tiles + s * kTcTileBytes, tc + tile * (int64_t)kTcTileBytes, kTcTileBytes, &full_bar[s]);
+            }
+        }
+        return;
+    }
+    if (warp > kTcNCW) {
+        // ---------------- MMA warps: warp-uniform loop, one elected lane issues tcgen05.mma ----------------
+        // per warpgroup w, row block rb, K step c:  D[:, 0:32] (+)= A_hi · [F_hi | F_lo]   (N = 32)
+        //                                           D[:, 0:16]  += A_lo · F_hi             (N = 16)
+        // The CTA owns all 512 TMEM columns, so the allocation starts at column 0 (checked above) and every
+        // TMEM operand is a compile-time constant; only the stage's B descriptor varies (warp-uniform).
+        const int mw = warp - kTcNCW - 1;
+        constexpr int kWPer = kTcWG / kTcMW;
+        uint32_t aph[kWPer][2] = {}, fph[kWPer] = {};
+        for (int64_t ub = u0; ub < u1; ub += kTcStages) {
+            const uint32_t round_ph = (uint32_t)(((ub - u0) / kTcStages) & 1);
+#pragma unroll
+            for (int s = 0; s < kTcStages; ++s) {   // stage index is a compile-time constant
+                if (ub + s >= u1) break;
+                mbar_wait(&full_bar[s], round_ph);
+#pragma unroll
+                for (int c = 0; c < kChunks; ++c) {
+                    const int buf = c & 1;   // kChunks is even: the buffer parity restarts every tile
+                    const uint64_t b32 = bdesc(smem_u32(&tiles_st[s][0]) + kTcBOff + 1024 * c);
+#pragma unroll
+                    for (int wi = 0; wi < kWPer; ++wi) {
+                        const int w = mw * kWPer + wi;
+                        if (c == 0 && (ub + s) > u0) {   // D must be drained before it is overwritten
+                            mbar_wait(&dfree[w], fph[wi]);
+                            fph[wi] ^= 1u;
+                        }
+                        mbar_wait(&afull[w][buf], aph[wi][buf]);
+                        aph[wi][buf] ^= 1u;
+                        tc_fence_after();
+                        if (elect_one()) {
+                            const uint32_t colD = (uint32_t)(w * kTcWGCols);
+                            const uint32_t colA = colD + 64 + buf * 32;
+#pragma unroll
+                            for (int rb = 0; rb < 2; ++rb) {
+                                mma_tf32_ts(colD + rb * 32, colA + rb * 16, b32, kTcIdesc32, c == 0 ? 0u : 1u);
+                                mma_tf32_ts(colD + rb * 32, colA + rb * 16 + 8, b32, kTcIdesc16, 1u);
+                            }
+                            mma_commit(&aempty[w][buf]);
+                            if (c == kChunks - 1) mma_commit(&dfull[w]);
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers: warpgroup wg, TMEM lane quadrant q ----------------
+    // Each thread owns one point in each of the two 128-row blocks; f32x2 instructions cover two
+    // consecutive TARGETS, so {p_m, p_m+1} pairs land directly in consecutive A columns of TMEM.
+    const int wg = warp >> 2, q = warp & 3;
+    const int tw = q * 32 + lane;                      // thread (= TMEM lane) within the warpgroup
+    const int tid = threadIdx.x;                       // consumer thread id (smem column)
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t colA0 = (uint32_t)(wg * kTcWGCols) + 64, colD0 = (uint32_t)(wg * kTcWGCols);
+    const uint32_t afull_a[2] = {smem_u32(&afull[wg][0]), smem_u32(&afull[wg][1])};
+    const uint32_t aempty_a[2] = {smem_u32(&aempty[wg][0]), smem_u32(&aempty[wg][1])};
+    const float k2 = st->k2;
+    const float2 nk2 = bc(-k2);
+    double Rm[9], tv[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Rm[i] = st->R[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) tv[i] = st->t[i];
+
+    float h[2][3], l[2][3];
+    float2 Rt, Ct;
+    int64_t cur_blk = -1;
+    uint32_t eph[2] = {0u, 0u}, dph = 0u;
+    bool used[2] = {false, false};
+    uint32_t cc = 0;
+    constexpr int kRC = kTcNCW * 32;
+
+    auto load_points = [&](int64_t j) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int64_t n = j * kBlk + wg * 256 + k * 128 + tw;
+            double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+            if (n < N) {
+                x0 = src[3 * n];
+                x1 = src[3 * n + 1];
+                x2 = src[3 * n + 2];
+            }
+            const double X[3] = {fma(Rm[0], x0, fma(Rm[1], x1, fma(Rm[2], x2, tv[0]))),
+                                 fma(Rm[3], x0, fma(Rm[4], x1, fma(Rm[5], x2, tv[1]))),
+                                 fma(Rm[6], x0, fma(Rm[7], x1, fma(Rm[8], x2, tv[2])))};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                h[k][a] = __double2float_rn(X[a]);
+                l[k][a] = __double2float_rn(X[a] - (double)h[k][a]);
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < 26; ++f) smRC[f * kRC + tid] = make_float2(0.f, 0.f);
+        Rt = Ct = make_float2(0.f, 0.f);
+    };
+    auto flush = [&](int64_t j) {
+        const int64_t slot = j * sc.kmax + (g - sched_owner(sc, j * sc.T));
+        float* base = part + slot * (int64_t)kPartF * kBlk;
+#pragma unroll
+        for (int f = 0; f < 13; ++f) {
+            const float2 R = smRC[f * kRC + tid], C = smRC[(13 + f) * kRC + tid];
+            base[f * kBlk + wg * 256 + tw] = __fsub_rn(R.x, C.x);
+            base[f * kBlk + wg * 256 + 128 + tw] = __fsub_rn(R.y, C.y);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int b = wg * 256 + k * 128 + tw;
+            base[13 * kBlk + b] = __fsub_rn(lane_of(Rt, k), lane_of(Ct, k));
+            base[14 * kBlk + b] = 0.f;
+            base[15 * kBlk + b] = 0.f;
+        }
+    };
+
+    int64_t it = 0;
+    for (int64_t u = u0; u < u1; ++u, ++it) {
+        const int64_t j = u / sc.T;
+        if (j != cur_blk) {
+            if (cur_blk >= 0) flush(cur_blk);
+            cur_blk = j;
+            load_points(j);
+        }
+        const int s = (int)(it % kTcStages);
+        mbar_wait(&full_bar[s], (uint32_t)((it / kTcStages) & 1));
+        const float4* core = reinterpret_cast<const float4*>(tiles + s * kTcTileBytes);
+        float2 Lt[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};   // Σ p τ, {even, odd} targets
+#pragma unroll 1
+        for (int c = 0; c < kChunks; ++c, ++cc) {
+            const int buf = (int)(cc & 1u);
+            if (used[buf]) {                 // wait until the MMAs of two chunks ago released this A buffer
+                asm volatile(
+                    "{\n"
+                    ".reg .pred P1;\n"
+                    "WAITE_%=:\n"
+                    "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                    "@!P1 bra WAITE_%=;\n"
+                    "}\n" ::"r"(aempty_a[buf]),
+                    "r"(eph[buf])
+                    : "memory");
+                eph[buf] ^= 1u;
+                tc_fence_after();
+            }
+            used[buf] = true;
+#pragma unroll
+            for (int rb = 0; rb < 2; ++rb) {
+                float2 hi[4], lo[4];
+#pragma unroll
+                for (int pp = 0; pp < 4; ++pp) {
+                    const int pr = c * 4 + pp;   // target pair within the tile
+                    const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
+                    // v0 = {y0a, y0b, y1a, y1b}, v1 = {y2a, y2b, ωa, ωb}, v2 = {n0a, n0b, n1a, n1b}, v3 = {n2a, n2b, -, -}
+                    const float2 rx = __fadd2_rn(__fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y)), bc(l[rb][0]));
+                    const float2 ry = __fadd2_rn(__fadd2_rn(bc(h[rb][1]), make_float2(-v0.z, -v0.w)), bc(l[rb][1]));
+                    const float2 rz = __fadd2_rn(__fadd2_rn(bc(h[rb][2]), make_float2(-v1.x, -v1.y)), bc(l[rb][2]));
+                    const float2 qv = __ffma2_rn(make_float2(v3.x, v3.y), rz,
+                                                 __ffma2_rn(make_float2(v2.z, v2.w), ry,
+                                                            __fmul2_rn(make_float2(v2.x, v2.y), rx)));
+                    const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
+                    const float2 e = kLiteral ? __fmul2_rn(nk2, tau) : __ffma2_rn(nk2, tau, make_float2(v1.z, v1.w));
+                    const float2 p = make_float2(ex2_approx(e.x), ex2_approx(e.y));
+                    Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
+                    hi[pp] = make_float2(__uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
+                                         __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
+                    lo[pp] = __fadd2_rn(p, make_float2(-hi[pp].x, -hi[pp].y));
+                }
+                const uint32_t va[16] = {__float_as_uint(hi[0].x), __float_as_uint(hi[0].y), __float_as_uint(hi[1].x),
+                                         __float_as_uint(hi[1].y), __float_as_uint(hi[2].x), __float_as_uint(hi[2].y),
+                                         __float_as_uint(hi[3].x), __float_as_uint(hi[3].y), __float_as_uint(lo[0].x),
+                                         __float_as_uint(lo[0].y), __float_as_uint(lo[1].x), __float_as_uint(lo[1].y),
+                                         __float_as_uint(lo[2].x), __float_as_uint(lo[2].y), __float_as_uint(lo[3].x),
+                                         __float_as_uint(lo[3].y)};
+                tmem_st16(tl + colA0 + buf * 32 + rb * 16, va);   // row block rb: [hi 0-7 | lo 0-7]
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(afull_a[buf]) : "memory");
+        }
+        // tile done: wait for D, drain it, free D and the smem stage, Kahan-fold into shared memory
+        mbar_wait(&dfull[wg], dph);
+        dph ^= 1u;
+        tc_fence_after();
+        uint32_t d0[16], d0l[16], d1[16], d1l[16];
+        tmem_ld16(tl + colD0, d0);          // row block 0: hi·hi + lo·hi
+        tmem_ld16(tl + colD0 + 16, d0l);    //              hi·lo
+        tmem_ld16(tl + colD0 + 32, d1);     // row block 1
+        tmem_ld16(tl + colD0 + 48, d1l);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&dfree[wg]);
+            mbar_arrive(&empty_bar[s]);
+        }
+#pragma unroll
+        for (int f = 0; f < 13; ++f) {
+            float2 R = smRC[f * kRC + tid], C = smRC[(13 + f) * kRC + tid];
+            const float2 L = make_float2(__uint_as_float(d0[f]) + __uint_as_float(d0l[f]),
+                                         __uint_as_float(d1[f]) + __uint_as_float(d1l[f]));
+            const float2 y = __fadd2_rn(L, make_float2(-C.x, -C.y));
+            const float2 t = __fadd2_rn(R, y);
+            C = __fadd2_rn(__fadd2_rn(t, make_float2(-R.x, -R.y)), make_float2(-y.x, -y.y));
+            smRC[f * kRC + tid] = t;
+            smRC[(13 + f) * kRC + tid] = C;
+        }
+        {
+            const float2 L = make_float2(Lt[0].x + Lt[0].y, Lt[1].x + Lt[1].y);
+            const float2 y = __fadd2_rn(L, make_float2(-Ct.x, -Ct.y));
+            const float2 t = __fadd2_rn(Rt, y);
+            Ct = __fadd2_rn(__fadd2_rn(t, make_float2(-Rt.x, -Rt.y)), make_float2(-y.x, -y.y));
+            Rt = t;
+        }
+    }
+    if (cur_blk >= 0) flush(cur_blk);
+    // all MMAs of this warpgroup completed (dfull of the last tile was awaited); release TMEM
+    tc_fence_before();
+    named_bar_sync(1, kTcNCW * 32);
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)kTcCols)
+                     : "memory");
+    }
+}
+
 // ---- merge: log-sum-exp over partials + outlier term → 16-float record -------------------
 __global__ void estep_merge_kernel(const float* __restrict__ part, int64_t N, const IterState* __restrict__ st,
                                    Sched sc, float* __restrict__ rec) {
@@ -448,7 +825,7 @@ struct Variant {
     {P, W, B, X, {(const void*)estep_kernel<P, W, B, X, false>, (const void*)estep_kernel<P, W, B, X, true>}}
 static const Variant kVariants[] = {
     LSG_VARIANT(2, 16, 1, true), LSG_VARIANT(2, 8, 2, true), LSG_VARIANT(4, 8, 1, true), LSG_VARIANT(2, 12, 1, true),
-    LSG_VARIANT(4, 4, 2, true),  LSG_VARIANT(2, 8, 2, false), LSG_VARIANT(1, 16, 1, false),
+    LSG_VARIANT(4, 4, 2, true),  LSG_VARIANT(2, 8, 2, false), LSG_VARIANT(1, 16, 1, false), LSG_VARIANT(2, 16, 1, true),
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 3;   // packed, 2 points/thread, 12 consumer warps (tools/estep_speed.py)
@@ -458,12 +835,20 @@ static int variant_index() {
     int v = e ? atoi(e) : kDefaultVariant;
     return (v >= 0 && v < kNumVariants) ? v : kDefaultVariant;
 }
+// Tensor-core E step (fixed-max mode) paired with CUDA-core variant 3 (same block of 768 points) for
+// the running-max mode.  LSGCPD_TC=0 disables it.
+static bool tc_enabled() {
+    const char* e = getenv("LSGCPD_TC");
+    return e ? atoi(e) != 0 : true;
+}
+constexpr int kTcPairVariant = 0;   // CUDA-core kernel with the same 1024-point blocks
 
 static int g_num_sms = 0;
 static int g_occ[kNumVariants] = {0};
 
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
-    const int vi = variant_index();
+    const bool tc = tc_enabled();
+    const int vi = tc ? kTcPairVariant : variant_index();
     const Variant& V = kVariants[vi];
     if (g_num_sms == 0) {
         int dev;
@@ -476,12 +861,12 @@ int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
         g_occ[vi] = occ > 0 ? occ : 1;
     }
     Sched s;
-    s.variant = vi;
+    s.variant = tc ? -1 - vi : vi;   // negative: tensor-core kernel + CUDA-core variant for running max
     s.B = (int64_t)V.ppt * V.ncw * 32;
     s.nblk = (N + s.B - 1) / s.B;
     s.T = M_pad / kTT;
     s.U = s.nblk * s.T;
-    const int64_t slots = (int64_t)g_num_sms * g_occ[vi];
+    const int64_t slots = (int64_t)g_num_sms * (tc ? 1 : g_occ[vi]);   // the TC kernel holds all TMEM: 1 CTA/SM
     s.G = s.U < slots ? s.U : slots;
     if (s.G < 1) s.G = 1;
     int64_t kmax = 1;
@@ -506,9 +891,25 @@ void estep_launch_setup(IterState* st, const void* d_target, const double* R, co
 void estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
                   float* part, float* rec, int consistent, cudaStream_t stream) {
     const float* body = target_body(d_target);
-    const Variant& V = kVariants[sc.variant];
+    const bool tc = sc.variant < 0;
+    const Variant& V = kVariants[tc ? -1 - sc.variant : sc.variant];
     Sched scv = sc;
-    void* args[] = {(void*)&body, (void*)&d_src, (void*)&N, (void*)&st, (void*)&scv, (void*)&part};
+    int skip_fixed = tc ? 1 : 0;
+    void* args[] = {(void*)&body, (void*)&d_src, (void*)&N, (void*)&st, (void*)&scv, (void*)&part, (void*)&skip_fixed};
+    if (tc) {
+        const int64_t M_pad = sc.T * kTT;
+        const char* tcb = reinterpret_cast<const char*>(target_tc(d_target, M_pad));
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(estep_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+            cudaFuncSetAttribute(estep_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+            attr_set = true;
+        }
+        if (consistent)
+            estep_tc_kernel<false><<<(unsigned)sc.G, kTcThreads, kTcSmem, stream>>>(tcb, d_src, N, st, sc, part);
+        else
+            estep_tc_kernel<true><<<(unsigned)sc.G, kTcThreads, kTcSmem, stream>>>(tcb, d_src, N, st, sc, part);
+    }
     cudaLaunchKernel(V.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3((V.ncw + 1) * 32), args, 0, stream);
     const int mt = 256;
     estep_merge_kernel<<<(unsigned)((N + mt - 1) / mt), mt, 0, stream>>>(part, N, st, sc, rec);

@@ -120,6 +120,53 @@ __global__ void pack_body_kernel(const float* __restrict__ xyz, const float* __r
     for (int i = 0; i < kTgtFloats; ++i) o[2 * i] = f[i];
 }
 
+// Tensor-core section: core fields and the hi/lo TF32 feature blocks (see common.cuh).
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+__global__ void pack_tc_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm,
+                               const float* __restrict__ alpha, int64_t M, int64_t M_pad,
+                               const double* __restrict__ stats2, float* __restrict__ tc) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M_pad) return;
+    const int64_t tile = m / kTcTile;
+    const int jt = (int)(m % kTcTile);
+    char* base = reinterpret_cast<char*>(tc) + tile * kTcTileBytes;
+    // core section, pair-interleaved: targets (2i, 2i+1) share 64 B = {f_2i, f_2i+1} for f = 0..7
+    float* core = reinterpret_cast<float*>(base) + (jt >> 1) * 16 + (jt & 1);
+    float cf[8];
+    float F[16];
+    for (int i = 0; i < 16; ++i) F[i] = 0.f;
+    if (m >= M) {
+        cf[0] = cf[1] = cf[2] = 1e18f;
+        cf[3] = -INFINITY;
+        cf[4] = cf[5] = cf[6] = cf[7] = 0.f;
+    } else {
+        const double y0 = xyz[3 * m], y1 = xyz[3 * m + 1], y2 = xyz[3 * m + 2];
+        const double n0 = nrm[3 * m], n1 = nrm[3 * m + 1], n2 = nrm[3 * m + 2];
+        const double a = alpha[m];
+        const double sa = sqrt(a);
+        const double ny = n0 * y0 + n1 * y1 + n2 * y2;
+        cf[0] = (float)y0; cf[1] = (float)y1; cf[2] = (float)y2;
+        cf[3] = (float)(0.5 * log2(1.0 + a) - stats2[0]);
+        cf[4] = (float)(sa * n0); cf[5] = (float)(sa * n1); cf[6] = (float)(sa * n2); cf[7] = 0.f;
+        F[0] = 1.f; F[1] = (float)y0; F[2] = (float)y1; F[3] = (float)y2;
+        F[4] = (float)(a * n0 * n0); F[5] = (float)(a * n0 * n1); F[6] = (float)(a * n0 * n2);
+        F[7] = (float)(a * n1 * n1); F[8] = (float)(a * n1 * n2); F[9] = (float)(a * n2 * n2);
+        F[10] = (float)(a * ny * n0); F[11] = (float)(a * ny * n1); F[12] = (float)(a * ny * n2);
+    }
+    for (int f = 0; f < 8; ++f) core[2 * f] = cf[f];
+    const int s = jt / 8, j = jt % 8;
+    for (int f = 0; f < 16; ++f) {
+        const int off = kTcBOff + 1024 * s + (f / 8) * 256 + (j / 4) * 128 + (f % 8) * 16 + (j % 4) * 4;
+        const float hi = tf32_rna(F[f]);
+        *reinterpret_cast<float*>(base + off) = hi;              // rows 0-15 of the K-step block: F_hi
+        *reinterpret_cast<float*>(base + off + 512) = F[f] - hi; // rows 16-31: F_lo
+    }
+}
+
 // ---- grid kNN ------------------------------------------------------------------------------------
 struct Grid {
     double lo[3];
@@ -359,6 +406,8 @@ static int finish_target(const float* d_xyz, const float* nrm, const float* alph
     const int64_t M_pad = pad_targets(M);
     pack_body_kernel<<<(unsigned)((M_pad + 255) / 256), 256, 0, stream>>>(d_xyz, nrm, alpha, M, M_pad, st2,
                                                                           target_body(d_target));
+    pack_tc_kernel<<<(unsigned)((M_pad + 255) / 256), 256, 0, stream>>>(d_xyz, nrm, alpha, M, M_pad, st2,
+                                                                        target_tc(d_target, M_pad));
     LSG_CUDA(cudaGetLastError());
     TargetHeader h;
     LSG_CUDA(cudaMemcpyAsync(&h, hdr, sizeof(h), cudaMemcpyDeviceToHost, stream));

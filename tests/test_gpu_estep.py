@@ -119,11 +119,24 @@ def test_estep_invalid_arguments_raise():
         lsg.estep(tgt, X, np.eye(3), np.array([np.nan, 0, 0]), 1e-3, 0.1, V)
 
 
-@pytest.mark.parametrize("variant", range(7))
+@pytest.mark.parametrize("variant", range(8))
 def test_estep_every_kernel_variant(variant, monkeypatch):
-    # every compiled kernel variant (scalar / packed f32x2, points per thread, warps) gives the same record
+    # every compiled CUDA-core kernel variant (scalar / packed f32x2, points per thread, warps), with the
+    # tensor-core kernel disabled, gives the same record
+    monkeypatch.setenv("LSGCPD_TC", "0")
     monkeypatch.setenv("LSGCPD_ESTEP_VARIANT", str(variant))
     wl, n32, a32, V, ext = oracle_target32("tiny")
     for w in (0.0, 0.1):
         rec, ora = _run_pair(wl.target, n32, a32, wl.source, wl.R_expected, wl.t_expected, 1e-4, w, V)
         assert_record_parity(rec, ora, wl.target, a32, what=f"variant {variant} w={w}")
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_estep_tensor_core_and_cuda_core_paths(tc, monkeypatch):
+    # default path = tcgen05 kernel (fixed max) + CUDA-core kernel (running max); LSGCPD_TC=0 = CUDA cores only
+    monkeypatch.setenv("LSGCPD_TC", tc)
+    for name in ("tiny", "object"):
+        wl, n32, a32, V, ext = oracle_target32(name)
+        for w, s2 in ((wl.w, 1e-3), (wl.w, 1e-5), (0.0, 1e-4)):
+            rec, ora = _run_pair(wl.target, n32, a32, wl.source, wl.R_expected, wl.t_expected, s2, w, V)
+            assert_record_parity(rec, ora, wl.target, a32, what=f"tc={tc} {name} w={w} s2={s2}")

@@ -19,7 +19,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblsgcpd.so")
+LIB_PATH = os.environ.get("LSGCPD_LIB") or os.path.join(_HERE, "liblsgcpd.so")
 
 REC = 16
 REC_P, REC_PY, REC_A, REC_B, REC_D, REC_LNP, REC_POUT = 0, 1, 4, 10, 13, 14, 15

@@ -190,7 +190,8 @@ struct Sched {
     int64_t nblk;     // source blocks
     int64_t kmax;     // max CTAs touching one source block (partial slots per block)
     int64_t B;        // source points per block
-    int variant;      // E-step kernel variant
+    int variant;      // E-step kernel variant (negative: tensor-core kernel + CUDA-core variant -1-variant)
+    int tc_variant;   // tensor-core kernel configuration
 };
 __host__ __device__ inline int64_t sched_start(const Sched& s, int64_t g) { return g * s.U / s.G; }
 __host__ __device__ inline int64_t sched_owner(const Sched& s, int64_t u) { return ((u + 1) * s.G - 1) / s.U; }

@@ -394,16 +394,21 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
 // Kahan-folded after every 64-target tile (FP32 error independent of M).  Fixed-max mode only; the
 // running-max mode (w = 0 or tiny w) is served by the CUDA-core kernel.
 constexpr int kTcStages = 4;
-constexpr int kTcWG = 4;                      // consumer warpgroups (128 TMEM lanes each)
-constexpr int kTcNCW = 4 * kTcWG;
-constexpr int kTcMW = 2;                      // MMA-issuing warps (each serves kTcWG / kTcMW warpgroups)
-constexpr int kTcThreads = (kTcNCW + 1 + kTcMW) * 32;   // + TMA producer warp + MMA warps
-constexpr int kTcCols = 512;                  // TMEM columns allocated
-constexpr int kTcWGCols = 128;                // per warpgroup: D 2 row blocks × 32 + A 2 buffers × (2 × 16)
+constexpr int kTcCols = 512;                  // TMEM columns allocated (the whole TMEM: base column 0)
 constexpr int kTcChunk = 8;                   // targets per A buffer (one K step)
-// dynamic shared memory: target stages + Kahan running sums (R, C) of the 13 TC features per thread
-constexpr size_t kTcSmemRC = (size_t)26 * kTcNCW * 32 * sizeof(float2);
-constexpr size_t kTcSmem = kTcSmemRC;   // dynamic part (the stages are static shared memory)
+// TC kernel configuration: NWG consumer warpgroups (128 TMEM lanes each), RB row blocks (points) per
+// thread, MW MMA-issuing warps.  TMEM per warpgroup: RB × (D 32 + A 2 buffers × 16) = 64·RB columns.
+template <int NWG, int RB, int MW>
+struct TcCfg {
+    static constexpr int kNCW = 4 * NWG;
+    static constexpr int kThreads = (kNCW + 1 + MW) * 32;
+    static constexpr int kWGCols = 64 * RB;
+    static constexpr int kBlk = NWG * 128 * RB;
+    static constexpr size_t kSmem = (size_t)26 * kNCW * 32 * RB * sizeof(float);   // Kahan R, C
+    static_assert(NWG * kWGCols <= kTcCols, "TMEM columns");
+    static_assert(kThreads <= 1024, "threads");
+    static_assert(NWG % MW == 0, "MMA warps must split the warpgroups evenly");
+};
 // instruction descriptors: D F32, A/B TF32, K-major A and B, M = 128, N = 32 ([hi | lo] features) or 16
 constexpr uint32_t kTcIdesc32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
 constexpr uint32_t kTcIdesc16 = (1u << 4) | (2u << 7) | (2u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
@@ -420,6 +425,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
         "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
         "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
+}
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, float2 v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(__float_as_uint(v.x)),
+                 "r"(__float_as_uint(v.y))
+                 : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile(
@@ -464,27 +474,28 @@ __device__ __forceinline__ uint64_t bdesc(uint32_t saddr) {
            ((uint64_t)1 << 46);
 }
 
-// Warp roles: 16 consumer warps (4 warpgroups × 128 TMEM lanes), 1 TMA producer warp, 2 MMA warps.
+// Warp roles: 4·NWG consumer warps (NWG warpgroups × 128 TMEM lanes), 1 TMA producer warp, MW MMA warps.
 // Per warpgroup mbarriers: afull[b] (4 warp arrivals: A buffer b written), aempty[b] (MMA commit: buffer
 // b consumed), dfull (commit after a tile's last MMAs: D ready), dfree (4 arrivals: D drained).
 // The running Kahan sums live in shared memory (touched once per tile), leaving registers for
 // in-flight pairs: the kernel is latency-bound on the τ → e → ex2 chain, so warps matter.
-template <bool kLiteral>
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int NWG, int RB, int MW, bool kLiteral>
+__global__ void __launch_bounds__(TcCfg<NWG, RB, MW>::kThreads, 1)
     estep_tc_kernel(const char* __restrict__ tc, const float* __restrict__ src, int64_t N,
                     const IterState* __restrict__ st, Sched sc, float* __restrict__ part) {
-    constexpr int PPT = 2;
-    constexpr int kBlk = kTcNCW * 32 * PPT;   // 1024
+    using Cfg = TcCfg<NWG, RB, MW>;
+    constexpr int kNCW = Cfg::kNCW;
+    constexpr int kBlk = Cfg::kBlk;
+    constexpr int kWGCols = Cfg::kWGCols;
     constexpr int kChunks = kTcTile / kTcChunk;
-    // static shared memory for the TMA stages (link-time constant addresses: the MMA warp's B
+    // static shared memory for the TMA stages (link-time constant addresses: the MMA warps' B
     // descriptors become immediates); dynamic shared memory for the Kahan running sums
     __shared__ __align__(1024) char tiles_st[kTcStages][kTcTileBytes];
-    char* tiles = &tiles_st[0][0];
     extern __shared__ __align__(16) char dsmem[];
-    float2* smRC = reinterpret_cast<float2*>(dsmem);   // [26][consumer threads]
+    float* smRC = reinterpret_cast<float*>(dsmem);   // [26][RB × consumer threads]
     __shared__ __align__(8) uint64_t full_bar[kTcStages];
     __shared__ __align__(8) uint64_t empty_bar[kTcStages];
-    __shared__ __align__(8) uint64_t afull[kTcWG][2], aempty[kTcWG][2], dfull[kTcWG], dfree[kTcWG];
+    __shared__ __align__(8) uint64_t afull[NWG][2], aempty[NWG][2], dfull[NWG], dfree[NWG];
     __shared__ uint32_t tmem_base_sh;
 
     if (!st->active || !st->fixed) return;
@@ -503,9 +514,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (threadIdx.x == 32) {
         for (int s = 0; s < kTcStages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], kTcNCW);
+            mbar_init(&empty_bar[s], kNCW);
         }
-        for (int w = 0; w < kTcWG; ++w) {
+        for (int w = 0; w < NWG; ++w) {
             mbar_init(&afull[w][0], 4);
             mbar_init(&afull[w][1], 4);
             mbar_init(&aempty[w][0], 1);
@@ -521,7 +532,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint32_t tmem = tmem_base_sh;
     if (tmem != 0u) __trap();   // 512 columns = the whole TMEM: the allocation must start at lane 0, column 0
 
-    if (warp == kTcNCW) {
+    if (warp == kNCW) {
         // ---------------- producer warp: TMA bulk copies of 10-KB tensor-core tiles ----------------
         if (lane == 0) {
             int64_t it = 0;
@@ -531,19 +542,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 mbar_wait_sleep(&empty_bar[s], ph ^ 1);
                 const int64_t tile = u % sc.T;
                 mbar_arrive_expect_tx(&full_bar[s], kTcTileBytes);
-                bulk_g2s(tiles + s * kTcTileBytes, tc + tile * (int64_t)kTcTileBytes, kTcTileBytes, &full_bar[s]);
+                bulk_g2s(&tiles_st[s][0], tc + tile * (int64_t)kTcTileBytes, kTcTileBytes, &full_bar[s]);
             }
         }
         return;
     }
-    if (warp > kTcNCW) {
+    if (warp > kNCW) {
         // ---------------- MMA warps: warp-uniform loop, one elected lane issues tcgen05.mma ----------------
         // per warpgroup w, row block rb, K step c:  D[:, 0:32] (+)= A_hi · [F_hi | F_lo]   (N = 32)
         //                                           D[:, 0:16]  += A_lo · F_hi             (N = 16)
-        // The CTA owns all 512 TMEM columns, so the allocation starts at column 0 (checked above) and every
-        // TMEM operand is a compile-time constant; only the stage's B descriptor varies (warp-uniform).
-        const int mw = warp - kTcNCW - 1;
-        constexpr int kWPer = kTcWG / kTcMW;
+        // The CTA owns all 512 TMEM columns, so every TMEM operand is a compile-time constant.
+        const int mw = warp - kNCW - 1;
+        constexpr int kWPer = NWG / MW;
         uint32_t aph[kWPer][2] = {}, fph[kWPer] = {};
         for (int64_t ub = u0; ub < u1; ub += kTcStages) {
             const uint32_t round_ph = (uint32_t)(((ub - u0) / kTcStages) & 1);
@@ -566,10 +576,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         aph[wi][buf] ^= 1u;
                         tc_fence_after();
                         if (elect_one()) {
-                            const uint32_t colD = (uint32_t)(w * kTcWGCols);
-                            const uint32_t colA = colD + 64 + buf * 32;
+                            const uint32_t colD = (uint32_t)(w * kWGCols);
+                            const uint32_t colA = colD + 32 * RB + buf * 16 * RB;
 #pragma unroll
-                            for (int rb = 0; rb < 2; ++rb) {
+                            for (int rb = 0; rb < RB; ++rb) {
                                 mma_tf32_ts(colD + rb * 32, colA + rb * 16, b32, kTcIdesc32, c == 0 ? 0u : 1u);
                                 mma_tf32_ts(colD + rb * 32, colA + rb * 16 + 8, b32, kTcIdesc16, 1u);
                             }
@@ -585,15 +595,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
 
     // ---------------- consumers: warpgroup wg, TMEM lane quadrant q ----------------
-    // Each thread owns one point in each of the two 128-row blocks; f32x2 instructions cover two
-    // consecutive TARGETS, so {p_m, p_m+1} pairs land directly in consecutive A columns of TMEM.
+    // Each thread owns one point in each of its RB 128-row blocks; f32x2 instructions cover two
+    // consecutive TARGETS, so {p_m, p_m+1} pairs go straight into consecutive A columns of TMEM.
     const int wg = warp >> 2, q = warp & 3;
     const int tw = q * 32 + lane;                      // thread (= TMEM lane) within the warpgroup
     const int tid = threadIdx.x;                       // consumer thread id (smem column)
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t colA0 = (uint32_t)(wg * kTcWGCols) + 64, colD0 = (uint32_t)(wg * kTcWGCols);
-    const uint32_t afull_a[2] = {smem_u32(&afull[wg][0]), smem_u32(&afull[wg][1])};
+    const uint32_t colD0 = (uint32_t)(wg * kWGCols), colA0 = colD0 + 32 * RB;
     const uint32_t aempty_a[2] = {smem_u32(&aempty[wg][0]), smem_u32(&aempty[wg][1])};
+    const uint32_t afull_a[2] = {smem_u32(&afull[wg][0]), smem_u32(&afull[wg][1])};
     const float k2 = st->k2;
     const float2 nk2 = bc(-k2);
     double Rm[9], tv[3];
@@ -602,18 +612,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
     for (int i = 0; i < 3; ++i) tv[i] = st->t[i];
 
-    float h[2][3], l[2][3];
-    float2 Rt, Ct;
+    float h[RB][3], l[RB][3];
+    float Rt[RB], Ct[RB];
     int64_t cur_blk = -1;
     uint32_t eph[2] = {0u, 0u}, dph = 0u;
     bool used[2] = {false, false};
     uint32_t cc = 0;
-    constexpr int kRC = kTcNCW * 32;
+    constexpr int kRC = kNCW * 32 * RB;
 
     auto load_points = [&](int64_t j) {
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int64_t n = j * kBlk + wg * 256 + k * 128 + tw;
+        for (int k = 0; k < RB; ++k) {
+            const int64_t n = j * kBlk + (wg * RB + k) * 128 + tw;
             double x0 = 0.0, x1 = 0.0, x2 = 0.0;
             if (n < N) {
                 x0 = src[3 * n];
@@ -628,24 +638,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 h[k][a] = __double2float_rn(X[a]);
                 l[k][a] = __double2float_rn(X[a] - (double)h[k][a]);
             }
-        }
+            Rt[k] = Ct[k] = 0.f;
 #pragma unroll
-        for (int f = 0; f < 26; ++f) smRC[f * kRC + tid] = make_float2(0.f, 0.f);
-        Rt = Ct = make_float2(0.f, 0.f);
+            for (int f = 0; f < 26; ++f) smRC[f * kRC + k * (kNCW * 32) + tid] = 0.f;
+        }
     };
     auto flush = [&](int64_t j) {
         const int64_t slot = j * sc.kmax + (g - sched_owner(sc, j * sc.T));
         float* base = part + slot * (int64_t)kPartF * kBlk;
 #pragma unroll
-        for (int f = 0; f < 13; ++f) {
-            const float2 R = smRC[f * kRC + tid], C = smRC[(13 + f) * kRC + tid];
-            base[f * kBlk + wg * 256 + tw] = __fsub_rn(R.x, C.x);
-            base[f * kBlk + wg * 256 + 128 + tw] = __fsub_rn(R.y, C.y);
-        }
+        for (int k = 0; k < RB; ++k) {
+            const int b = (wg * RB + k) * 128 + tw;
+            const int rc = k * (kNCW * 32) + tid;
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int b = wg * 256 + k * 128 + tw;
-            base[13 * kBlk + b] = __fsub_rn(lane_of(Rt, k), lane_of(Ct, k));
+            for (int f = 0; f < 13; ++f) base[f * kBlk + b] = __fsub_rn(smRC[f * kRC + rc], smRC[(13 + f) * kRC + rc]);
+            base[13 * kBlk + b] = __fsub_rn(Rt[k], Ct[k]);
             base[14 * kBlk + b] = 0.f;
             base[15 * kBlk + b] = 0.f;
         }
@@ -661,8 +668,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         const int s = (int)(it % kTcStages);
         mbar_wait(&full_bar[s], (uint32_t)((it / kTcStages) & 1));
-        const float4* core = reinterpret_cast<const float4*>(tiles + s * kTcTileBytes);
-        float2 Lt[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};   // Σ p τ, {even, odd} targets
+        const float4* core = reinterpret_cast<const float4*>(&tiles_st[s][0]);
+        float2 Lt[RB];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) Lt[k] = make_float2(0.f, 0.f);   // Σ p τ, {even, odd} targets
 #pragma unroll 1
         for (int c = 0; c < kChunks; ++c, ++cc) {
             const int buf = (int)(cc & 1u);
@@ -680,14 +689,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tc_fence_after();
             }
             used[buf] = true;
+#ifdef LSG_TC_DIAG
+            float2 sink = make_float2(0.f, 0.f);
+#endif
 #pragma unroll
-            for (int rb = 0; rb < 2; ++rb) {
-                float2 hi[4], lo[4];
+            for (int pp = 0; pp < 4; ++pp) {
+                const int pr = c * 4 + pp;   // target pair within the tile
+                const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
+                // v0 = {y0a, y0b, y1a, y1b}, v1 = {y2a, y2b, ωa, ωb}, v2 = {n0a, n0b, n1a, n1b}, v3 = {n2a, n2b, -, -}
 #pragma unroll
-                for (int pp = 0; pp < 4; ++pp) {
-                    const int pr = c * 4 + pp;   // target pair within the tile
-                    const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
-                    // v0 = {y0a, y0b, y1a, y1b}, v1 = {y2a, y2b, ωa, ωb}, v2 = {n0a, n0b, n1a, n1b}, v3 = {n2a, n2b, -, -}
+                for (int rb = 0; rb < RB; ++rb) {
                     const float2 rx = __fadd2_rn(__fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y)), bc(l[rb][0]));
                     const float2 ry = __fadd2_rn(__fadd2_rn(bc(h[rb][1]), make_float2(-v0.z, -v0.w)), bc(l[rb][1]));
                     const float2 rz = __fadd2_rn(__fadd2_rn(bc(h[rb][2]), make_float2(-v1.x, -v1.y)), bc(l[rb][2]));
@@ -698,20 +709,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     const float2 e = kLiteral ? __fmul2_rn(nk2, tau) : __ffma2_rn(nk2, tau, make_float2(v1.z, v1.w));
                     const float2 p = make_float2(ex2_approx(e.x), ex2_approx(e.y));
                     Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
-                    hi[pp] = make_float2(__uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
-                                         __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
-                    lo[pp] = __fadd2_rn(p, make_float2(-hi[pp].x, -hi[pp].y));
+                    const float2 hi = make_float2(__uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
+                                                  __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
+                    const float2 lo = __fadd2_rn(p, make_float2(-hi.x, -hi.y));
+                    // row block rb, A columns: [hi of targets 0-7 | lo of targets 0-7] of this K step
+#ifdef LSG_TC_DIAG
+                    sink = __fadd2_rn(sink, __fadd2_rn(hi, lo));
+#else
+                    tmem_st2(tl + colA0 + buf * 16 * RB + rb * 16 + 2 * pp, hi);
+                    tmem_st2(tl + colA0 + buf * 16 * RB + rb * 16 + 8 + 2 * pp, lo);
+#endif
                 }
-                const uint32_t va[16] = {__float_as_uint(hi[0].x), __float_as_uint(hi[0].y), __float_as_uint(hi[1].x),
-                                         __float_as_uint(hi[1].y), __float_as_uint(hi[2].x), __float_as_uint(hi[2].y),
-                                         __float_as_uint(hi[3].x), __float_as_uint(hi[3].y), __float_as_uint(lo[0].x),
-                                         __float_as_uint(lo[0].y), __float_as_uint(lo[1].x), __float_as_uint(lo[1].y),
-                                         __float_as_uint(lo[2].x), __float_as_uint(lo[2].y), __float_as_uint(lo[3].x),
-                                         __float_as_uint(lo[3].y)};
-                tmem_st16(tl + colA0 + buf * 32 + rb * 16, va);   // row block rb: [hi 0-7 | lo 0-7]
             }
+#ifdef LSG_TC_DIAG
+            Lt[0].x += sink.x + sink.y;
+#else
             tmem_wait_st();
             tc_fence_before();
+#endif
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(afull_a[buf]) : "memory");
         }
@@ -719,11 +734,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         mbar_wait(&dfull[wg], dph);
         dph ^= 1u;
         tc_fence_after();
-        uint32_t d0[16], d0l[16], d1[16], d1l[16];
-        tmem_ld16(tl + colD0, d0);          // row block 0: hi·hi + lo·hi
-        tmem_ld16(tl + colD0 + 16, d0l);    //              hi·lo
-        tmem_ld16(tl + colD0 + 32, d1);     // row block 1
-        tmem_ld16(tl + colD0 + 48, d1l);
+        uint32_t dh[RB][16], dl[RB][16];
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+            tmem_ld16(tl + colD0 + rb * 32, dh[rb]);        // hi·hi + lo·hi
+            tmem_ld16(tl + colD0 + rb * 32 + 16, dl[rb]);   // hi·lo
+        }
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -732,28 +748,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_arrive(&empty_bar[s]);
         }
 #pragma unroll
-        for (int f = 0; f < 13; ++f) {
-            float2 R = smRC[f * kRC + tid], C = smRC[(13 + f) * kRC + tid];
-            const float2 L = make_float2(__uint_as_float(d0[f]) + __uint_as_float(d0l[f]),
-                                         __uint_as_float(d1[f]) + __uint_as_float(d1l[f]));
-            const float2 y = __fadd2_rn(L, make_float2(-C.x, -C.y));
-            const float2 t = __fadd2_rn(R, y);
-            C = __fadd2_rn(__fadd2_rn(t, make_float2(-R.x, -R.y)), make_float2(-y.x, -y.y));
-            smRC[f * kRC + tid] = t;
-            smRC[(13 + f) * kRC + tid] = C;
-        }
-        {
-            const float2 L = make_float2(Lt[0].x + Lt[0].y, Lt[1].x + Lt[1].y);
-            const float2 y = __fadd2_rn(L, make_float2(-Ct.x, -Ct.y));
-            const float2 t = __fadd2_rn(Rt, y);
-            Ct = __fadd2_rn(__fadd2_rn(t, make_float2(-Rt.x, -Rt.y)), make_float2(-y.x, -y.y));
-            Rt = t;
+        for (int rb = 0; rb < RB; ++rb) {
+            const int rc = rb * (kNCW * 32) + tid;
+#pragma unroll
+            for (int f = 0; f < 13; ++f) {
+                const float L = __uint_as_float(dh[rb][f]) + __uint_as_float(dl[rb][f]);
+                const float R = smRC[f * kRC + rc], C = smRC[(13 + f) * kRC + rc];
+                const float y = L - C;
+                const float t = R + y;
+                smRC[(13 + f) * kRC + rc] = (t - R) - y;
+                smRC[f * kRC + rc] = t;
+            }
+            const float L = Lt[rb].x + Lt[rb].y;
+            const float y = L - Ct[rb];
+            const float t = Rt[rb] + y;
+            Ct[rb] = (t - Rt[rb]) - y;
+            Rt[rb] = t;
         }
     }
     if (cur_blk >= 0) flush(cur_blk);
     // all MMAs of this warpgroup completed (dfull of the last tile was awaited); release TMEM
     tc_fence_before();
-    named_bar_sync(1, kTcNCW * 32);
+    named_bar_sync(1, kNCW * 32);
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)kTcCols)
@@ -826,6 +842,7 @@ struct Variant {
 static const Variant kVariants[] = {
     LSG_VARIANT(2, 16, 1, true), LSG_VARIANT(2, 8, 2, true), LSG_VARIANT(4, 8, 1, true), LSG_VARIANT(2, 12, 1, true),
     LSG_VARIANT(4, 4, 2, true),  LSG_VARIANT(2, 8, 2, false), LSG_VARIANT(1, 16, 1, false), LSG_VARIANT(2, 16, 1, true),
+    LSG_VARIANT(2, 14, 1, true), LSG_VARIANT(2, 8, 1, true),
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 3;   // packed, 2 points/thread, 12 consumer warps (tools/estep_speed.py)
@@ -835,20 +852,46 @@ static int variant_index() {
     int v = e ? atoi(e) : kDefaultVariant;
     return (v >= 0 && v < kNumVariants) ? v : kDefaultVariant;
 }
-// Tensor-core E step (fixed-max mode) paired with CUDA-core variant 3 (same block of 768 points) for
-// the running-max mode.  LSGCPD_TC=0 disables it.
+// Tensor-core E step (fixed-max mode) paired with a CUDA-core variant of the same block size for the
+// running-max mode.  LSGCPD_TC=0 disables it; LSGCPD_TC_VARIANT picks the configuration.
+struct TcVariant {
+    int nwg, rb, mw, pair_variant;
+    int threads, blk;
+    size_t smem;
+    const void* fn[2];
+};
+#define LSG_TC(NWG, RB, MW, PV)                                                                           \
+    {NWG, RB, MW, PV, TcCfg<NWG, RB, MW>::kThreads, TcCfg<NWG, RB, MW>::kBlk, TcCfg<NWG, RB, MW>::kSmem, \
+     {(const void*)estep_tc_kernel<NWG, RB, MW, false>, (const void*)estep_tc_kernel<NWG, RB, MW, true>}}
+static const TcVariant kTcVariants[] = {
+    LSG_TC(4, 2, 2, 0),   // 16 consumer warps, 2 points/thread (1024-point blocks) — CUDA-core variant 0
+    LSG_TC(6, 1, 2, 3),   // 24 consumer warps, 1 point/thread (768) — variant 3
+    LSG_TC(7, 1, 1, 8),   // 28 consumer warps (896) — variant 8
+    LSG_TC(4, 1, 2, 9),   // 16 consumer warps, 1 point/thread (512) — variant 9
+    LSG_TC(4, 2, 4, 0),   // as 0 with one MMA warp per warpgroup
+    LSG_TC(4, 2, 1, 0),   // as 0 with a single MMA warp
+    LSG_TC(2, 4, 1, 0),   // 8 consumer warps, 4 points/thread (1024)
+    LSG_TC(3, 2, 1, 3),   // 12 consumer warps, 2 points/thread (768)
+};
+constexpr int kNumTcVariants = sizeof(kTcVariants) / sizeof(kTcVariants[0]);
 static bool tc_enabled() {
     const char* e = getenv("LSGCPD_TC");
     return e ? atoi(e) != 0 : true;
 }
-constexpr int kTcPairVariant = 0;   // CUDA-core kernel with the same 1024-point blocks
+constexpr int kDefaultTcVariant = 7;   // 12 consumer warps × 2 points, 1 MMA warp (tools/tc_check.py sweep)
+static int tc_variant_index() {
+    const char* e = getenv("LSGCPD_TC_VARIANT");
+    int v = e ? atoi(e) : kDefaultTcVariant;
+    return (v >= 0 && v < kNumTcVariants) ? v : kDefaultTcVariant;
+}
 
 static int g_num_sms = 0;
 static int g_occ[kNumVariants] = {0};
 
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
     const bool tc = tc_enabled();
-    const int vi = tc ? kTcPairVariant : variant_index();
+    const int tvi = tc_variant_index();
+    const int vi = tc ? kTcVariants[tvi].pair_variant : variant_index();
     const Variant& V = kVariants[vi];
     if (g_num_sms == 0) {
         int dev;
@@ -862,6 +905,7 @@ int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
     }
     Sched s;
     s.variant = tc ? -1 - vi : vi;   // negative: tensor-core kernel + CUDA-core variant for running max
+    s.tc_variant = tvi;
     s.B = (int64_t)V.ppt * V.ncw * 32;
     s.nblk = (N + s.B - 1) / s.B;
     s.T = M_pad / kTT;
@@ -899,16 +943,15 @@ void estep_launch(const void* d_target, const float* d_src, int64_t N, const Ite
     if (tc) {
         const int64_t M_pad = sc.T * kTT;
         const char* tcb = reinterpret_cast<const char*>(target_tc(d_target, M_pad));
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(estep_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-            cudaFuncSetAttribute(estep_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-            attr_set = true;
+        const TcVariant& TV = kTcVariants[sc.tc_variant];
+        static bool attr_set[kNumTcVariants] = {};
+        if (!attr_set[sc.tc_variant]) {
+            cudaFuncSetAttribute(TV.fn[0], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TV.smem);
+            cudaFuncSetAttribute(TV.fn[1], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TV.smem);
+            attr_set[sc.tc_variant] = true;
         }
-        if (consistent)
-            estep_tc_kernel<false><<<(unsigned)sc.G, kTcThreads, kTcSmem, stream>>>(tcb, d_src, N, st, sc, part);
-        else
-            estep_tc_kernel<true><<<(unsigned)sc.G, kTcThreads, kTcSmem, stream>>>(tcb, d_src, N, st, sc, part);
+        void* targs[] = {(void*)&tcb, (void*)&d_src, (void*)&N, (void*)&st, (void*)&scv, (void*)&part};
+        cudaLaunchKernel(TV.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3(TV.threads), targs, TV.smem, stream);
     }
     cudaLaunchKernel(V.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3((V.ncw + 1) * 32), args, 0, stream);
     const int mt = 256;

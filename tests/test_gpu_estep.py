@@ -131,10 +131,13 @@ def test_estep_every_kernel_variant(variant, monkeypatch):
         assert_record_parity(rec, ora, wl.target, a32, what=f"variant {variant} w={w}")
 
 
-@pytest.mark.parametrize("tc", ["1", "0"])
+@pytest.mark.parametrize("tc", ["1:0", "1:1", "1:2", "1:3", "1:4", "1:5", "1:6", "1:7", "0"])
 def test_estep_tensor_core_and_cuda_core_paths(tc, monkeypatch):
-    # default path = tcgen05 kernel (fixed max) + CUDA-core kernel (running max); LSGCPD_TC=0 = CUDA cores only
-    monkeypatch.setenv("LSGCPD_TC", tc)
+    # default path = tcgen05 kernel (fixed max) + CUDA-core kernel (running max); every tensor-core
+    # configuration (LSGCPD_TC_VARIANT) and LSGCPD_TC=0 (CUDA cores only)
+    on, _, tv = tc.partition(":")
+    monkeypatch.setenv("LSGCPD_TC", on)
+    monkeypatch.setenv("LSGCPD_TC_VARIANT", tv or "0")
     for name in ("tiny", "object"):
         wl, n32, a32, V, ext = oracle_target32(name)
         for w, s2 in ((wl.w, 1e-3), (wl.w, 1e-5), (0.0, 1e-4)):

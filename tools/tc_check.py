@@ -15,8 +15,10 @@ for cfg in os.environ.get("CFGS", "tiny,scale").split(","):
     idx = np.arange(wl.N) if wl.N <= 2000 else np.sort(rng.choice(wl.N, 64, replace=False))
     for s2 in (oracle.sigma2_init(wl.source, wl.target, wl.R_expected, wl.t_expected), 1e-3, 1e-5):
         ora = oracle.estep(wl.target, n.astype(np.float64), a.astype(np.float64), wl.source[idx], wl.R_expected, wl.t_expected, s2, wl.w, tgt.volume)
-        for tc in ("1", "0"):
-            os.environ["LSGCPD_TC"] = tc
+        for tc in os.environ.get("TCS", "1:0,0").split(","):
+            on, _, tv = tc.partition(":")
+            os.environ["LSGCPD_TC"] = on
+            os.environ["LSGCPD_TC_VARIANT"] = tv or "0"
             run = lsg.EstepRunner(tgt, X)
             run(wl.R_expected, wl.t_expected, s2, wl.w); torch.cuda.synchronize()
             err = record_errors(run.rec.cpu().numpy()[idx], ora, wl.target, a)

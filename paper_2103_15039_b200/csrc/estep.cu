@@ -789,19 +789,22 @@ __global__ void estep_merge_kernel(const float* __restrict__ part, int64_t N, co
     const int64_t g0 = sched_owner(sc, j * sc.T);
     const int64_t g1 = sched_owner(sc, (j + 1) * sc.T - 1);
     const int64_t nk = g1 - g0 + 1;
-    double mustar = st->Lo;  // -inf when w == 0
+    // reference max over the segments' maxima (all 0 in the fixed-max mode: no rescaling needed)
+    double mustar = -INFINITY;
     for (int64_t k = 0; k < nk; ++k) {
         const float* base = part + (j * sc.kmax + k) * (int64_t)kPartF * kB;
         mustar = fmax(mustar, (double)base[14 * kB + b]);
     }
+    if (st->w > 0.0) mustar = fmax(mustar, fmin(st->Lo, 0.0));   // keep the outlier term representable
     double a[kAcc];
 #pragma unroll
     for (int f = 0; f < kAcc; ++f) a[f] = 0.0;
     for (int64_t k = 0; k < nk; ++k) {
         const float* base = part + (j * sc.kmax + k) * (int64_t)kPartF * kB;
-        const double sc_k = exp2((double)base[14 * kB + b] - mustar);
+        const double muk = (double)base[14 * kB + b];
+        const double sc_k = (muk == mustar) ? 1.0 : exp2(muk - mustar);
 #pragma unroll
-        for (int f = 0; f < kAcc; ++f) a[f] += sc_k * (double)base[f * kB + b];
+        for (int f = 0; f < kAcc; ++f) a[f] = fma(sc_k, (double)base[f * kB + b], a[f]);
     }
     const double O = (st->w > 0.0) ? exp2(st->Lo - mustar) : 0.0;
     const double Z = a[0] + O;
@@ -842,7 +845,7 @@ struct Variant {
 static const Variant kVariants[] = {
     LSG_VARIANT(2, 16, 1, true), LSG_VARIANT(2, 8, 2, true), LSG_VARIANT(4, 8, 1, true), LSG_VARIANT(2, 12, 1, true),
     LSG_VARIANT(4, 4, 2, true),  LSG_VARIANT(2, 8, 2, false), LSG_VARIANT(1, 16, 1, false), LSG_VARIANT(2, 16, 1, true),
-    LSG_VARIANT(2, 14, 1, true), LSG_VARIANT(2, 8, 1, true),
+    LSG_VARIANT(2, 14, 1, true), LSG_VARIANT(2, 8, 1, true), LSG_VARIANT(2, 2, 8, true),
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 3;   // packed, 2 points/thread, 12 consumer warps (tools/estep_speed.py)
@@ -874,9 +877,10 @@ static const TcVariant kTcVariants[] = {
     LSG_TC(3, 2, 1, 3),   // 12 consumer warps, 2 points/thread (768)
 };
 constexpr int kNumTcVariants = sizeof(kTcVariants) / sizeof(kTcVariants[0]);
-static bool tc_enabled() {
+// LSGCPD_TC: unset = automatic (tensor cores unless the problem is too small), 0 = off, 1 = forced on
+static int tc_mode() {
     const char* e = getenv("LSGCPD_TC");
-    return e ? atoi(e) != 0 : true;
+    return e ? (atoi(e) != 0 ? 1 : 0) : 2;
 }
 constexpr int kDefaultTcVariant = 7;   // 12 consumer warps × 2 points, 1 MMA warp (tools/tc_check.py sweep)
 static int tc_variant_index() {
@@ -888,16 +892,28 @@ static int tc_variant_index() {
 static int g_num_sms = 0;
 static int g_occ[kNumVariants] = {0};
 
+constexpr int kSmallVariant = 10;   // 128-point blocks for problems too small to fill the GPU
+
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
-    const bool tc = tc_enabled();
     const int tvi = tc_variant_index();
-    const int vi = tc ? kTcVariants[tvi].pair_variant : variant_index();
-    const Variant& V = kVariants[vi];
+    const int mode = tc_mode();
+    bool tc = mode != 0;
+    int vi = tc ? kTcVariants[tvi].pair_variant : variant_index();
     if (g_num_sms == 0) {
         int dev;
         LSG_CUDA(cudaGetDevice(&dev));
         LSG_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
+    if (mode == 2 && !getenv("LSGCPD_ESTEP_VARIANT")) {
+        // small problems (tiny / object configs): too few (block, tile) units for one CTA per SM with the
+        // big blocks — use the small-block CUDA-core kernel so every SM gets work
+        const int64_t units_big = (N + kTcVariants[tvi].blk - 1) / kTcVariants[tvi].blk * (M_pad / kTT);
+        if (units_big < 2 * (int64_t)g_num_sms) {
+            tc = false;
+            vi = kSmallVariant;
+        }
+    }
+    const Variant& V = kVariants[vi];
     if (g_occ[vi] == 0) {
         int occ = 0;
         LSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.fn[0], (V.ncw + 1) * 32, 0));

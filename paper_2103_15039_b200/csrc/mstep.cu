@@ -234,107 +234,143 @@ __device__ inline bool chol_solve6(const double* A, double mu, const double* b, 
     return true;
 }
 
-__global__ void newton_kernel(IterState* st, const double* __restrict__ mom, RegParams rp, double* nll_trace,
-                              double* sigma2_trace, int* iters_done) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    IterState s = *st;
-    if (!s.active) return;
+// One warp: the dense algebra (v = U + 𝔾Δθ, J, 𝔾J, ∇, H) is spread over the lanes; the damping loop
+// (Cholesky 6×6, exp, candidate q) runs on lane 0.  All lanes end with identical state.
+__global__ void __launch_bounds__(32) newton_kernel(IterState* st, const double* __restrict__ mom, RegParams rp,
+                                                    double* nll_trace, double* sigma2_trace, int* iters_done) {
     __shared__ Mom mo;
-    build_mom(mo, mom);
+    __shared__ double S[21][16];
+    __shared__ double J[6][12], GJ[6][12], v[12], Bm[16], H[36], grad[6];
+    __shared__ double Rs[9], tsh[3], th_E[12];
+    __shared__ double q_cur, step_rot, step_trans;
+    __shared__ int stop;
+    const int lane = threadIdx.x;
+    const IterState s = *st;
+    if (!s.active) return;
+    for (int e = lane; e < 144; e += 32) {
+        const int r = e / 12, c = e % 12;
+        const int i = r / 4, a = r % 4, jj = c / 4, b = c % 4;
+        mo.GG[r][c] = mom[s3(i, jj) * 10 + s4(a, b)];
+    }
+    if (lane < 12) mo.U[lane] = mom[60 + lane];
+    if (lane < 21) {
+        int k = 0, l = 0, idx = 0;
+        for (k = 0; k < 6; ++k) {
+            for (l = k; l < 6; ++l, ++idx)
+                if (idx == lane) break;
+            if (idx == lane && l < 6) break;
+        }
+        double Ek[16], El[16], EE1[16], EE2[16];
+        basis4(k, Ek);
+        basis4(l, El);
+        mat4mul(Ek, El, EE1);
+        mat4mul(El, Ek, EE2);
+        for (int i = 0; i < 16; ++i) S[lane][i] = 0.5 * (EE1[i] + EE2[i]);
+    }
+    if (lane == 0) {
+        for (int i = 0; i < 9; ++i) Rs[i] = s.R[i];
+        for (int i = 0; i < 3; ++i) tsh[i] = s.t[i];
+        theta_of(s.R, s.t, th_E);
+        q_cur = 0.0;
+        step_rot = step_trans = 0.0;
+        stop = 0;
+    }
+    __syncwarp();
     const double sig2D = mom[72], sumP = mom[73], sumlnp = mom[74];
-    const double ntot = mom[75];  // total source points (appended by the host-side layout)
-    double th_E[12];
-    theta_of(s.R, s.t, th_E);
-    double R[9], t[3];
-    for (int i = 0; i < 9; ++i) R[i] = s.R[i];
-    for (int i = 0; i < 3; ++i) t[i] = s.t[i];
-    double q_cur = 0.0;
-    double E[6][16];
-    for (int k = 0; k < 6; ++k) basis4(k, E[k]);
-    double step_rot = 0.0, step_trans = 0.0;
+    const double ntot = mom[75];  // total source points (written by the σ²₀ kernel)
 
     for (int itn = 0; itn < rp.newton_max; ++itn) {
-        double th[12], dth[12], v[12];
-        theta_of(R, t, th);
+        double th[12], dth[12];
+        theta_of(Rs, tsh, th);
         for (int r = 0; r < 12; ++r) dth[r] = th[r] - th_E[r];
-        for (int r = 0; r < 12; ++r) {
+        const double Gt[16] = {Rs[0], Rs[1], Rs[2], tsh[0], Rs[3], Rs[4], Rs[5], tsh[1],
+                               Rs[6], Rs[7], Rs[8], tsh[2], 0, 0, 0, 1};
+        if (lane < 12) {
             double gr = 0.0;
-            for (int c = 0; c < 12; ++c) gr = fma(mo.GG[r][c], dth[c], gr);
-            v[r] = mo.U[r] + gr;                       // ½ ∇_θ q
-        }
-        double Gt[16] = {R[0], R[1], R[2], t[0], R[3], R[4], R[5], t[1], R[6], R[7], R[8], t[2], 0, 0, 0, 1};
-        double J[6][12];                               // dθ/dξ_k = (Θ̃ E_k)[0:3,:]
-        for (int k = 0; k < 6; ++k) {
-            double P4[16];
-            mat4mul(Gt, E[k], P4);
+            for (int c = 0; c < 12; ++c) gr = fma(mo.GG[lane][c], dth[c], gr);
+            v[lane] = mo.U[lane] + gr;                // ½ ∇_θ q
+        } else if (lane < 18) {
+            const int k = lane - 12;                  // dθ/dξ_k = (Θ̃ E_k)[0:3,:]
+            double Ek[16], P4[16];
+            basis4(k, Ek);
+            mat4mul(Gt, Ek, P4);
             for (int r = 0; r < 12; ++r) J[k][r] = P4[r];
         }
-        double grad[6], H[36];
-        double GJ[6][12];
-        for (int k = 0; k < 6; ++k) {
+        __syncwarp();
+        for (int e = lane; e < 72; e += 32) {         // 𝔾 J_k
+            const int k = e / 12, r = e % 12;
+            double a = 0.0;
+            for (int c = 0; c < 12; ++c) a = fma(mo.GG[r][c], J[k][c], a);
+            GJ[k][r] = a;
+        }
+        if (lane < 6) {
             double g = 0.0;
-            for (int r = 0; r < 12; ++r) g = fma(J[k][r], v[r], g);
-            grad[k] = g;
-            for (int r = 0; r < 12; ++r) {
-                double a = 0.0;
-                for (int c = 0; c < 12; ++c) a = fma(mo.GG[r][c], J[k][c], a);
-                GJ[k][r] = a;
-            }
+            for (int r = 0; r < 12; ++r) g = fma(J[lane][r], v[r], g);
+            grad[lane] = g;
+        } else if (lane >= 16) {                      // B = Θ̃[0:3,:]ᵀ v  (second-order term ⟨B, S_kl⟩)
+            const int mi = (lane - 16) / 4, j = (lane - 16) % 4;
+            double b = 0.0;
+            for (int i = 0; i < 3; ++i) b = fma(Gt[i * 4 + mi], v[4 * i + j], b);
+            Bm[mi * 4 + j] = b;
         }
-        for (int k = 0; k < 6; ++k)
-            for (int l = k; l < 6; ++l) {
-                double h = 0.0;
-                for (int r = 0; r < 12; ++r) h = fma(J[k][r], GJ[l][r], h);
-                // second-order term: v · (Θ̃ ½(E_k E_l + E_l E_k))[0:3,:]
-                double EE1[16], EE2[16], S4[16], P4[16];
-                mat4mul(E[k], E[l], EE1);
-                mat4mul(E[l], E[k], EE2);
-                for (int i = 0; i < 16; ++i) S4[i] = 0.5 * (EE1[i] + EE2[i]);
-                mat4mul(Gt, S4, P4);
-                for (int r = 0; r < 12; ++r) h = fma(v[r], P4[r], h);
-                H[k * 6 + l] = h;
-                H[l * 6 + k] = h;
-            }
-        double tr = fabs(H[0] + H[7] + H[14] + H[21] + H[28] + H[35]) / 6.0;
-        double mu = 0.0;
-        bool accepted = false, converged = false;
-        for (int tries = 0; tries < 20; ++tries) {
-            double delta[6], mg[6];
-            for (int k = 0; k < 6; ++k) mg[k] = -grad[k];
-            if (!chol_solve6(H, mu, mg, delta)) {
+        __syncwarp();
+        if (lane < 21) {
+            int k = 0, l = 0;
+            for (int idx = 0, kk = 0; kk < 6; ++kk)
+                for (int ll = kk; ll < 6; ++ll, ++idx)
+                    if (idx == lane) { k = kk; l = ll; }
+            double h = 0.0;
+            for (int r = 0; r < 12; ++r) h = fma(J[k][r], GJ[l][r], h);
+            for (int i = 0; i < 16; ++i) h = fma(Bm[i], S[lane][i], h);
+            H[k * 6 + l] = h;
+            H[l * 6 + k] = h;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const double tr = fabs(H[0] + H[7] + H[14] + H[21] + H[28] + H[35]) / 6.0;
+            double mu = 0.0;
+            bool accepted = false, converged = false;
+            for (int tries = 0; tries < 20; ++tries) {
+                double delta[6], mg[6];
+                for (int k = 0; k < 6; ++k) mg[k] = -grad[k];
+                if (!chol_solve6(H, mu, mg, delta)) {
+                    mu = fmax(10.0 * mu, 1e-6 * tr);
+                    continue;
+                }
+                const double nr = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]);
+                const double nt = sqrt(delta[3] * delta[3] + delta[4] * delta[4] + delta[5] * delta[5]);
+                if (nr < 1e-10 && nt < 1e-10 * s.extent) {
+                    converged = true;
+                    break;
+                }
+                double dR[9], dt[3], Rn[9], tn[3];
+                se3_exp(delta, dR, dt);
+                for (int i = 0; i < 3; ++i) {
+                    for (int j = 0; j < 3; ++j)
+                        Rn[3 * i + j] = Rs[3 * i] * dR[j] + Rs[3 * i + 1] * dR[3 + j] + Rs[3 * i + 2] * dR[6 + j];
+                    tn[i] = Rs[3 * i] * dt[0] + Rs[3 * i + 1] * dt[1] + Rs[3 * i + 2] * dt[2] + tsh[i];
+                }
+                double thn[12], dthn[12];
+                theta_of(Rn, tn, thn);
+                for (int r = 0; r < 12; ++r) dthn[r] = thn[r] - th_E[r];
+                const double qn = q_rel(mo, dthn);
+                if (qn < q_cur) {
+                    for (int i = 0; i < 9; ++i) Rs[i] = Rn[i];
+                    for (int i = 0; i < 3; ++i) tsh[i] = tn[i];
+                    q_cur = qn;
+                    accepted = true;
+                    step_rot += nr;
+                    step_trans += nt;
+                    break;
+                }
                 mu = fmax(10.0 * mu, 1e-6 * tr);
-                continue;
             }
-            const double nr = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]);
-            const double nt = sqrt(delta[3] * delta[3] + delta[4] * delta[4] + delta[5] * delta[5]);
-            if (nr < 1e-10 && nt < 1e-10 * s.extent) {
-                converged = true;
-                break;
-            }
-            double dR[9], dt[3], Rn[9], tn[3];
-            se3_exp(delta, dR, dt);
-            for (int i = 0; i < 3; ++i) {
-                for (int j = 0; j < 3; ++j)
-                    Rn[3 * i + j] = R[3 * i] * dR[j] + R[3 * i + 1] * dR[3 + j] + R[3 * i + 2] * dR[6 + j];
-                tn[i] = R[3 * i] * dt[0] + R[3 * i + 1] * dt[1] + R[3 * i + 2] * dt[2] + t[i];
-            }
-            double thn[12], dthn[12];
-            theta_of(Rn, tn, thn);
-            for (int r = 0; r < 12; ++r) dthn[r] = thn[r] - th_E[r];
-            const double qn = q_rel(mo, dthn);
-            if (qn < q_cur) {
-                for (int i = 0; i < 9; ++i) R[i] = Rn[i];
-                for (int i = 0; i < 3; ++i) t[i] = tn[i];
-                q_cur = qn;
-                accepted = true;
-                step_rot += nr;
-                step_trans += nt;
-                break;
-            }
-            mu = fmax(10.0 * mu, 1e-6 * tr);
+            stop = (converged || !accepted) ? 1 : 0;
         }
-        if (converged || !accepted) break;
+        __syncwarp();
+        if (stop) break;
     }
+    if (lane != 0) return;
 
     // σ² at the new pose: q(g_new) / (3 Σ P), floored; unchanged without mass.
     const int k = s.iter;
@@ -347,7 +383,10 @@ __global__ void newton_kernel(IterState* st, const double* __restrict__ mom, Reg
     }
     const double s2_old = s.sigma2;
     IterState nx = s;
-    make_state(nx, R, t, s2, rp.w, rp.V, rp.M, rp.omega_ref_target, rp.consistent);
+    double Rf[9], tf[3];
+    for (int i = 0; i < 9; ++i) Rf[i] = Rs[i];
+    for (int i = 0; i < 3; ++i) tf[i] = tsh[i];
+    make_state(nx, Rf, tf, s2, rp.w, rp.V, rp.M, rp.omega_ref_target, rp.consistent);
     nx.extent = s.extent;
     nx.iter = k + 1;
     nx.no_mass = has_mass ? 0 : s.no_mass + 1;
@@ -368,13 +407,19 @@ __global__ void newton_kernel(IterState* st, const double* __restrict__ mom, Reg
 }
 
 // ---- host launchers ----------------------------------------------------------------------------
+// Grid: a function of N only (deterministic reduction order for a given problem), ≤ 256 blocks,
+// ≥ 8 points per thread, so small problems do not pay for a 256-way cross-block sum.
+static unsigned moment_blocks(int64_t N) {
+    const int64_t b = (N + kMomThreads * 8 - 1) / (kMomThreads * 8);
+    return (unsigned)(b < 1 ? 1 : (b > kMomBlocks ? kMomBlocks : b));
+}
 void moments_launch(const float* rec, const float* src, int64_t N, const IterState* st, double* blockpart,
                     double* out, unsigned int* counter, cudaStream_t stream) {
-    moments_kernel<<<kMomBlocks, kMomThreads, 0, stream>>>(rec, src, N, st, blockpart, out, counter);
+    moments_kernel<<<moment_blocks(N), kMomThreads, 0, stream>>>(rec, src, N, st, blockpart, out, counter);
 }
 void sigma2_sums_launch(const float* src, int64_t N, const IterState* st, const void* d_target, double* blockpart,
                         double* out, unsigned int* counter, cudaStream_t stream) {
-    sigma2_sums_kernel<<<kMomBlocks, kMomThreads, 0, stream>>>(src, N, st,
+    sigma2_sums_kernel<<<moment_blocks(N), kMomThreads, 0, stream>>>(src, N, st,
                                                                reinterpret_cast<const TargetHeader*>(d_target),
                                                                blockpart, out, counter);
 }

@@ -135,12 +135,13 @@ def cpu_oracle_rate(wl, target_sample_pts: int = 0, budget_s: float = 12.0):
     alpha = rng.uniform(0, 50, wl.M)
     V, _ = oracle.working_volume(wl.target)
     cores = int(oracle._lib.lib().ora_max_threads())
-    # calibrate on 8 points, then size the sample for ~budget_s of CPU work
-    idx = rng.choice(wl.N, 8, replace=False)
+    # calibrate on a sample worth ~1 s, then size the sample for ~budget_s of CPU work
+    n0 = int(np.clip(2e8 / wl.M, 8, wl.N))
+    idx = rng.choice(wl.N, n0, replace=False)
     t0 = time.perf_counter()
     oracle.estep(wl.target, tgt_n, alpha, wl.source[idx], wl.R_expected, wl.t_expected, 1e-3, wl.w, V)
     dt = max(time.perf_counter() - t0, 1e-3)
-    n = int(np.clip(8 * budget_s / dt, 8, wl.N))
+    n = int(np.clip(n0 * budget_s / dt, 8, wl.N))
     idx = rng.choice(wl.N, n, replace=False)
     t0 = time.perf_counter()
     oracle.estep(wl.target, tgt_n, alpha, wl.source[idx], wl.R_expected, wl.t_expected, 1e-3, wl.w, V)
@@ -330,7 +331,9 @@ def main():
     if world > 1:
         dist.barrier()
     if rank == 0:
-        launches_per_step = 3 + 4 * iters
+        # per registration: setup + σ²₀ sums + σ²₀ init, then per EM iteration: tensor-core E step,
+        # CUDA-core E step (returns at once in the fixed-max mode), merge, moments, Newton
+        launches_per_step = 3 + 5 * iters
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,

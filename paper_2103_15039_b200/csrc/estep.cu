@@ -418,6 +418,9 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
@@ -430,6 +433,20 @@ __device__ __forceinline__ void tmem_st2(uint32_t taddr, float2 v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(__float_as_uint(v.x)),
                  "r"(__float_as_uint(v.y))
                  : "memory");
+}
+// columns [c, c+8) ← a, [c+8, c+16) ← b, in one asm block so the TMEM address is moved to a uniform
+// register once
+__device__ __forceinline__ void tmem_st8x2(uint32_t taddr, const uint32_t (&a)[8], const uint32_t (&b)[8]) {
+    asm volatile(
+        "{\n"
+        ".reg .b32 t2;\n"
+        "add.u32 t2, %0, 8;\n"
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n"
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [t2], {%9, %10, %11, %12, %13, %14, %15, %16};\n"
+        "}\n" ::"r"(taddr),
+        "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]), "r"(b[0]), "r"(b[1]),
+        "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]), "r"(b[6]), "r"(b[7])
+        : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
     asm volatile(
@@ -777,6 +794,383 @@ __global__ void __launch_bounds__(TcCfg<NWG, RB, MW>::kThreads, 1)
     }
 }
 
+// ---- tensor-core E step, second generation ---------------------------------------------------------
+// Same arithmetic as estep_tc_kernel; the pipeline is restructured so that the consumer warps never wait
+// on the tensor core in steady state (ncu of the first generation: 22 % of warp samples in local-memory
+// round trips for the runtime-indexed A-buffer state, 8 % waiting for D after every tile):
+//  * the chunk loop is unrolled by two, so the A buffer, every mbarrier parity and every TMEM column are
+//    compile-time constants (no local memory, one uniform TMEM base per warp);
+//  * D is double-buffered and a single 16-column accumulator: D += A_hi·F_hi + A_lo·F_hi + A_hi·F_lo
+//    (three N = 16 MMAs per K step); tile t's D is drained after the second chunk of tile t + 1, by when
+//    its MMAs have long completed;
+//  * drained tile sums go into a plain FP32 running sum S1 (one add), which is Kahan-folded into the
+//    (R, C) running sums every kTc2Fold tiles: the FP32 error stays independent of M at a quarter of
+//    the per-tile cost;
+//  * unit → (source block, tile) bookkeeping is incremental (no 64-bit division per tile).
+// TMEM per warpgroup: D 2 × 16·RB columns, A 2 × 16·RB columns (hi 8 | lo 8 per row block).
+constexpr int kTc2Fold = 16;
+template <int NWG, int RB, bool kSelf, int MW>
+struct Tc2Cfg {
+    static constexpr int kNCW = 4 * NWG;
+    // consumers + TMA producer warp + MW MMA warps (none if each warpgroup issues its own MMAs)
+    static constexpr int kThreads = (kNCW + 1 + (kSelf ? 0 : MW)) * 32;
+    static_assert(NWG % MW == 0, "MMA warps must split the warpgroups evenly");
+    static constexpr int kWGCols = 64 * RB;
+    static constexpr int kBlk = NWG * 128 * RB;
+    static constexpr int kSmF = 39;                    // S1[13], R[13], C[13] per point
+    static constexpr size_t kSmem = (size_t)kSmF * kNCW * 32 * RB * sizeof(float);
+    static_assert(NWG * kWGCols <= kTcCols, "TMEM columns");
+    static_assert(kThreads <= 1024, "threads");
+};
+static_assert(kTcStages == 4, "stage arithmetic below assumes 4 stages");
+
+template <int NWG, int RB, bool kLiteral, bool kStX8, bool kSelf, int MW>
+__global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
+    estep_tc2_kernel(const char* __restrict__ tc, const float* __restrict__ src, int64_t N,
+                     const IterState* __restrict__ st, Sched sc, float* __restrict__ part) {
+    using Cfg = Tc2Cfg<NWG, RB, kSelf, MW>;
+    constexpr int kNCW = Cfg::kNCW;
+    constexpr int kBlk = Cfg::kBlk;
+    constexpr int kWGCols = Cfg::kWGCols;
+    constexpr int kChunks = kTcTile / kTcChunk;
+    static_assert(kChunks % 2 == 0, "chunks per tile must be even");
+    __shared__ __align__(1024) char tiles_st[kTcStages][kTcTileBytes];
+    extern __shared__ __align__(16) char dsmem[];
+    float* smS = reinterpret_cast<float*>(dsmem);   // [39][RB × consumer threads]
+    __shared__ __align__(8) uint64_t full_bar[kTcStages];
+    __shared__ __align__(8) uint64_t empty_bar[kTcStages];
+    __shared__ __align__(8) uint64_t afull[NWG][2], aempty[NWG][2], dfull[NWG][2], dfree[NWG][2];
+    __shared__ uint32_t tmem_base_sh;
+
+    if (!st->active || !st->fixed) return;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t g = blockIdx.x;
+    const int64_t u0 = sched_start(sc, g), u1 = sched_start(sc, g + 1);
+    if (u0 >= u1) return;
+    const int64_t nunits = u1 - u0;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"((uint32_t)kTcCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 32) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], kNCW);
+        }
+        for (int w = 0; w < NWG; ++w)
+            for (int b = 0; b < 2; ++b) {
+                mbar_init(&afull[w][b], 4);
+                mbar_init(&aempty[w][b], 1);
+                mbar_init(&dfull[w][b], 1);
+                mbar_init(&dfree[w][b], 4);
+            }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    if (tmem != 0u) __trap();   // 512 columns = the whole TMEM: the allocation must start at column 0
+
+    if (warp == kNCW) {
+        // ---------------- producer warp: TMA bulk copies of the 10-KB tensor-core tiles ----------------
+        if (lane == 0) {
+            int64_t tile = u0 % sc.T;
+            for (int64_t it = 0; it < nunits; ++it) {
+                const int s = (int)(it & 3);
+                mbar_wait_sleep(&empty_bar[s], (uint32_t)(((it >> 2) & 1) ^ 1));
+                mbar_arrive_expect_tx(&full_bar[s], kTcTileBytes);
+                bulk_g2s(&tiles_st[s][0], tc + tile * (int64_t)kTcTileBytes, kTcTileBytes, &full_bar[s]);
+                if (++tile == sc.T) tile = 0;
+            }
+        }
+        return;
+    }
+    if (!kSelf && warp > kNCW) {
+        // ---------------- MMA warp: one elected lane issues tcgen05.mma for every warpgroup ----------------
+        // D[db] (+)= A_hi·F_hi, += A_lo·F_hi, += A_hi·F_lo per row block and K step (N = 16 each).
+        // Parities: the k-th completion of a barrier has parity k & 1; A buffer b of K step c of any tile
+        // is used for the (4·it + c/2)-th time, so its parity is the constant (c >> 1) & 1.
+        const uint32_t tiles0 = smem_u32(&tiles_st[0][0]) + kTcBOff;
+        constexpr int kWPer = NWG / MW;
+        const int w0 = (warp - kNCW - 1) * kWPer;   // this MMA warp serves warpgroups [w0, w0 + kWPer)
+        for (int64_t it = 0; it < nunits; ++it) {
+            const int s = (int)(it & 3);
+            const int db = (int)(it & 1);
+            const uint32_t dpar = (uint32_t)(((it >> 1) & 1) ^ 1);   // completion (it>>1) - 1 of dfree[db]
+            mbar_wait(&full_bar[s], (uint32_t)((it >> 2) & 1));
+            const uint32_t bbase = tiles0 + (uint32_t)s * kTcTileBytes;
+#pragma unroll
+            for (int c = 0; c < kChunks; ++c) {
+                const int ab = c & 1;
+                const uint64_t bhi = bdesc(bbase + 1024 * c), blo = bdesc(bbase + 1024 * c + 512);
+#pragma unroll
+                for (int wi = 0; wi < kWPer; ++wi) {
+                    const int w = w0 + wi;
+                    if (c == 0) mbar_wait(&dfree[w][db], dpar);
+                    mbar_wait(&afull[w][ab], (uint32_t)((c >> 1) & 1));
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
+                        const uint32_t colA = (uint32_t)(w * kWGCols + 32 * RB + ab * 16 * RB);
+#ifndef LSG_TC2_NOMMA   // diagnostic builds only (tools/build_diag.sh)
+#pragma unroll
+                        for (int rb = 0; rb < RB; ++rb) {
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, c == 0 ? 0u : 1u);
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
+                        }
+#endif
+                        mma_commit(&aempty[w][ab]);
+                        if (c == kChunks - 1) mma_commit(&dfull[w][db]);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumers: warpgroup wg, TMEM lane quadrant q ----------------
+    const int wg = warp >> 2, q = warp & 3;
+    const int tw = q * 32 + lane;
+    const int tid = threadIdx.x;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(wg * kWGCols);
+    const float k2 = st->k2;
+    const float2 nk2 = bc(-k2);
+    double Rm[9], tv[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Rm[i] = st->R[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) tv[i] = st->t[i];
+    constexpr int kRC = kNCW * 32 * RB;
+
+    float h[RB][3], l[RB][3];
+    float Rt[RB], Ct[RB];
+    int nfold = 0;
+
+    auto load_points = [&](int64_t j) {
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+            const int64_t n = j * kBlk + (wg * RB + k) * 128 + tw;
+            double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+            if (n < N) {
+                x0 = src[3 * n];
+                x1 = src[3 * n + 1];
+                x2 = src[3 * n + 2];
+            }
+            const double X[3] = {fma(Rm[0], x0, fma(Rm[1], x1, fma(Rm[2], x2, tv[0]))),
+                                 fma(Rm[3], x0, fma(Rm[4], x1, fma(Rm[5], x2, tv[1]))),
+                                 fma(Rm[6], x0, fma(Rm[7], x1, fma(Rm[8], x2, tv[2])))};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                h[k][a] = __double2float_rn(X[a]);
+                l[k][a] = __double2float_rn(X[a] - (double)h[k][a]);
+            }
+            Rt[k] = Ct[k] = 0.f;
+#pragma unroll
+            for (int f = 0; f < Cfg::kSmF; ++f) smS[f * kRC + k * (kNCW * 32) + tid] = 0.f;
+        }
+        nfold = 0;
+    };
+    // Kahan-fold S1 into (R, C) and clear S1
+    auto fold_s1 = [&]() {
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+            const int rc = rb * (kNCW * 32) + tid;
+#pragma unroll
+            for (int f = 0; f < 13; ++f) {
+                const float L = smS[f * kRC + rc];
+                const float R = smS[(13 + f) * kRC + rc], C = smS[(26 + f) * kRC + rc];
+                const float y = L - C;
+                const float t = R + y;
+                smS[(26 + f) * kRC + rc] = (t - R) - y;
+                smS[(13 + f) * kRC + rc] = t;
+                smS[f * kRC + rc] = 0.f;
+            }
+        }
+        nfold = 0;
+    };
+    // drain tile `itd`'s D (all its MMAs are complete once dfull fires), release D and the smem stage
+    auto drain = [&](int64_t itd) {
+        const int db = (int)(itd & 1);
+        mbar_wait(&dfull[wg][db], (uint32_t)((itd >> 1) & 1));
+        tc_fence_after();
+        uint32_t d[RB][16];
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) tmem_ld16(tl + (uint32_t)(db * 16 * RB + rb * 16), d[rb]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+            if (!kSelf) mbar_arrive(&dfree[wg][db]);   // self-issue: the next chunk-0 barrier orders it
+            mbar_arrive(&empty_bar[itd & 3]);
+        }
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+            const int rc = rb * (kNCW * 32) + tid;
+#pragma unroll
+            for (int f = 0; f < 13; ++f) smS[f * kRC + rc] += __uint_as_float(d[rb][f]);
+        }
+        if (++nfold == kTc2Fold) fold_s1();
+    };
+    auto flush = [&](int64_t j) {
+        fold_s1();
+        const int64_t slot = j * sc.kmax + (g - sched_owner(sc, j * sc.T));
+        float* base = part + slot * (int64_t)kPartF * kBlk;
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+            const int b = (wg * RB + k) * 128 + tw;
+            const int rc = k * (kNCW * 32) + tid;
+#pragma unroll
+            for (int f = 0; f < 13; ++f) base[f * kBlk + b] = __fsub_rn(smS[(13 + f) * kRC + rc], smS[(26 + f) * kRC + rc]);
+            base[13 * kBlk + b] = __fsub_rn(Rt[k], Ct[k]);
+            base[14 * kBlk + b] = 0.f;
+            base[15 * kBlk + b] = 0.f;
+        }
+    };
+
+    uint32_t cur_b = 0, cur_db = 0;   // self-issue: B operand base of the current stage, D buffer
+    // one K step (8 targets = 4 target pairs) for buffer AB: residual, τ, ex2, Σpτ, TF32 split → TMEM A
+    auto chunk = [&](const float4* core, int c, float2 (&Lt)[RB], auto ABc) {
+        constexpr int AB = decltype(ABc)::value;
+        // wait for the MMAs of this buffer's previous use (K step c - 2): parity of completion 4·it + c/2 - 1
+        const uint32_t apar = (uint32_t)(((c >> 1) & 1) ^ 1);
+        if (!kStX8) {
+            mbar_wait(&aempty[wg][AB], apar);
+            tc_fence_after();
+        }
+        uint32_t ahi[RB][8], alo[RB][8];
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+            const int pr = c * 4 + pp;
+            const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) {
+                const float2 rx = __fadd2_rn(__fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y)), bc(l[rb][0]));
+                const float2 ry = __fadd2_rn(__fadd2_rn(bc(h[rb][1]), make_float2(-v0.z, -v0.w)), bc(l[rb][1]));
+                const float2 rz = __fadd2_rn(__fadd2_rn(bc(h[rb][2]), make_float2(-v1.x, -v1.y)), bc(l[rb][2]));
+                const float2 qv = __ffma2_rn(make_float2(v3.x, v3.y), rz,
+                                             __ffma2_rn(make_float2(v2.z, v2.w), ry, __fmul2_rn(make_float2(v2.x, v2.y), rx)));
+                const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
+                const float2 e = kLiteral ? __fmul2_rn(nk2, tau) : __ffma2_rn(nk2, tau, make_float2(v1.z, v1.w));
+                const float2 p = make_float2(ex2_approx(e.x), ex2_approx(e.y));
+                Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
+                const float2 hi = make_float2(__uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
+                                              __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
+                const float2 lo = __fadd2_rn(p, make_float2(-hi.x, -hi.y));
+                if (kStX8) {
+                    ahi[rb][2 * pp] = __float_as_uint(hi.x);
+                    ahi[rb][2 * pp + 1] = __float_as_uint(hi.y);
+                    alo[rb][2 * pp] = __float_as_uint(lo.x);
+                    alo[rb][2 * pp + 1] = __float_as_uint(lo.y);
+                } else {
+                    tmem_st2(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16 + 2 * pp), hi);
+                    tmem_st2(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16 + 8 + 2 * pp), lo);
+                }
+            }
+        }
+        if (kStX8) {
+            // the A buffer is needed only now: the MMAs of its previous use had this chunk's math to finish
+            mbar_wait(&aempty[wg][AB], apar);
+            tc_fence_after();
+#ifndef LSG_TC2_NOSTTM
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) tmem_st8x2(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16), ahi[rb], alo[rb]);
+#else
+            float sink = 0.f;
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) sink += __uint_as_float(ahi[rb][k]) + __uint_as_float(alo[rb][k]);
+            Lt[0].x += sink * 1e-30f;
+#endif
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (!kSelf) {
+            if (lane == 0) mbar_arrive(&afull[wg][AB]);
+        } else {
+            // the warpgroup's four warps meet at a named barrier (two ids, alternating with the A buffer, so
+            // a warp one K step ahead cannot complete the wrong phase); warp 0 then issues the MMAs
+            const int bid = 2 + 2 * wg + AB;
+            if (q != 0) {
+                named_bar_arrive(bid, 128);
+            } else {
+                named_bar_sync(bid, 128);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint64_t bhi = bdesc(cur_b + 1024 * c), blo = bdesc(cur_b + 1024 * c + 512);
+                    const uint32_t colD = (uint32_t)(wg * kWGCols) + cur_db * 16 * RB;
+                    constexpr uint32_t kColA = 32 * RB + AB * 16 * RB;
+#pragma unroll
+                    for (int rb = 0; rb < RB; ++rb) {
+                        mma_tf32_ts(colD + rb * 16, (uint32_t)(wg * kWGCols) + kColA + rb * 16, bhi, kTcIdesc16,
+                                    c == 0 ? 0u : 1u);
+                        mma_tf32_ts(colD + rb * 16, (uint32_t)(wg * kWGCols) + kColA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
+                        mma_tf32_ts(colD + rb * 16, (uint32_t)(wg * kWGCols) + kColA + rb * 16, blo, kTcIdesc16, 1u);
+                    }
+                    mma_commit(&aempty[wg][AB]);
+                    if (c == kChunks - 1) mma_commit(&dfull[wg][cur_db]);
+                }
+                __syncwarp();
+            }
+        }
+    };
+
+    int64_t j = u0 / sc.T, tile = u0 % sc.T;
+    load_points(j);
+    bool pending = false;   // the previous tile's D has not been drained yet
+    for (int64_t it = 0; it < nunits; ++it) {
+        mbar_wait(&full_bar[it & 3], (uint32_t)((it >> 2) & 1));
+        cur_b = smem_u32(&tiles_st[0][0]) + kTcBOff + (uint32_t)(it & 3) * kTcTileBytes;
+        cur_db = (uint32_t)(it & 1);
+        const float4* core = reinterpret_cast<const float4*>(&tiles_st[it & 3][0]);
+        float2 Lt[RB];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) Lt[k] = make_float2(0.f, 0.f);
+#pragma unroll 1
+        for (int c = 0; c < kChunks; c += 2) {
+            chunk(core, c, Lt, std::integral_constant<int, 0>());
+            chunk(core, c + 1, Lt, std::integral_constant<int, 1>());
+            if (c == 0 && pending) {
+                drain(it - 1);
+                pending = false;
+            }
+        }
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+            const float L = Lt[rb].x + Lt[rb].y;
+            const float y = L - Ct[rb];
+            const float t = Rt[rb] + y;
+            Ct[rb] = (t - Rt[rb]) - y;
+            Rt[rb] = t;
+        }
+        pending = true;
+        if (++tile == sc.T || it + 1 == nunits) {   // source block (or the CTA's range) ends here
+            drain(it);
+            pending = false;
+            flush(j);
+            tile = 0;
+            ++j;
+            if (it + 1 < nunits) load_points(j);
+        }
+    }
+    // all MMAs of this warpgroup completed (dfull of the last tile was awaited); release TMEM
+    tc_fence_before();
+    named_bar_sync(1, kNCW * 32);
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)kTcCols)
+                     : "memory");
+    }
+}
+
 // ---- merge: log-sum-exp over partials + outlier term → 16-float record -------------------
 __global__ void estep_merge_kernel(const float* __restrict__ part, int64_t N, const IterState* __restrict__ st,
                                    Sched sc, float* __restrict__ rec) {
@@ -866,6 +1260,12 @@ struct TcVariant {
 #define LSG_TC(NWG, RB, MW, PV)                                                                           \
     {NWG, RB, MW, PV, TcCfg<NWG, RB, MW>::kThreads, TcCfg<NWG, RB, MW>::kBlk, TcCfg<NWG, RB, MW>::kSmem, \
      {(const void*)estep_tc_kernel<NWG, RB, MW, false>, (const void*)estep_tc_kernel<NWG, RB, MW, true>}}
+#define LSG_TC2M(NWG, RB, X8, SELF, MW, PV)                                                          \
+    {NWG, RB, MW, PV, Tc2Cfg<NWG, RB, SELF, MW>::kThreads, Tc2Cfg<NWG, RB, SELF, MW>::kBlk,          \
+     Tc2Cfg<NWG, RB, SELF, MW>::kSmem,                                                               \
+     {(const void*)estep_tc2_kernel<NWG, RB, false, X8, SELF, MW>,                                   \
+      (const void*)estep_tc2_kernel<NWG, RB, true, X8, SELF, MW>}}
+#define LSG_TC2(NWG, RB, X8, SELF, PV) LSG_TC2M(NWG, RB, X8, SELF, 1, PV)
 static const TcVariant kTcVariants[] = {
     LSG_TC(4, 2, 2, 0),   // 16 consumer warps, 2 points/thread (1024-point blocks) — CUDA-core variant 0
     LSG_TC(6, 1, 2, 3),   // 24 consumer warps, 1 point/thread (768) — variant 3
@@ -875,6 +1275,23 @@ static const TcVariant kTcVariants[] = {
     LSG_TC(4, 2, 1, 0),   // as 0 with a single MMA warp
     LSG_TC(2, 4, 1, 0),   // 8 consumer warps, 4 points/thread (1024)
     LSG_TC(3, 2, 1, 3),   // 12 consumer warps, 2 points/thread (768)
+    // second generation (estep_tc2_kernel): one MMA warp, double-buffered D
+    LSG_TC2(3, 2, false, false, 3),   // 8: 12 consumer warps × 2 points (768), per-pair TMEM stores
+    LSG_TC2(3, 2, true, false, 3),    // 9: as 8 with two x8 TMEM stores per row block and K step
+    LSG_TC2(4, 2, true, false, 0),    // 10: 16 consumer warps × 2 points (1024)
+    LSG_TC2(2, 4, true, false, 0),    // 11: 8 consumer warps × 4 points (1024)
+    LSG_TC2(6, 1, true, false, 3),    // 12: 24 consumer warps × 1 point (768)
+    LSG_TC2(6, 1, false, false, 3),   // 13: as 12 with per-pair TMEM stores
+    LSG_TC2(2, 2, true, false, 9),    // 14: 8 consumer warps × 2 points (512)
+    // each warpgroup issues its own MMAs (no MMA warp)
+    LSG_TC2(3, 2, true, true, 3),     // 15: as 9
+    LSG_TC2(4, 2, true, true, 0),     // 16: as 10
+    LSG_TC2(2, 4, true, true, 0),     // 17: as 11
+    LSG_TC2(6, 1, true, true, 3),     // 18: as 12
+    // one MMA warp per warpgroup
+    LSG_TC2M(3, 2, true, false, 3, 3),   // 19: as 9
+    LSG_TC2M(6, 1, true, false, 3, 3),   // 20: as 12, one MMA warp per two warpgroups
+    LSG_TC2M(2, 2, true, false, 2, 9),   // 21: as 14
 };
 constexpr int kNumTcVariants = sizeof(kTcVariants) / sizeof(kTcVariants[0]);
 // LSGCPD_TC: unset = automatic (tensor cores unless the problem is too small), 0 = off, 1 = forced on
@@ -882,7 +1299,7 @@ static int tc_mode() {
     const char* e = getenv("LSGCPD_TC");
     return e ? (atoi(e) != 0 ? 1 : 0) : 2;
 }
-constexpr int kDefaultTcVariant = 7;   // 12 consumer warps × 2 points, 1 MMA warp (tools/tc_check.py sweep)
+constexpr int kDefaultTcVariant = 19;  // tc2: 12 consumer warps × 2 points, one MMA warp per warpgroup (tools/tc_speed.py)
 static int tc_variant_index() {
     const char* e = getenv("LSGCPD_TC_VARIANT");
     int v = e ? atoi(e) : kDefaultTcVariant;

@@ -834,9 +834,10 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
     constexpr int kWGCols = Cfg::kWGCols;
     constexpr int kChunks = kTcTile / kTcChunk;
     static_assert(kChunks % 2 == 0, "chunks per tile must be even");
+    constexpr int kNF = 13;   // D features kept: 1, y, W, b
     __shared__ __align__(1024) char tiles_st[kTcStages][kTcTileBytes];
     extern __shared__ __align__(16) char dsmem[];
-    float* smS = reinterpret_cast<float*>(dsmem);   // [39][RB × consumer threads]
+    float* smS = reinterpret_cast<float*>(dsmem);   // [3 kNF][RB × consumer threads]: S1, R, C
     __shared__ __align__(8) uint64_t full_bar[kTcStages];
     __shared__ __align__(8) uint64_t empty_bar[kTcStages];
     __shared__ __align__(8) uint64_t afull[NWG][2], aempty[NWG][2], dfull[NWG][2], dfree[NWG][2];
@@ -902,7 +903,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
             const int s = (int)(it & 3);
             const int db = (int)(it & 1);
             const uint32_t dpar = (uint32_t)(((it >> 1) & 1) ^ 1);   // completion (it>>1) - 1 of dfree[db]
-            mbar_wait(&full_bar[s], (uint32_t)((it >> 2) & 1));
+            mbar_wait_sleep(&full_bar[s], (uint32_t)((it >> 2) & 1));
             const uint32_t bbase = tiles0 + (uint32_t)s * kTcTileBytes;
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
@@ -911,8 +912,8 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
 #pragma unroll
                 for (int wi = 0; wi < kWPer; ++wi) {
                     const int w = w0 + wi;
-                    if (c == 0) mbar_wait(&dfree[w][db], dpar);
-                    mbar_wait(&afull[w][ab], (uint32_t)((c >> 1) & 1));
+                    if (c == 0) mbar_wait_sleep(&dfree[w][db], dpar);
+                    mbar_wait_sleep(&afull[w][ab], (uint32_t)((c >> 1) & 1));
                     tc_fence_after();
                     if (elect_one()) {
                         const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
@@ -949,7 +950,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
     for (int i = 0; i < 3; ++i) tv[i] = st->t[i];
     constexpr int kRC = kNCW * 32 * RB;
 
-    float h[RB][3], l[RB][3];
+    float2 h[RB][3], l[RB][3];   // x̂ as FP32 hi/lo, broadcast to both f32x2 lanes (two targets per instruction)
     float Rt[RB], Ct[RB];
     int nfold = 0;
 
@@ -968,8 +969,9 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
                                  fma(Rm[6], x0, fma(Rm[7], x1, fma(Rm[8], x2, tv[2])))};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                h[k][a] = __double2float_rn(X[a]);
-                l[k][a] = __double2float_rn(X[a] - (double)h[k][a]);
+                const float hi = __double2float_rn(X[a]);
+                h[k][a] = bc(hi);
+                l[k][a] = bc(__double2float_rn(X[a] - (double)hi));
             }
             Rt[k] = Ct[k] = 0.f;
 #pragma unroll
@@ -983,13 +985,13 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         for (int rb = 0; rb < RB; ++rb) {
             const int rc = rb * (kNCW * 32) + tid;
 #pragma unroll
-            for (int f = 0; f < 13; ++f) {
+            for (int f = 0; f < kNF; ++f) {
                 const float L = smS[f * kRC + rc];
-                const float R = smS[(13 + f) * kRC + rc], C = smS[(26 + f) * kRC + rc];
+                const float R = smS[(kNF + f) * kRC + rc], C = smS[(2 * kNF + f) * kRC + rc];
                 const float y = L - C;
                 const float t = R + y;
-                smS[(26 + f) * kRC + rc] = (t - R) - y;
-                smS[(13 + f) * kRC + rc] = t;
+                smS[(2 * kNF + f) * kRC + rc] = (t - R) - y;
+                smS[(kNF + f) * kRC + rc] = t;
                 smS[f * kRC + rc] = 0.f;
             }
         }
@@ -998,7 +1000,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
     // drain tile `itd`'s D (all its MMAs are complete once dfull fires), release D and the smem stage
     auto drain = [&](int64_t itd) {
         const int db = (int)(itd & 1);
-        mbar_wait(&dfull[wg][db], (uint32_t)((itd >> 1) & 1));
+        mbar_wait_sleep(&dfull[wg][db], (uint32_t)((itd >> 1) & 1));
         tc_fence_after();
         uint32_t d[RB][16];
 #pragma unroll
@@ -1014,7 +1016,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         for (int rb = 0; rb < RB; ++rb) {
             const int rc = rb * (kNCW * 32) + tid;
 #pragma unroll
-            for (int f = 0; f < 13; ++f) smS[f * kRC + rc] += __uint_as_float(d[rb][f]);
+            for (int f = 0; f < kNF; ++f) smS[f * kRC + rc] += __uint_as_float(d[rb][f]);
         }
         if (++nfold == kTc2Fold) fold_s1();
     };
@@ -1027,7 +1029,8 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
             const int b = (wg * RB + k) * 128 + tw;
             const int rc = k * (kNCW * 32) + tid;
 #pragma unroll
-            for (int f = 0; f < 13; ++f) base[f * kBlk + b] = __fsub_rn(smS[(13 + f) * kRC + rc], smS[(26 + f) * kRC + rc]);
+            for (int f = 0; f < 13; ++f)
+                base[f * kBlk + b] = __fsub_rn(smS[(kNF + f) * kRC + rc], smS[(2 * kNF + f) * kRC + rc]);
             base[13 * kBlk + b] = __fsub_rn(Rt[k], Ct[k]);
             base[14 * kBlk + b] = 0.f;
             base[15 * kBlk + b] = 0.f;
@@ -1041,19 +1044,19 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         // wait for the MMAs of this buffer's previous use (K step c - 2): parity of completion 4·it + c/2 - 1
         const uint32_t apar = (uint32_t)(((c >> 1) & 1) ^ 1);
         if (!kStX8) {
-            mbar_wait(&aempty[wg][AB], apar);
+            mbar_wait_sleep(&aempty[wg][AB], apar);
             tc_fence_after();
         }
-        uint32_t ahi[RB][8], alo[RB][8];
+        uint32_t av[RB][16];   // A row of this K step: TF32 hi of the 8 targets, then lo
 #pragma unroll
         for (int pp = 0; pp < 4; ++pp) {
             const int pr = c * 4 + pp;
             const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
 #pragma unroll
             for (int rb = 0; rb < RB; ++rb) {
-                const float2 rx = __fadd2_rn(__fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y)), bc(l[rb][0]));
-                const float2 ry = __fadd2_rn(__fadd2_rn(bc(h[rb][1]), make_float2(-v0.z, -v0.w)), bc(l[rb][1]));
-                const float2 rz = __fadd2_rn(__fadd2_rn(bc(h[rb][2]), make_float2(-v1.x, -v1.y)), bc(l[rb][2]));
+                const float2 rx = __fadd2_rn(__fadd2_rn(h[rb][0], make_float2(-v0.x, -v0.y)), l[rb][0]);
+                const float2 ry = __fadd2_rn(__fadd2_rn(h[rb][1], make_float2(-v0.z, -v0.w)), l[rb][1]);
+                const float2 rz = __fadd2_rn(__fadd2_rn(h[rb][2], make_float2(-v1.x, -v1.y)), l[rb][2]);
                 const float2 qv = __ffma2_rn(make_float2(v3.x, v3.y), rz,
                                              __ffma2_rn(make_float2(v2.z, v2.w), ry, __fmul2_rn(make_float2(v2.x, v2.y), rx)));
                 const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
@@ -1064,10 +1067,10 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
                                               __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
                 const float2 lo = __fadd2_rn(p, make_float2(-hi.x, -hi.y));
                 if (kStX8) {
-                    ahi[rb][2 * pp] = __float_as_uint(hi.x);
-                    ahi[rb][2 * pp + 1] = __float_as_uint(hi.y);
-                    alo[rb][2 * pp] = __float_as_uint(lo.x);
-                    alo[rb][2 * pp + 1] = __float_as_uint(lo.y);
+                    av[rb][2 * pp] = __float_as_uint(hi.x);
+                    av[rb][2 * pp + 1] = __float_as_uint(hi.y);
+                    av[rb][8 + 2 * pp] = __float_as_uint(lo.x);
+                    av[rb][8 + 2 * pp + 1] = __float_as_uint(lo.y);
                 } else {
                     tmem_st2(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16 + 2 * pp), hi);
                     tmem_st2(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16 + 8 + 2 * pp), lo);
@@ -1076,17 +1079,17 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         }
         if (kStX8) {
             // the A buffer is needed only now: the MMAs of its previous use had this chunk's math to finish
-            mbar_wait(&aempty[wg][AB], apar);
+            mbar_wait_sleep(&aempty[wg][AB], apar);
             tc_fence_after();
 #ifndef LSG_TC2_NOSTTM
 #pragma unroll
-            for (int rb = 0; rb < RB; ++rb) tmem_st8x2(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16), ahi[rb], alo[rb]);
+            for (int rb = 0; rb < RB; ++rb) tmem_st16(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16), av[rb]);
 #else
             float sink = 0.f;
 #pragma unroll
             for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
-                for (int k = 0; k < 8; ++k) sink += __uint_as_float(ahi[rb][k]) + __uint_as_float(alo[rb][k]);
+                for (int k = 0; k < 16; ++k) sink += __uint_as_float(av[rb][k]);
             Lt[0].x += sink * 1e-30f;
 #endif
         }
@@ -1127,7 +1130,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
     load_points(j);
     bool pending = false;   // the previous tile's D has not been drained yet
     for (int64_t it = 0; it < nunits; ++it) {
-        mbar_wait(&full_bar[it & 3], (uint32_t)((it >> 2) & 1));
+        mbar_wait_sleep(&full_bar[it & 3], (uint32_t)((it >> 2) & 1));
         cur_b = smem_u32(&tiles_st[0][0]) + kTcBOff + (uint32_t)(it & 3) * kTcTileBytes;
         cur_db = (uint32_t)(it & 1);
         const float4* core = reinterpret_cast<const float4*>(&tiles_st[it & 3][0]);

@@ -1,0 +1,91 @@
+// Microbenchmark: the CUDA-core part of the tensor-core E step in isolation (residual with hi/lo,
+// τ, e, ex2, Σpτ, TF32 split of p) over broadcast shared-memory targets, no TMEM / MMA / barriers.
+// Reports pairs per clock per SM for several warp counts and points per thread: the ceiling the
+// E-step consumer code can reach on this SM.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pairloop pairloop.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float ex2a(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+constexpr int kTgt = 1024;   // targets in shared memory (pair-interleaved, 32 B per target)
+constexpr int kReps = 64;
+
+template <int RB, int MODE>
+__global__ void pairloop(const float4* __restrict__ gt, float* out, long long* cyc, float k2) {
+    __shared__ float4 core[kTgt / 2 * 4];
+    for (int i = threadIdx.x; i < kTgt / 2 * 4; i += blockDim.x) core[i] = gt[i];
+    __syncthreads();
+    float h[RB][3], l[RB][3];
+    for (int rb = 0; rb < RB; ++rb)
+        for (int a = 0; a < 3; ++a) { h[rb][a] = 0.01f * (threadIdx.x % 7 + a + rb); l[rb][a] = 1e-9f * a; }
+    float2 Lt[RB];
+    for (int rb = 0; rb < RB; ++rb) Lt[rb] = make_float2(0.f, 0.f);
+    unsigned sink = 0;
+    const float2 nk2 = bc(-k2);
+    long long t0 = clock64();
+    for (int rep = 0; rep < kReps; ++rep) {
+#pragma unroll 4
+        for (int pr = 0; pr < kTgt / 2; ++pr) {
+            const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) {
+                const float2 rx = __fadd2_rn(__fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y)), bc(l[rb][0]));
+                const float2 ry = __fadd2_rn(__fadd2_rn(bc(h[rb][1]), make_float2(-v0.z, -v0.w)), bc(l[rb][1]));
+                const float2 rz = __fadd2_rn(__fadd2_rn(bc(h[rb][2]), make_float2(-v1.x, -v1.y)), bc(l[rb][2]));
+                const float2 qv = __ffma2_rn(make_float2(v3.x, v3.y), rz,
+                                             __ffma2_rn(make_float2(v2.z, v2.w), ry, __fmul2_rn(make_float2(v2.x, v2.y), rx)));
+                const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
+                const float2 e = __ffma2_rn(nk2, tau, make_float2(v1.z, v1.w));
+                if (MODE == 2) { Lt[rb] = __fadd2_rn(Lt[rb], e); continue; }          // no MUFU
+                const float2 p = make_float2(ex2a(e.x), ex2a(e.y));
+                Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
+                if (MODE == 1) { sink ^= __float_as_uint(p.x) ^ __float_as_uint(p.y); continue; }   // no split
+                const unsigned hx = __float_as_uint(p.x) & 0xFFFFE000u, hy = __float_as_uint(p.y) & 0xFFFFE000u;
+                const float2 lo = __fadd2_rn(p, make_float2(-__uint_as_float(hx), -__uint_as_float(hy)));
+                sink ^= hx ^ hy ^ __float_as_uint(lo.x) ^ __float_as_uint(lo.y);
+            }
+        }
+    }
+    long long t1 = clock64();
+    float s = 0.f;
+    for (int rb = 0; rb < RB; ++rb) s += Lt[rb].x + Lt[rb].y;
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s + (float)(sink & 1);
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int RB, int MODE>
+void run(int warps, const float4* gt, float* out, long long* cyc, int nsm) {
+    const int thr = warps * 32;
+    pairloop<RB, MODE><<<nsm, thr>>>(gt, out, cyc, 721.f);
+    cudaDeviceSynchronize();
+    pairloop<RB, MODE><<<nsm, thr>>>(gt, out, cyc, 721.f);
+    cudaDeviceSynchronize();
+    long long c[1024];
+    cudaMemcpy(c, cyc, nsm * sizeof(long long), cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < nsm; ++i) avg += c[i];
+    avg /= nsm;
+    const double pairs = (double)thr * RB * kTgt * kReps;   // per SM
+    printf("mode=%d RB=%d warps=%2d  %.3f pairs/clk/SM  (%.3e pairs/s at 1965 MHz x %d SMs)\n", MODE, RB, warps,
+           pairs / avg, pairs / avg * 1.965e9 * nsm, nsm);
+}
+
+int main() {
+    int nsm;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    float4* gt; float* out; long long* cyc;
+    cudaMalloc(&gt, kTgt / 2 * 4 * sizeof(float4));
+    cudaMalloc(&out, 1024 * 1024 * sizeof(float));
+    cudaMalloc(&cyc, 1024 * sizeof(long long));
+    float4 hbuf[kTgt / 2 * 4];
+    for (int i = 0; i < kTgt / 2 * 4; ++i) hbuf[i] = make_float4(0.013f * (i % 17), 0.011f * (i % 13), -0.5f, 0.3f);
+    cudaMemcpy(gt, hbuf, sizeof(hbuf), cudaMemcpyHostToDevice);
+    for (int w : {8, 12, 16, 24, 32}) run<2, 0>(w, gt, out, cyc, nsm);
+    for (int w : {12, 16, 24}) run<1, 0>(w, gt, out, cyc, nsm);
+    for (int w : {8, 12, 16}) run<4, 0>(w, gt, out, cyc, nsm);
+    for (int w : {12, 16}) run<2, 1>(w, gt, out, cyc, nsm);
+    for (int w : {12, 16}) run<2, 2>(w, gt, out, cyc, nsm);
+    return 0;
+}

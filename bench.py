@@ -285,7 +285,7 @@ def main():
             traffic = None
     roofline = {"bound": "alu", "achieved": achieved_tflops, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
                 "frac": achieved_tflops / fp32_peak_tflops, "traffic": traffic,
-                "kernel": "lsg::estep_tc_kernel (tcgen05 TF32 feature sums) + merge, via lsgcpd_estep",
+                "kernel": "lsg::estep_tc2_kernel (tcgen05 TF32 feature sums, default LSGCPD_TC_VARIANT) + merge, via lsgcpd_estep",
                 "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 flop x {f_max/1e6:.0f} MHz "
                                f"(sm_max_mhz {peak_src}, MEASURED_PEAKS.json); algorithmic "
                                f"{FLOPS_PER_PAIR:.0f} flop/pair (SURVEY 8(d).2)",

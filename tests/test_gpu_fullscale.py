@@ -1,0 +1,76 @@
+"""Registration parity at the BASELINE configs' full sizes (rgbd, lidar, scale), where a full FP64 oracle
+registration takes 0.5-12 h: teacher forcing.  At EM states k taken from the GPU's
+own trajectory (lsgcpd_register stopped after k iterations):
+  * E step: the GPU record at (R_k, t_k, σ²_k) vs the oracle's Eq. 5 record on sampled source points
+    (every target), tolerance 2e-5 of scale (tests/parity.py);
+  * M step: the oracle's damped Newton + σ² update (oracle/mstep.py) run on the GPU's full
+    record must land where the GPU's iteration k+1 landed: R within 1e-4 rad, t within 1e-4·extent
+    (the north-star bar), σ² within 1e-6 relative.
+Each EM step of the GPU trajectory is then an oracle step within tolerance, for the whole run.
+Also: the NCCL all-reduce path of lsgcpd_register with a one-rank communicator equals the no-comm path."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import se3
+from tests.gpu_common import to_dev, workload
+from tests.parity import assert_record_parity
+
+pytestmark = pytest.mark.gpu
+
+
+def _states(iters):
+    return sorted({0, 1, iters // 2, iters - 1})
+
+
+@pytest.mark.parametrize("name", ["rgbd", "lidar", "scale"])
+def test_register_teacher_forced_full_scale(name):
+    import paper_2103_15039_b200 as lsg
+    wl = workload(name)
+    tgt, ann = lsg.prepare_target(to_dev(wl.target), wl.knn_k, annotations=True)
+    n64 = ann["normals"].cpu().numpy().astype(np.float64)
+    a64 = ann["alpha"].cpu().numpy().astype(np.float64)
+    X = to_dev(wl.source)
+    iters = wl.iters
+    reg = lsg.Registrar(tgt, X, iters)
+    rng = np.random.default_rng(17)
+    idx = np.sort(rng.choice(wl.N, 96, replace=False))
+    floor = 1e-12 * tgt.extent ** 2
+    first = lsg.Registrar(tgt, X, 1)(w=wl.w, traces=True)
+    for k in _states(iters):
+        if k == 0:
+            R, t, s2 = np.eye(3), np.zeros(3), float(first["sigma2_trace"][0])
+        else:
+            st = lsg.Registrar(tgt, X, k)(w=wl.w)
+            assert st["iters"] == k and st["status"] == 0
+            R, t, s2 = st["R"], st["t"], st["sigma2"]
+        nxt = first if k == 0 else lsg.Registrar(tgt, X, k + 1)(w=wl.w)
+        rec = lsg.estep(tgt, X, R, t, s2, wl.w, tgt.volume).cpu().numpy()
+        ora = oracle.estep(wl.target, n64, a64, wl.source[idx], R, t, s2, wl.w, tgt.volume)
+        assert_record_parity(rec[idx], ora, wl.target, a64, what=f"{name} E step at state {k}")
+        R1, t1, s21, _ = oracle.mstep(wl.source, rec, R, t, s2, tgt.extent, 10, floor)
+        ang = se3.rotation_angle(np.asarray(nxt["R"]).T @ R1)
+        dt = np.linalg.norm(np.asarray(nxt["t"]) - t1)
+        assert ang <= 1e-4, f"{name} M step {k}: rotation differs by {ang:.2e} rad"
+        assert dt <= 1e-4 * tgt.extent, f"{name} M step {k}: translation differs by {dt:.2e}"
+        assert abs(nxt["sigma2"] - s21) <= 1e-6 * s21, (name, k, nxt["sigma2"], s21)
+    del reg
+
+
+def test_register_with_one_rank_nccl_comm_equals_no_comm():
+    # the communicator path (ncclAllReduce of the 75 moments per iteration) with world size 1
+    import paper_2103_15039_b200 as lsg
+    wl = workload("object")
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    X = to_dev(wl.source)
+    reg = lsg.Registrar(tgt, X, 20)
+    plain = reg(w=wl.w, traces=True)
+    comm = lsg.Comm(0, 1)
+    try:
+        viac = reg(w=wl.w, traces=True, comm=comm)
+    finally:
+        comm.close()
+    assert viac["iters"] == plain["iters"] == 20
+    assert np.array_equal(viac["R"], plain["R"]) and np.array_equal(viac["t"], plain["t"])
+    assert viac["sigma2"] == plain["sigma2"]
+    np.testing.assert_array_equal(viac["nll"], plain["nll"])

@@ -10,9 +10,9 @@ the EM *trajectory choice* among stationary points, which is "parity unpinned" b
 readings (SURVEY §8(c).5 last row).
 """
 from ._lib import build  # noqa: F401
-from .estep import estep, posterior, sym6, REC  # noqa: F401
+from .estep import estep, estep_cf, posterior, sym6, REC  # noqa: F401
 from .model import (knn, alpha_from_kappa, local_surface, prepare_target, working_volume,  # noqa: F401
                     sigma2_init, sum_sq_pairs, mean_nn_spacing)
 from .mstep import PointStats, newton, mstep, grad_hess_literal  # noqa: F401
 from .em import register, register_workload  # noqa: F401
-from . import se3, matrix_form  # noqa: F401
+from . import se3, matrix_form, outlier  # noqa: F401

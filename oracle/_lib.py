@@ -39,6 +39,9 @@ def lib():
             L.ora_estep.argtypes = [dp, dp, dp, i64, dp, i64, dp, dp, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_double, ctypes.c_int, dp, ctypes.c_int]
             L.ora_estep.restype = None
+            L.ora_estep_cf.argtypes = [dp, dp, dp, dp, i64, dp, dp, i64, dp, dp, ctypes.c_double,
+                                       ctypes.c_double, ctypes.c_int, dp, ctypes.c_int]
+            L.ora_estep_cf.restype = None
             L.ora_posterior.argtypes = [dp, dp, dp, i64, dp, i64, dp, dp, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_int, dp, dp]
             L.ora_posterior.restype = None

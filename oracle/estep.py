@@ -29,6 +29,23 @@ def estep(Y, normals, alpha, X, R, t, sigma2: float, w: float, V: float, consist
     return rec
 
 
+def estep_cf(Y, normals, alpha, prior, X, wn, R, t, sigma2: float, V: float, consistent: bool = True,
+             nthreads: int = 0) -> np.ndarray:
+    """E-step record with per-component priors π(m) and per-point outlier weights w_n (Eq. 8, P:248-255;
+    Eq. 1 and Eq. 5 with π(m), w_n in place of 1/M, w)."""
+    Y, normals, alpha, prior, X, wn = f64(Y), f64(normals), f64(alpha), f64(prior), f64(X), f64(wn)
+    R, t = f64(R).reshape(9), f64(t).reshape(3)
+    M, N = Y.shape[0], X.shape[0]
+    if prior.shape != (M,) or wn.shape != (N,):
+        raise ValueError("prior must be [M], wn must be [N]")
+    rec = np.empty((N, REC), dtype=np.float64)
+    if N == 0:
+        return rec
+    lib().ora_estep_cf(ptr(Y), ptr(normals), ptr(alpha), ptr(prior), M, ptr(X), ptr(wn), N, ptr(R), ptr(t),
+                       float(sigma2), float(V), int(bool(consistent)), ptr(rec), int(nthreads))
+    return rec
+
+
 def posterior(Y, normals, alpha, X, R, t, sigma2: float, w: float, V: float, consistent: bool = True):
     """Full posterior matrix P (M×N) and outlier posterior (N,) — small sizes only."""
     Y, normals, alpha, X = f64(Y), f64(normals), f64(alpha), f64(X)

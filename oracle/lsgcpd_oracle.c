@@ -114,6 +114,82 @@ void ora_estep(const double* Y, const double* Nrm, const double* alpha, int64_t 
 }
 
 /*
+ * Eq. 1 / Eq. 5 with the confidence-filtered model of Eq. 8: per-component prior
+ * π(m) (prior[m], Σ_m π(m) = 1) and per-point outlier weight w_n (wn[n] ∈ [0, 1]):
+ *   p(x̂_n) = w_n p_o + (1 - w_n) Σ_m π(m) p(x̂_n|m),
+ *   P_mn   = (1 - w_n) π(m) p(x̂_n|m) / p(x̂_n),   P_o,n = w_n p_o / p(x̂_n).
+ * With π(m) = 1/M and w_n = w it is ora_estep term for term.  w_n = 1 gives P_o,n = 1 exactly
+ * (every component term is multiplied by 1 - w_n = 0).  Same record layout as ora_estep.
+ */
+void ora_estep_cf(const double* Y, const double* Nrm, const double* alpha, const double* prior, int64_t M,
+                  const double* X, const double* wn, int64_t N, const double* R, const double* t,
+                  double sigma2, double V, int consistent, double* rec, int nthreads)
+{
+    const double ln_gauss = -1.5 * log(2.0 * M_PI * sigma2);          /* ln (2πσ²)^{-3/2} */
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel
+    {
+        double* lbuf = (double*)malloc(sizeof(double) * (size_t)M);
+        double* dbuf = (double*)malloc(sizeof(double) * (size_t)M);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t n = 0; n < N; ++n) {
+            const double w = wn[n];
+            const double l_out = (w > 0.0) ? log(w / V) : -INFINITY;      /* ln(w_n p_o) */
+            const double ln_keep = (w < 1.0) ? log(1.0 - w) : -INFINITY;  /* ln(1 - w_n) */
+            const double* x = X + 3 * n;
+            double xh[3];
+            for (int i = 0; i < 3; ++i)
+                xh[i] = R[3 * i + 0] * x[0] + R[3 * i + 1] * x[1] + R[3 * i + 2] * x[2] + t[i];
+            double mu = l_out;
+            for (int64_t m = 0; m < M; ++m) {
+                const double* y = Y + 3 * m;
+                const double* nm = Nrm + 3 * m;
+                const double r0 = xh[0] - y[0], r1 = xh[1] - y[1], r2 = xh[2] - y[2];
+                const double q = nm[0] * r0 + nm[1] * r1 + nm[2] * r2;
+                const double d = (r0 * r0 + r1 * r1 + r2 * r2 + alpha[m] * q * q) / sigma2;
+                const double ln_cm = ln_gauss + (consistent ? 0.5 * log(1.0 + alpha[m]) : 0.0);
+                const double l = ln_keep + log(prior[m]) + ln_cm - 0.5 * d;   /* ln((1-w_n) π(m) p(x̂|m)) */
+                lbuf[m] = l;
+                dbuf[m] = d;
+                if (l > mu) mu = l;
+            }
+            double Z = (w > 0.0) ? exp(l_out - mu) : 0.0;
+            for (int64_t m = 0; m < M; ++m) Z += exp(lbuf[m] - mu);
+            double acc[ORA_REC];
+            memset(acc, 0, sizeof(acc));
+            for (int64_t m = 0; m < M; ++m) {
+                const double Pmn = exp(lbuf[m] - mu) / Z;
+                const double* y = Y + 3 * m;
+                const double* nm = Nrm + 3 * m;
+                const double a = alpha[m];
+                const double ny = nm[0] * y[0] + nm[1] * y[1] + nm[2] * y[2];
+                acc[0] += Pmn;
+                acc[1] += Pmn * y[0];
+                acc[2] += Pmn * y[1];
+                acc[3] += Pmn * y[2];
+                acc[4] += Pmn * a * nm[0] * nm[0];
+                acc[5] += Pmn * a * nm[0] * nm[1];
+                acc[6] += Pmn * a * nm[0] * nm[2];
+                acc[7] += Pmn * a * nm[1] * nm[1];
+                acc[8] += Pmn * a * nm[1] * nm[2];
+                acc[9] += Pmn * a * nm[2] * nm[2];
+                acc[10] += Pmn * a * ny * nm[0];
+                acc[11] += Pmn * a * ny * nm[1];
+                acc[12] += Pmn * a * ny * nm[2];
+                acc[13] += Pmn * dbuf[m];
+            }
+            acc[14] = mu + log(Z);
+            acc[15] = (w > 0.0) ? exp(l_out - mu) / Z : 0.0;
+            memcpy(rec + ORA_REC * n, acc, sizeof(acc));
+        }
+        free(lbuf);
+        free(dbuf);
+    }
+}
+
+/*
  * Posterior matrix P (M×N, row-major P[m*N+n]) and outlier posterior (N) — tiny sizes only.
  * Same per-pair evaluation as ora_estep; used by the tests to compare element by element.
  */

@@ -83,6 +83,12 @@ typedef struct {
     double sigma2_init;        /* ≤ 0: CPD closed form Σ_mn||x̂_n-y_m||²/(3MN) (R7)  */
     double sigma2_floor_rel;   /* σ² ≥ sigma2_floor_rel · extent² (default 1e-12, R16)           */
     double tol;                /* > 0: stop when |Δσ²|/σ² < tol and the pose step < tol          */
+    /* Model extensions (§3.2-3.3).  Defaults (eta < 0, NULL) reproduce the uniform model above.   */
+    double eta;                /* outlier ratio η ∈ [0,1): w0 = w_max(η) = ηVΣπc/((1-η)+ηVΣπc)     */
+                               /* (Eq. 7), re-evaluated from σ² at every E step (reading    */
+                               /* R22); w is then ignored.  < 0: use w.                            */
+    const float* d_src_conf;   /* DEVICE [N] source confidences φ(x_n) ∈ [0,1] (Eq. 8):  */
+                               /* w_n = 1 - (1 - w0) φ(x_n); NULL: w_n = w0 for every point          */
 } lsgcpd_em_params;
 
 /* Library identity. */
@@ -128,6 +134,45 @@ int lsgcpd_estep(const void* d_target, int64_t M, const float* d_src, int64_t N,
                  int consistent_normalizer, float* d_record, void* d_ws, size_t ws_bytes,
                  lsgcpd_stream_t stream);
 
+/* E step with the §3.2-3.3 model extensions: w, eta, consistent_normalizer and d_src_conf are
+ * taken from `params` (the other fields are ignored); the target's component priors π(m) are
+ * whatever lsgcpd_target_set_prior last installed (uniform 1/M by default).  With per-point w_n:
+ *   P_mn = (1-w_n) π(m) c_m e^{-d_mn/2} / (w_n/V + (1-w_n) Σ_k π(k) c_k e^{-d_kn/2}),
+ * and a point with φ(x_n) = 0 (w_n = 1) is all outlier (P_out = 1, ln p = -ln V).  async.
+ * Errors: as lsgcpd_estep, plus EINVAL for eta ≥ 1. */
+int lsgcpd_estep_ex(const void* d_target, int64_t M, const float* d_src, int64_t N,
+                    const double R[9], const double t[3], double sigma2, const lsgcpd_em_params* params,
+                    double volume, float* d_record, void* d_ws, size_t ws_bytes, lsgcpd_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Confidence filtering.  φ(x) = e_min/e(x) is a sensor's measurement confidence.
+ * ------------------------------------------------------------------------------------- */
+/* Install component priors π(m) = φ(y_m)/Σ_m φ(y_m) (Eq. 8) into a prepared target, in place:
+ * the per-target log weight becomes ½log2(1+α_m) + log2(M π(m)).  Idempotent (α_m is read back
+ * from the packed model; a uniform φ restores π = 1/M).  d_phi: DEVICE [M], φ ≥ 0, Σφ > 0;
+ * φ(y_m) = 0 removes component m.  h_spc (may be NULL) receives Σ_m π(m)√(1+α_m).  sync.
+ * Non-uniform priors need consistent_normalizer = 1 in the E step / registration (the Eq. 9-10
+ * literal form has π(m) = 1/M): with 0 those calls return EINVAL (and the E step then reads the
+ * target header, a host sync).
+ * Errors: EINVAL (null, M mismatch, negative / non-finite φ, all zero, ws too small), ECUDA. */
+size_t lsgcpd_target_prior_workspace_bytes(int64_t M);
+int lsgcpd_target_set_prior(void* d_target, int64_t M, const float* d_phi, void* d_ws, size_t ws_bytes,
+                            double* h_spc, lsgcpd_stream_t stream);
+
+/* Truncation of low-confidence points: copy the points with φ ≥ threshold, in their original
+ * order, to d_xyz_out [n][3] (and their φ to d_phi_out [n], may be NULL); *h_n_out = count.  The
+ * output buffers must hold n points.  sync.  Errors: EINVAL (null, n < 1, ws too small), ECUDA. */
+size_t lsgcpd_select_workspace_bytes(int64_t n);
+int lsgcpd_select_confident(const float* d_xyz, const float* d_phi, int64_t n, float threshold,
+                            float* d_xyz_out, float* d_phi_out, int64_t* h_n_out, void* d_ws,
+                            size_t ws_bytes, lsgcpd_stream_t stream);
+
+/* Depth error model (reading R23): for points in their sensor's camera frame
+ * (z = depth), φ = e(z_min)/e(z) with e(z) = c0 + c1 z², clipped to [0, 1].  d_phi: DEVICE [n].
+ * async.  Errors: EINVAL (null, n < 1, c0 < 0, c1 < 0, c0 + c1 z_min² ≤ 0). */
+int lsgcpd_depth_confidence(const float* d_xyz, int64_t n, double c0, double c1, double z_min,
+                            float* d_phi, lsgcpd_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------
  * Multi-GPU communicator (one process per GPU).  Wraps an NCCL communicator loaded at run time
  * (libnccl.so.2); the 128-byte id is produced on rank 0 and broadcast by the caller (e.g. over
@@ -141,6 +186,8 @@ int lsgcpd_comm_destroy(void* comm);
  * Registration (the EM loop): σ²₀ (CPD closed form) → for k < max_iters:
  * E step → per-point FP64 moments (75 numbers) → [all-reduce over comm] → damped SE(3)
  * Newton on the exact frozen-P objective (Eq. 11-13, readings R11-R13) → σ².
+ * params->eta and params->d_src_conf (indexed like d_src_local) select the §3.2-3.3 model as in
+ * lsgcpd_estep_ex; the target's priors are those installed by lsgcpd_target_set_prior.
  * Each rank passes its own contiguous source shard (N_local points) and the same prepared
  * target; all ranks return bit-identical R, t, σ².  volume ≤ 0 uses the target's V.
  * Optional host traces (may be NULL): nll_trace[max_iters] (NLL at each E step, Eq. 4),

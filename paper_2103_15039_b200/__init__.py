@@ -50,7 +50,8 @@ class Annotations(ctypes.Structure):
 class EmParams(ctypes.Structure):
     _fields_ = [("w", ctypes.c_double), ("max_iters", ctypes.c_int), ("newton_max", ctypes.c_int),
                 ("consistent_normalizer", ctypes.c_int), ("sigma2_init", ctypes.c_double),
-                ("sigma2_floor_rel", ctypes.c_double), ("tol", ctypes.c_double)]
+                ("sigma2_floor_rel", ctypes.c_double), ("tol", ctypes.c_double), ("eta", ctypes.c_double),
+                ("d_src_conf", ctypes.c_void_p)]
 
 
 _lock = threading.Lock()
@@ -71,6 +72,13 @@ _SIGS = {
     "lsgcpd_pack_target": ([_vp, _vp, _vp, _i64, _d, _vp, _vp, _sz, ctypes.POINTER(TargetInfo), _vp], _i32),
     "lsgcpd_estep_workspace_bytes": ([_i64, _i64], _sz),
     "lsgcpd_estep": ([_vp, _i64, _vp, _i64, _dp, _dp, _d, _d, _d, _i32, _vp, _vp, _sz, _vp], _i32),
+    "lsgcpd_estep_ex": ([_vp, _i64, _vp, _i64, _dp, _dp, _d, ctypes.POINTER(EmParams), _d, _vp, _vp, _sz, _vp], _i32),
+    "lsgcpd_target_prior_workspace_bytes": ([_i64], _sz),
+    "lsgcpd_target_set_prior": ([_vp, _i64, _vp, _vp, _sz, _dp, _vp], _i32),
+    "lsgcpd_select_workspace_bytes": ([_i64], _sz),
+    "lsgcpd_select_confident": ([_vp, _vp, _i64, ctypes.c_float, _vp, _vp, ctypes.POINTER(ctypes.c_int64), _vp, _sz,
+                                 _vp], _i32),
+    "lsgcpd_depth_confidence": ([_vp, _i64, _d, _d, _d, _vp, _vp], _i32),
     "lsgcpd_comm_unique_id": ([_vp], _i32),
     "lsgcpd_comm_init": ([_i32, _i32, _vp, ctypes.POINTER(ctypes.c_void_p)], _i32),
     "lsgcpd_comm_destroy": ([_vp], _i32),
@@ -206,20 +214,78 @@ class EstepRunner:
         self.rec = out if out is not None else torch.empty((self.N, REC), dtype=torch.float32, device=src.device)
 
     def __call__(self, R, t, sigma2: float, w: float, volume: Optional[float] = None, consistent: bool = True,
-                 stream=None):
+                 stream=None, eta: Optional[float] = None, src_conf=None):
         Ra, Rp = _darr(R, 9)
         ta, tp = _darr(t, 3)
         V = self.target.volume if volume is None else float(volume)
-        _check(lib().lsgcpd_estep(self.target.buf.data_ptr(), self.target.M, self.src.data_ptr(), self.N, Rp, tp,
-                                  float(sigma2), float(w), V, int(bool(consistent)), self.rec.data_ptr(),
-                                  self.ws.data_ptr(), self.ws.numel(), _stream_ptr(stream)))
+        if eta is None and src_conf is None:
+            _check(lib().lsgcpd_estep(self.target.buf.data_ptr(), self.target.M, self.src.data_ptr(), self.N, Rp, tp,
+                                      float(sigma2), float(w), V, int(bool(consistent)), self.rec.data_ptr(),
+                                      self.ws.data_ptr(), self.ws.numel(), _stream_ptr(stream)))
+        else:
+            p = EmParams()
+            lib().lsgcpd_em_params_default(ctypes.byref(p))
+            p.w = float(w)
+            p.consistent_normalizer = int(bool(consistent))
+            p.eta = -1.0 if eta is None else float(eta)
+            p.d_src_conf = _conf_ptr(src_conf, self.N)
+            _check(lib().lsgcpd_estep_ex(self.target.buf.data_ptr(), self.target.M, self.src.data_ptr(), self.N, Rp, tp,
+                                         float(sigma2), ctypes.byref(p), V, self.rec.data_ptr(), self.ws.data_ptr(),
+                                         self.ws.numel(), _stream_ptr(stream)))
         return self.rec
 
 
 def estep(target: Target, src, R, t, sigma2: float, w: float, volume: Optional[float] = None,
-          consistent: bool = True, stream=None):
-    """lsgcpd_estep → [N,16] float32 CUDA record tensor."""
-    return EstepRunner(target, src)(R, t, sigma2, w, volume, consistent, stream)
+          consistent: bool = True, stream=None, eta: Optional[float] = None, src_conf=None):
+    """lsgcpd_estep (or lsgcpd_estep_ex with eta / src_conf) → [N,16] float32 CUDA record tensor."""
+    return EstepRunner(target, src)(R, t, sigma2, w, volume, consistent, stream, eta, src_conf)
+
+
+def _conf_ptr(conf, n):
+    if conf is None:
+        return None
+    _need_cuda_f32(conf, "src_conf")
+    if conf.numel() != n:
+        raise ValueError(f"src_conf must have {n} entries")
+    return conf.data_ptr()
+
+
+def set_prior(target: Target, phi, stream=None) -> float:
+    """lsgcpd_target_set_prior: π(m) = φ(y_m)/Σφ installed in place (Eq. 8).  Returns Σ π √(1+α)."""
+    _need_cuda_f32(phi, "phi")
+    if phi.numel() != target.M:
+        raise ValueError(f"phi must have {target.M} entries")
+    ws = _alloc_bytes(lib().lsgcpd_target_prior_workspace_bytes(target.M), phi.device)
+    spc = ctypes.c_double()
+    _check(lib().lsgcpd_target_set_prior(target.buf.data_ptr(), target.M, phi.data_ptr(), ws.data_ptr(), ws.numel(),
+                                         ctypes.byref(spc), _stream_ptr(stream)))
+    return spc.value
+
+
+def select_confident(xyz, phi, threshold: float, stream=None):
+    """lsgcpd_select_confident: (points with φ ≥ threshold, their φ), order preserved."""
+    import torch
+    _need_cuda_f32(xyz, "xyz", 3)
+    _need_cuda_f32(phi, "phi")
+    n = int(xyz.shape[0])
+    out = torch.empty_like(xyz)
+    pout = torch.empty_like(phi)
+    ws = _alloc_bytes(lib().lsgcpd_select_workspace_bytes(n), xyz.device)
+    k = ctypes.c_int64()
+    _check(lib().lsgcpd_select_confident(xyz.data_ptr(), phi.data_ptr(), n, float(threshold), out.data_ptr(),
+                                         pout.data_ptr(), ctypes.byref(k), ws.data_ptr(), ws.numel(),
+                                         _stream_ptr(stream)))
+    return out[: k.value].contiguous(), pout[: k.value].contiguous()
+
+
+def depth_confidence(xyz, c0: float = 0.0, c1: float = 0.002, z_min: float = 0.4, stream=None):
+    """lsgcpd_depth_confidence: φ = e(z_min)/e(z), e(z) = c0 + c1 z² of the camera-frame depth."""
+    import torch
+    _need_cuda_f32(xyz, "xyz", 3)
+    phi = torch.empty(int(xyz.shape[0]), dtype=torch.float32, device=xyz.device)
+    _check(lib().lsgcpd_depth_confidence(xyz.data_ptr(), int(xyz.shape[0]), float(c0), float(c1), float(z_min),
+                                         phi.data_ptr(), _stream_ptr(stream)))
+    return phi
 
 
 class Comm:
@@ -258,8 +324,10 @@ class Registrar:
 
     def __call__(self, w: float = 0.1, newton_max: int = 10, consistent: bool = True, sigma2_init: float = 0.0,
                  sigma2_floor_rel: float = 1e-12, tol: float = 0.0, R0=None, t0=None, volume: float = 0.0,
-                 comm: Optional[Comm] = None, traces: bool = False, stream=None, check: bool = True):
-        p = EmParams(w, self.max_iters, newton_max, int(bool(consistent)), sigma2_init, sigma2_floor_rel, tol)
+                 comm: Optional[Comm] = None, traces: bool = False, stream=None, check: bool = True,
+                 eta: Optional[float] = None, src_conf=None):
+        p = EmParams(w, self.max_iters, newton_max, int(bool(consistent)), sigma2_init, sigma2_floor_rel, tol,
+                     -1.0 if eta is None else float(eta), _conf_ptr(src_conf, self.N))
         R0a, R0p = _darr(np.eye(3) if R0 is None else R0, 9)
         t0a, t0p = _darr(np.zeros(3) if t0 is None else t0, 3)
         Ro = np.zeros(9)

@@ -150,7 +150,8 @@ static int enqueue_iteration(const void* d_target, const float* d_src, int64_t N
     IterState* st = reinterpret_cast<IterState*>(ws + L.state);
     double* mom = reinterpret_cast<double*>(ws + L.mom);
     float* rec = reinterpret_cast<float*>(ws + L.rec);
-    estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), rec, rp.consistent, stream);
+    estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), rec, rp.consistent, rp.phi,
+                 stream);
     moments_launch(rec, d_src, N, st, reinterpret_cast<double*>(ws + L.blockpart), mom,
                    reinterpret_cast<unsigned*>(ws + L.counters), stream);
     if (comm) {
@@ -169,7 +170,7 @@ using namespace lsg;
 // =============================================================================================
 // exported C ABI
 // =============================================================================================
-LSG_EXPORT int lsgcpd_version(void) { return 10000; }
+LSG_EXPORT int lsgcpd_version(void) { return 10100; }
 LSG_EXPORT const char* lsgcpd_last_error(void) { return g_err; }
 
 LSG_EXPORT void lsgcpd_prep_params_default(lsgcpd_prep_params* p) {
@@ -189,6 +190,8 @@ LSG_EXPORT void lsgcpd_em_params_default(lsgcpd_em_params* p) {
     p->sigma2_init = 0.0;
     p->sigma2_floor_rel = 1e-12;
     p->tol = 0.0;
+    p->eta = -1.0;
+    p->d_src_conf = nullptr;
 }
 
 LSG_EXPORT size_t lsgcpd_target_bytes(int64_t M) {
@@ -252,9 +255,30 @@ LSG_EXPORT size_t lsgcpd_estep_workspace_bytes(int64_t M, int64_t N) {
     return L.total;
 }
 
+static int estep_impl(const void* d_target, int64_t M, const float* d_src, int64_t N, const double R[9],
+                      const double t[3], double sigma2, double w, double eta, const float* phi, double volume,
+                      int consistent_normalizer, float* d_record, void* d_ws, size_t ws_bytes, cudaStream_t s);
+
 LSG_EXPORT int lsgcpd_estep(const void* d_target, int64_t M, const float* d_src, int64_t N, const double R[9],
                             const double t[3], double sigma2, double w, double volume, int consistent_normalizer,
                             float* d_record, void* d_ws, size_t ws_bytes, lsgcpd_stream_t stream) {
+    return estep_impl(d_target, M, d_src, N, R, t, sigma2, w, -1.0, nullptr, volume, consistent_normalizer,
+                      d_record, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+LSG_EXPORT int lsgcpd_estep_ex(const void* d_target, int64_t M, const float* d_src, int64_t N, const double R[9],
+                               const double t[3], double sigma2, const lsgcpd_em_params* params, double volume,
+                               float* d_record, void* d_ws, size_t ws_bytes, lsgcpd_stream_t stream) {
+    LSG_CHECK(params, LSGCPD_EINVAL, "null params");
+    LSG_CHECK(!(params->eta >= 1.0) && !isnan(params->eta), LSGCPD_EINVAL, "eta must be < 1 (negative: off)");
+    return estep_impl(d_target, M, d_src, N, R, t, sigma2, params->eta >= 0.0 ? 0.0 : params->w, params->eta,
+                      params->d_src_conf, volume, params->consistent_normalizer, d_record, d_ws, ws_bytes,
+                      (cudaStream_t)stream);
+}
+
+static int estep_impl(const void* d_target, int64_t M, const float* d_src, int64_t N, const double R[9],
+                      const double t[3], double sigma2, double w, double eta, const float* phi, double volume,
+                      int consistent_normalizer, float* d_record, void* d_ws, size_t ws_bytes, cudaStream_t s) {
     LSG_CHECK(d_target && d_src && d_record && d_ws && R && t, LSGCPD_EINVAL, "null pointer argument");
     LSG_CHECK(aligned16(d_target) && aligned16(d_record) && aligned16(d_ws), LSGCPD_EINVAL,
               "d_target, d_record and d_ws must be 16-byte aligned");
@@ -270,12 +294,17 @@ LSG_EXPORT int lsgcpd_estep(const void* d_target, int64_t M, const float* d_src,
     int rc = estep_layout(pad_targets(M), N, &L, &sc);
     if (rc) return rc;
     LSG_CHECK(ws_bytes >= L.total, LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
-    cudaStream_t s = (cudaStream_t)stream;
+    if (!consistent_normalizer) {   // the Eq. 9-10 literal form has π(m) = 1/M (reads the header: a host sync)
+        TargetHeader h;
+        rc = read_header(d_target, M, &h, s);
+        if (rc) return rc;
+        LSG_CHECK(!h.prior, LSGCPD_EINVAL, "component priors require consistent_normalizer = 1");
+    }
     char* ws = static_cast<char*>(d_ws);
     IterState* st = reinterpret_cast<IterState*>(ws + L.state);
-    estep_launch_setup(st, d_target, R, t, sigma2, w, volume, M, consistent_normalizer ? 1 : 0, s);
+    estep_launch_setup(st, d_target, R, t, sigma2, w, volume, M, consistent_normalizer ? 1 : 0, eta, s);
     estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), d_record,
-                 consistent_normalizer ? 1 : 0, s);
+                 consistent_normalizer ? 1 : 0, phi, s);
     LSG_CUDA(cudaGetLastError());
     return 0;
 }
@@ -346,6 +375,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     LSG_CHECK(p.newton_max >= 0 && p.newton_max <= 1000, LSGCPD_EINVAL, "newton_max out of range");
     LSG_CHECK(isfinite(p.sigma2_floor_rel) && p.sigma2_floor_rel >= 0.0, LSGCPD_EINVAL, "bad sigma2_floor_rel");
     LSG_CHECK(isfinite(p.sigma2_init) && isfinite(p.tol), LSGCPD_EINVAL, "sigma2_init and tol must be finite");
+    LSG_CHECK(!(p.eta >= 1.0) && !isnan(p.eta), LSGCPD_EINVAL, "eta must be < 1 (negative: off)");
     double Rid[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, tid[3] = {0, 0, 0};
     const double* R = R0 ? R0 : Rid;
     const double* t = t0 ? t0 : tid;
@@ -355,6 +385,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     TargetHeader h;
     int rc = read_header(d_target, M, &h, s);
     if (rc) return rc;
+    LSG_CHECK(p.consistent_normalizer || !h.prior, LSGCPD_EINVAL, "component priors require consistent_normalizer = 1");
     const double V = volume > 0.0 ? volume : h.volume;
     LSG_CHECK(isfinite(V) && V > 0.0, LSGCPD_EINVAL, "volume must be finite and > 0");
     RegLayout L;
@@ -373,7 +404,10 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     double* mom = reinterpret_cast<double*>(ws + L.mom);
     double* sums = reinterpret_cast<double*>(ws + L.sums);
     RegParams rp;
-    rp.w = p.w;
+    rp.w = p.eta >= 0.0 ? 0.0 : p.w;
+    rp.eta = p.eta >= 0.0 ? p.eta : -1.0;
+    rp.spc = h.spc;
+    rp.phi = p.d_src_conf;
     rp.V = V;
     rp.floor = p.sigma2_floor_rel * h.extent * h.extent;
     rp.tol = p.tol;
@@ -388,7 +422,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     LSG_CUDA(cudaMemsetAsync(ws + L.nll, 0, sizeof(double) * (p.max_iters + 1), s));
     LSG_CUDA(cudaMemsetAsync(ws + L.sig2, 0, sizeof(double) * (p.max_iters + 2), s));
     // initial pose, then σ²₀ (CPD closed form over all ranks' points)
-    estep_launch_setup(st, d_target, R, t, 1.0, p.w, V, M, rp.consistent, s);
+    estep_launch_setup(st, d_target, R, t, 1.0, rp.w, V, M, rp.consistent, rp.eta, s);
     sigma2_sums_launch(d_src_local, N_local, st, d_target, reinterpret_cast<double*>(ws + L.blockpart), sums,
                        reinterpret_cast<unsigned*>(ws + L.counters), s);
     if (c) {
@@ -451,5 +485,54 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
         set_error("no inlier mass (sum P <= 1e-12 N) for 3 consecutive iterations");
         return LSGCPD_ENOMASS;
     }
+    return 0;
+}
+
+LSG_EXPORT size_t lsgcpd_target_prior_workspace_bytes(int64_t M) {
+    if (M < 1) return 0;
+    return prior_ws_bytes(M);
+}
+
+LSG_EXPORT int lsgcpd_target_set_prior(void* d_target, int64_t M, const float* d_phi, void* d_ws, size_t ws_bytes,
+                                       double* h_spc, lsgcpd_stream_t stream) {
+    LSG_CHECK(d_target && d_phi && d_ws, LSGCPD_EINVAL, "null pointer argument");
+    LSG_CHECK(aligned16(d_target), LSGCPD_EINVAL, "d_target must be 16-byte aligned");
+    LSG_CHECK(M >= 1 && M < (int64_t)1 << 30, LSGCPD_EINVAL, "M=%lld out of range", (long long)M);
+    LSG_CHECK(ws_bytes >= prior_ws_bytes(M), LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes,
+              prior_ws_bytes(M));
+    cudaStream_t s = (cudaStream_t)stream;
+    TargetHeader h;
+    int rc = read_header(d_target, M, &h, s);
+    if (rc) return rc;
+    return set_prior_impl(d_target, M, d_phi, d_ws, h_spc, s);
+}
+
+LSG_EXPORT size_t lsgcpd_select_workspace_bytes(int64_t n) {
+    if (n < 1 || n >= (int64_t)1 << 31) return 0;
+    return select_ws_bytes(n);
+}
+
+LSG_EXPORT int lsgcpd_select_confident(const float* d_xyz, const float* d_phi, int64_t n, float threshold,
+                                       float* d_xyz_out, float* d_phi_out, int64_t* h_n_out, void* d_ws,
+                                       size_t ws_bytes, lsgcpd_stream_t stream) {
+    LSG_CHECK(d_xyz && d_phi && d_xyz_out && h_n_out && d_ws, LSGCPD_EINVAL, "null pointer argument");
+    LSG_CHECK(n >= 1 && n < (int64_t)1 << 31, LSGCPD_EINVAL, "n=%lld out of range", (long long)n);
+    LSG_CHECK(isfinite(threshold), LSGCPD_EINVAL, "threshold must be finite");
+    LSG_CHECK(aligned16(d_ws), LSGCPD_EINVAL, "d_ws must be 16-byte aligned");
+    LSG_CHECK(ws_bytes >= select_ws_bytes(n), LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes,
+              select_ws_bytes(n));
+    return select_confident_impl(d_xyz, d_phi, n, threshold, d_xyz_out, d_phi_out, h_n_out, d_ws,
+                                 (cudaStream_t)stream);
+}
+
+LSG_EXPORT int lsgcpd_depth_confidence(const float* d_xyz, int64_t n, double c0, double c1, double z_min,
+                                       float* d_phi, lsgcpd_stream_t stream) {
+    LSG_CHECK(d_xyz && d_phi, LSGCPD_EINVAL, "null pointer argument");
+    LSG_CHECK(n >= 1, LSGCPD_EINVAL, "n must be >= 1");
+    LSG_CHECK(isfinite(c0) && isfinite(c1) && isfinite(z_min) && c0 >= 0.0 && c1 >= 0.0 &&
+                  c0 + c1 * z_min * z_min > 0.0,
+              LSGCPD_EINVAL, "error model must have c0, c1 >= 0 and e(z_min) > 0");
+    depth_confidence_launch(d_xyz, n, c0, c1, z_min, d_phi, (cudaStream_t)stream);
+    LSG_CUDA(cudaGetLastError());
     return 0;
 }

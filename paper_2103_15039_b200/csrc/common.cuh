@@ -53,9 +53,11 @@ struct TargetHeader {
     double ybar[3];          // centroid
     double syy;              // Σ_m ||y_m - ȳ||²
     double alpha_sum;
+    double spc;              // Σ_m π(m) √(1+α_m): Σ_m π(m) c_m (2πσ²)^{3/2} for w_max of Eq. 7
     int64_t n_degenerate;
     uint32_t magic;
-    uint32_t pad_[3];
+    uint32_t prior;          // 1: non-uniform component priors installed (lsgcpd_target_set_prior)
+    uint32_t pad_[2];
 };
 static_assert(sizeof(TargetHeader) <= kHeaderBytes, "header too big");
 constexpr uint32_t kTargetMagic = 0x4c534743u;  // "LSGC"
@@ -106,10 +108,20 @@ struct IterState {
     double last_step_rot, last_step_trans;
 };
 
+// eta ≥ 0 replaces w by the outlier-ratio bound of §3.2 (Eq. 7) at this σ²:
+//   w_max = η V S / ((1 - η) + η V S),  S = Σ_m π(m) c_m = (2πσ²)^{-3/2} · (Σ π √(1+α) | 1)
+// (re-evaluated at every E step because c_m depends on σ², reading R22).
 __host__ __device__ inline void make_state(IterState& s, const double* R, const double* t, double sigma2, double w,
-                                           double V, int64_t M, double omega_ref_target, int consistent) {
+                                           double V, int64_t M, double omega_ref_target, int consistent,
+                                           double eta = -1.0, double spc = 1.0) {
     for (int i = 0; i < 9; ++i) s.R[i] = R[i];
     for (int i = 0; i < 3; ++i) s.t[i] = t[i];
+    if (eta >= 0.0) {
+        const double S = pow(2.0 * 3.14159265358979323846 * sigma2, -1.5) * (consistent ? spc : 1.0);
+        const double a = eta * V * S;
+        w = a / ((1.0 - eta) + a);
+        if (!(w < 1.0)) w = 1.0 - 1e-16;
+    }
     s.sigma2 = sigma2;
     s.w = w;
     s.volume = V;

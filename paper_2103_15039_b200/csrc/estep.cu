@@ -173,11 +173,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __global__ void estep_setup_kernel(IterState* st, const TargetHeader* hdr, double r0, double r1, double r2,
                                    double r3, double r4, double r5, double r6, double r7, double r8, double t0,
                                    double t1, double t2, double sigma2, double w, double V, int64_t M,
-                                   int consistent) {
+                                   int consistent, double eta) {
     const double R[9] = {r0, r1, r2, r3, r4, r5, r6, r7, r8};
     const double t[3] = {t0, t1, t2};
     IterState s;
-    make_state(s, R, t, sigma2, w, V, M, hdr->omega_ref, consistent);
+    make_state(s, R, t, sigma2, w, V, M, hdr->omega_ref, consistent, eta, hdr->spc);
     s.extent = hdr->extent;
     s.active = 1;
     s.iter = 0;
@@ -1137,7 +1137,12 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         float2 Lt[RB];
 #pragma unroll
         for (int k = 0; k < RB; ++k) Lt[k] = make_float2(0.f, 0.f);
-#pragma unroll 1
+#ifndef LSG_TC2_UNROLL
+#define LSG_TC2_UNROLL 1
+#endif
+#define LSG_PRAGMA(x) _Pragma(#x)
+#define LSG_UNROLL(n) LSG_PRAGMA(unroll n)
+        LSG_UNROLL(LSG_TC2_UNROLL)
         for (int c = 0; c < kChunks; c += 2) {
             chunk(core, c, Lt, std::integral_constant<int, 0>());
             chunk(core, c + 1, Lt, std::integral_constant<int, 1>());
@@ -1175,11 +1180,29 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
 }
 
 // ---- merge: log-sum-exp over partials + outlier term → 16-float record -------------------
+// With per-point confidences (Eq. 8) the outlier weight is w_n = 1 - (1 - w0) φ(x_n), so the
+// outlier log2-weight and the density constant are per point:
+//   C1_n = ln((1 - w_n)/M) - 1.5 ln(2πσ²) = C1 + ln((1 - w_n)/(1 - w0)),
+//   L_o,n = (ln(w_n/V) - C1_n)/ln2 - ω_ref;   w_n = 1 → the point is all outlier (P_out = 1, ln p = -ln V).
+// The pair kernels do not depend on w_n (the fixed-max mode needs L_o,n ≥ L_o, true since w_n ≥ w0).
 __global__ void estep_merge_kernel(const float* __restrict__ part, int64_t N, const IterState* __restrict__ st,
-                                   Sched sc, float* __restrict__ rec) {
+                                   Sched sc, float* __restrict__ rec, const float* __restrict__ phi) {
     if (!st->active) return;
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
+    double wn = st->w, C1n = st->C1, Lon = st->Lo;
+    if (phi) {
+        const double f = fmin(fmax((double)phi[n], 0.0), 1.0);
+        wn = 1.0 - (1.0 - st->w) * f;
+        if (!(wn < 1.0)) {
+            float4* r4 = reinterpret_cast<float4*>(rec + n * LSGCPD_REC);
+            r4[0] = r4[1] = r4[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+            r4[3] = make_float4(0.f, 0.f, (float)(-log(st->volume)), 1.f);
+            return;
+        }
+        C1n = st->C1 + log((1.0 - wn) / (1.0 - st->w));
+        Lon = wn > 0.0 ? (log(wn / st->volume) - C1n) * 1.4426950408889634074 - st->omega_ref : -INFINITY;
+    }
     const int64_t kB = sc.B;
     const int64_t j = n / kB;
     const int b = (int)(n % kB);
@@ -1192,7 +1215,7 @@ __global__ void estep_merge_kernel(const float* __restrict__ part, int64_t N, co
         const float* base = part + (j * sc.kmax + k) * (int64_t)kPartF * kB;
         mustar = fmax(mustar, (double)base[14 * kB + b]);
     }
-    if (st->w > 0.0) mustar = fmax(mustar, fmin(st->Lo, 0.0));   // keep the outlier term representable
+    if (wn > 0.0) mustar = fmax(mustar, fmin(Lon, 0.0));   // keep the outlier term representable
     double a[kAcc];
 #pragma unroll
     for (int f = 0; f < kAcc; ++f) a[f] = 0.0;
@@ -1203,7 +1226,7 @@ __global__ void estep_merge_kernel(const float* __restrict__ part, int64_t N, co
 #pragma unroll
         for (int f = 0; f < kAcc; ++f) a[f] = fma(sc_k, (double)base[f * kB + b], a[f]);
     }
-    const double O = (st->w > 0.0) ? exp2(st->Lo - mustar) : 0.0;
+    const double O = (wn > 0.0) ? exp2(Lon - mustar) : 0.0;
     const double Z = a[0] + O;
     const double iz = 1.0 / Z;
     float* r = rec + n * LSGCPD_REC;
@@ -1222,7 +1245,7 @@ __global__ void estep_merge_kernel(const float* __restrict__ part, int64_t N, co
     o2.w = (float)(a[11] * iz);
     o3.x = (float)(a[12] * iz);
     o3.y = (float)(a[13] * iz / st->sigma2);
-    o3.z = (float)(st->C1 + 0.69314718055994530942 * (st->omega_ref + mustar + log2(Z)));
+    o3.z = (float)(C1n + 0.69314718055994530942 * (st->omega_ref + mustar + log2(Z)));
     o3.w = (float)(O * iz);
     reinterpret_cast<float4*>(r)[0] = o0;
     reinterpret_cast<float4*>(r)[1] = o1;
@@ -1362,14 +1385,14 @@ int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
 size_t estep_partial_bytes(const Sched& s) { return (size_t)s.nblk * s.kmax * kPartF * s.B * sizeof(float); }
 
 void estep_launch_setup(IterState* st, const void* d_target, const double* R, const double* t, double sigma2,
-                        double w, double V, int64_t M, int consistent, cudaStream_t stream) {
+                        double w, double V, int64_t M, int consistent, double eta, cudaStream_t stream) {
     estep_setup_kernel<<<1, 1, 0, stream>>>(st, reinterpret_cast<const TargetHeader*>(d_target), R[0], R[1], R[2],
                                              R[3], R[4], R[5], R[6], R[7], R[8], t[0], t[1], t[2], sigma2, w, V, M,
-                                             consistent);
+                                             consistent, eta);
 }
 
 void estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
-                  float* part, float* rec, int consistent, cudaStream_t stream) {
+                  float* part, float* rec, int consistent, const float* phi, cudaStream_t stream) {
     const float* body = target_body(d_target);
     const bool tc = sc.variant < 0;
     const Variant& V = kVariants[tc ? -1 - sc.variant : sc.variant];
@@ -1391,7 +1414,7 @@ void estep_launch(const void* d_target, const float* d_src, int64_t N, const Ite
     }
     cudaLaunchKernel(V.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3((V.ncw + 1) * 32), args, 0, stream);
     const int mt = 256;
-    estep_merge_kernel<<<(unsigned)((N + mt - 1) / mt), mt, 0, stream>>>(part, N, st, sc, rec);
+    estep_merge_kernel<<<(unsigned)((N + mt - 1) / mt), mt, 0, stream>>>(part, N, st, sc, rec, phi);
 }
 
 }  // namespace lsg

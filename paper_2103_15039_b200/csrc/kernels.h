@@ -7,6 +7,8 @@ namespace lsg {
 // Registration parameters passed by value to the device-side EM state machine.
 struct RegParams {
     double w, V, floor, tol, omega_ref_target;
+    double eta, spc;          // outlier ratio (< 0: use w) and the target's Σ π √(1+α) (Eq. 7)
+    const float* phi;         // per-source-point confidences φ(x_n) (Eq. 8) or NULL
     int64_t M;
     int newton_max, consistent, max_iters;
 };
@@ -15,9 +17,10 @@ struct RegParams {
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc);
 size_t estep_partial_bytes(const Sched& s);
 void estep_launch_setup(IterState* st, const void* d_target, const double* R, const double* t, double sigma2,
-                        double w, double V, int64_t M, int consistent, cudaStream_t stream);
+                        double w, double V, int64_t M, int consistent, double eta, cudaStream_t stream);
+// phi: optional per-source-point confidence φ(x_n) (Eq. 8: w_n = 1 - (1 - w0) φ(x_n)), NULL = uniform w0
 void estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
-                  float* part, float* rec, int consistent, cudaStream_t stream);
+                  float* part, float* rec, int consistent, const float* phi, cudaStream_t stream);
 
 // mstep.cu
 constexpr int kMomentCount = 75;          // G 60, U 12, σ²ΣD, ΣP, Σ ln p
@@ -36,6 +39,13 @@ size_t prepare_ws_bytes(int64_t M);
 size_t pack_ws_bytes(int64_t M);
 int pack_target_impl(const float* d_xyz, const float* d_nrm, const float* d_alpha, int64_t M, double margin,
                      void* d_target, void* d_ws, lsgcpd_target_info* info, cudaStream_t stream);
+size_t prior_ws_bytes(int64_t M);
+int set_prior_impl(void* d_target, int64_t M, const float* d_phi, void* d_ws, double* h_spc, cudaStream_t stream);
+size_t select_ws_bytes(int64_t n);
+int select_confident_impl(const float* d_xyz, const float* d_phi, int64_t n, float threshold, float* d_xyz_out,
+                          float* d_phi_out, int64_t* h_n_out, void* d_ws, cudaStream_t stream);
+void depth_confidence_launch(const float* d_xyz, int64_t n, double c0, double c1, double z_min, float* d_phi,
+                             cudaStream_t stream);
 int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p, void* d_target, void* d_ws,
                         lsgcpd_target_info* info, const lsgcpd_annotations* ann, cudaStream_t stream);
 

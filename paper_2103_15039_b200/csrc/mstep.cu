@@ -111,7 +111,7 @@ __global__ void sigma2_init_kernel(IterState* st, const TargetHeader* hdr, const
     if (!(s2 > 0.0)) s2 = ((double)rp.M * sums[0] + N * hdr->syy) / (3.0 * (double)rp.M * N);
     const double floor = rp.floor;
     if (s2 < floor) s2 = floor;
-    make_state(s, s.R, s.t, s2, rp.w, rp.V, rp.M, rp.omega_ref_target, rp.consistent);
+    make_state(s, s.R, s.t, s2, rp.w, rp.V, rp.M, rp.omega_ref_target, rp.consistent, rp.eta, rp.spc);
     s.extent = hdr->extent;
     s.active = 1;
     s.iter = 0;
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(32) newton_kernel(IterState* st, const double*
     double Rf[9], tf[3];
     for (int i = 0; i < 9; ++i) Rf[i] = Rs[i];
     for (int i = 0; i < 3; ++i) tf[i] = tsh[i];
-    make_state(nx, Rf, tf, s2, rp.w, rp.V, rp.M, rp.omega_ref_target, rp.consistent);
+    make_state(nx, Rf, tf, s2, rp.w, rp.V, rp.M, rp.omega_ref_target, rp.consistent, rp.eta, rp.spc);
     nx.extent = s.extent;
     nx.iter = k + 1;
     nx.no_mass = has_mass ? 0 : s.no_mass + 1;

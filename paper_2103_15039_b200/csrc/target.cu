@@ -29,17 +29,18 @@ __global__ void __launch_bounds__(kRedThreads)
     block_reduce_store<9, 6, kRedThreads>(v, blockpart, out, counter);
 }
 
-// stats2 (after the model is built): [max ω, Σ α, Σ ||y - ȳ||², Σ nn-distance, n_degenerate]
+// stats2 (after the model is built): [max ω, Σ α, Σ ||y - ȳ||², Σ nn-distance, n_degenerate, Σ √(1+α)]
 __global__ void __launch_bounds__(kRedThreads)
     model_stats_kernel(const float* __restrict__ xyz, const float* __restrict__ alpha, const float* __restrict__ nnd,
                        const int* __restrict__ degen, int64_t M, const double* __restrict__ stats1, double* blockpart,
                        double* out, unsigned* counter) {
-    double v[5] = {-INFINITY, 0.0, 0.0, 0.0, 0.0};
+    double v[6] = {-INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0};
     const double yb[3] = {stats1[6] / M, stats1[7] / M, stats1[8] / M};
     for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
         const double a = alpha[m];
         v[0] = fmax(v[0], 0.5 * log2(1.0 + a));
         v[1] += a;
+        v[5] += sqrt(1.0 + a);
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
             const double d = (double)xyz[3 * m + i] - yb[i];
@@ -48,7 +49,7 @@ __global__ void __launch_bounds__(kRedThreads)
         if (nnd) v[3] += nnd[m];
         if (degen) v[4] += degen[m];
     }
-    block_reduce_store<5, 1, kRedThreads>(v, blockpart, out, counter);
+    block_reduce_store<6, 1, kRedThreads>(v, blockpart, out, counter);
 }
 
 // Header: AABB, centroid, V (margin per side; a zero-extent axis is floored at the mean
@@ -83,9 +84,11 @@ __global__ void header_kernel(TargetHeader* hdr, int64_t M, const double* stats1
     h.volume = V;
     h.syy = stats2[2];
     h.alpha_sum = stats2[1];
+    h.spc = stats2[5] / (double)M;   // uniform prior π(m) = 1/M
     h.n_degenerate = (int64_t)stats2[4];
     h.magic = kTargetMagic;
-    h.pad_[0] = h.pad_[1] = h.pad_[2] = 0;
+    h.prior = 0;
+    h.pad_[0] = h.pad_[1] = 0;
     *hdr = h;
 }
 
@@ -497,6 +500,157 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
                                                                         nnd, degen);
     LSG_CUDA(cudaGetLastError());
     return finish_target(d_xyz, nrm, alp, nnd, degen, M, p.volume_margin, ws, L, d_target, info, stream);
+}
+
+// ---- confidence filtering (Eq. 8) ----------------------------------------------------------
+// Component prior π(m) = φ(y_m)/Σφ folds into the per-target log2 weight: ω_m = ½log2(1+α_m) + log2(M π(m))
+// (the E step's constant keeps ln((1-w)/M)), re-referenced to ω_ref = max_m ω_m.  α_m = tr(α n nᵀ) is read
+// back from the packed model, so the call is idempotent (it never compounds an earlier prior).
+__device__ __forceinline__ double packed_alpha(const float* __restrict__ body, int64_t m) {
+    const float* b = body + (m >> 1) * (2 * kTgtFloats) + (m & 1);
+    return (double)b[2 * 7] + (double)b[2 * 10] + (double)b[2 * 12];   // W_xx + W_yy + W_zz
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+    prior_sum_kernel(const float* __restrict__ phi, int64_t M, double* blockpart, double* out, unsigned* counter) {
+    double v[4] = {-INFINITY, -INFINITY, 0.0, 0.0};   // [max φ, -min φ, Σ φ, #invalid]
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
+        const double f = phi[m];
+        if (isfinite(f) && f >= 0.0) {
+            v[0] = fmax(v[0], f);
+            v[1] = fmax(v[1], -f);
+            v[2] += f;
+        } else {
+            v[3] += 1.0;
+        }
+    }
+    block_reduce_store<4, 2, kRedThreads>(v, blockpart, out, counter);
+}
+
+// out: [max ω, Σ π √(1+α)]
+__global__ void __launch_bounds__(kRedThreads)
+    prior_stats_kernel(const float* __restrict__ phi, const float* __restrict__ body, int64_t M,
+                       const double* __restrict__ sums, double* blockpart, double* out, unsigned* counter) {
+    double v[2] = {-INFINITY, 0.0};
+    const double inv = 1.0 / sums[2];
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
+        const double pi = (double)phi[m] * inv;
+        const double a = packed_alpha(body, m);
+        if (pi > 0.0) v[0] = fmax(v[0], 0.5 * log2(1.0 + a) + log2((double)M * pi));
+        v[1] += pi * sqrt(1.0 + a);
+    }
+    block_reduce_store<2, 1, kRedThreads>(v, blockpart, out, counter);
+}
+
+__global__ void prior_write_kernel(const float* __restrict__ phi, float* __restrict__ body, float* __restrict__ tc,
+                                   int64_t M, const double* __restrict__ sums, const double* __restrict__ stats,
+                                   TargetHeader* hdr) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m == 0) {
+        hdr->omega_ref = stats[0];
+        hdr->spc = stats[1];
+        hdr->prior = (sums[0] != -sums[1]) ? 1u : 0u;   // max φ ≠ min φ: non-uniform
+    }
+    if (m >= M) return;
+    const double pi = (double)phi[m] / sums[2];
+    const double a = packed_alpha(body, m);
+    const float om = pi > 0.0 ? (float)(0.5 * log2(1.0 + a) + log2((double)M * pi) - stats[0]) : -INFINITY;
+    body[(m >> 1) * (2 * kTgtFloats) + (m & 1) + 2 * 3] = om;
+    const int64_t tile = m / kTcTile;
+    const int jt = (int)(m % kTcTile);
+    float* core = reinterpret_cast<float*>(reinterpret_cast<char*>(tc) + tile * kTcTileBytes) + (jt >> 1) * 16 + (jt & 1);
+    core[2 * 3] = om;
+}
+
+size_t prior_ws_bytes(int64_t M) {
+    (void)M;
+    return al(sizeof(double) * kRedBlocks * 4) + al(sizeof(double) * 8) + al(sizeof(unsigned) * 4);   // K ≤ 4
+}
+
+int set_prior_impl(void* d_target, int64_t M, const float* d_phi, void* d_ws, double* h_spc, cudaStream_t stream) {
+    char* ws = static_cast<char*>(d_ws);
+    double* bp = reinterpret_cast<double*>(ws);
+    double* st = reinterpret_cast<double*>(ws + al(sizeof(double) * kRedBlocks * 4));
+    unsigned* ctr = reinterpret_cast<unsigned*>(ws + al(sizeof(double) * kRedBlocks * 4) + al(sizeof(double) * 8));
+    LSG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 4, stream));
+    prior_sum_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_phi, M, bp, st, ctr);
+    double sums[4];
+    LSG_CUDA(cudaMemcpyAsync(sums, st, sizeof(sums), cudaMemcpyDeviceToHost, stream));
+    LSG_CUDA(cudaStreamSynchronize(stream));
+    LSG_CHECK(sums[3] == 0.0, LSGCPD_EINVAL, "%lld target confidences are negative or non-finite", (long long)sums[3]);
+    LSG_CHECK(sums[2] > 0.0 && isfinite(sums[2]), LSGCPD_EINVAL, "all target confidences are zero");
+    const int64_t M_pad = pad_targets(M);
+    float* body = target_body(d_target);
+    prior_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_phi, body, M, st, bp, st + 4, ctr);
+    prior_write_kernel<<<(unsigned)((M + 255) / 256), 256, 0, stream>>>(d_phi, body, target_tc(d_target, M_pad), M, st,
+                                                                        st + 4, reinterpret_cast<TargetHeader*>(d_target));
+    LSG_CUDA(cudaGetLastError());
+    if (h_spc) {
+        LSG_CUDA(cudaMemcpyAsync(h_spc, st + 5, sizeof(double), cudaMemcpyDeviceToHost, stream));
+        LSG_CUDA(cudaStreamSynchronize(stream));
+    }
+    return 0;
+}
+
+// ---- confidence truncation and the depth error model (reading R23) ----------------------------
+__global__ void select_flags_kernel(const float* __restrict__ phi, int64_t n, float thr, int* __restrict__ flags) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[i] = phi[i] >= thr ? 1 : 0;
+}
+__global__ void select_scatter_kernel(const float* __restrict__ xyz, const float* __restrict__ phi, int64_t n,
+                                      const int* __restrict__ flags, const int* __restrict__ pos,
+                                      float* __restrict__ xyz_out, float* __restrict__ phi_out, int64_t* count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (i == n - 1) *count = (int64_t)pos[i] + flags[i];
+    if (!flags[i]) return;
+    const int64_t o = pos[i];
+    xyz_out[3 * o] = xyz[3 * i];
+    xyz_out[3 * o + 1] = xyz[3 * i + 1];
+    xyz_out[3 * o + 2] = xyz[3 * i + 2];
+    if (phi_out) phi_out[o] = phi[i];
+}
+
+static size_t scan_tmp_bytes(int64_t n) {
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (const int*)nullptr, (int*)nullptr, (int)n);
+    return b;
+}
+size_t select_ws_bytes(int64_t n) {
+    return al(sizeof(int) * n) * 2 + al(sizeof(int64_t)) + al(scan_tmp_bytes(n));
+}
+
+int select_confident_impl(const float* d_xyz, const float* d_phi, int64_t n, float threshold, float* d_xyz_out,
+                          float* d_phi_out, int64_t* h_n_out, void* d_ws, cudaStream_t stream) {
+    char* ws = static_cast<char*>(d_ws);
+    int* flags = reinterpret_cast<int*>(ws);
+    int* pos = reinterpret_cast<int*>(ws + al(sizeof(int) * n));
+    int64_t* cnt = reinterpret_cast<int64_t*>(ws + 2 * al(sizeof(int) * n));
+    void* tmp = ws + 2 * al(sizeof(int) * n) + al(sizeof(int64_t));
+    size_t tb = scan_tmp_bytes(n);
+    const unsigned g = (unsigned)((n + 255) / 256);
+    select_flags_kernel<<<g, 256, 0, stream>>>(d_phi, n, threshold, flags);
+    LSG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, flags, pos, (int)n, stream));
+    select_scatter_kernel<<<g, 256, 0, stream>>>(d_xyz, d_phi, n, flags, pos, d_xyz_out, d_phi_out, cnt);
+    LSG_CUDA(cudaGetLastError());
+    LSG_CUDA(cudaMemcpyAsync(h_n_out, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+    LSG_CUDA(cudaStreamSynchronize(stream));
+    return 0;
+}
+
+// φ = e_min / e(z), e(z) = c0 + c1 z² of the camera-frame depth z (the point's third coordinate),
+// e_min = e(z_min); clipped to [0, 1].
+__global__ void depth_confidence_kernel(const float* __restrict__ xyz, int64_t n, double c0, double c1, double zmin,
+                                        float* __restrict__ phi) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double z = xyz[3 * i + 2];
+    const double f = (c0 + c1 * zmin * zmin) / (c0 + c1 * z * z);
+    phi[i] = (float)fmin(fmax(isfinite(f) ? f : 0.0, 0.0), 1.0);
+}
+void depth_confidence_launch(const float* d_xyz, int64_t n, double c0, double c1, double z_min, float* d_phi,
+                             cudaStream_t stream) {
+    depth_confidence_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(d_xyz, n, c0, c1, z_min, d_phi);
 }
 
 }  // namespace lsg

@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_version_and_pure_host_queries(L):
-    assert L.lsgcpd_version() == 10000
+    assert L.lsgcpd_version() == 10100
     assert L.lsgcpd_last_error() is not None
     assert L.lsgcpd_target_bytes(1000) == 256 + 1024 * 64 + (1024 // 64) * 10240   # + tensor-core section
     assert L.lsgcpd_target_bytes(0) == 256
@@ -49,12 +49,15 @@ def test_struct_layouts_match_header(tmp_path):
     prog.write_text('#include "lsgcpd.h"\n#include <stdio.h>\n#include <stddef.h>\n'
                     'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(lsgcpd_prep_params),'
                     ' sizeof(lsgcpd_target_info), sizeof(lsgcpd_annotations), sizeof(lsgcpd_em_params),'
-                    ' offsetof(lsgcpd_em_params, sigma2_init), offsetof(lsgcpd_target_info, n_degenerate));return 0;}\n')
+                    ' offsetof(lsgcpd_em_params, sigma2_init), offsetof(lsgcpd_target_info, n_degenerate));'
+                    'printf("%zu %zu\\n", offsetof(lsgcpd_em_params, eta), offsetof(lsgcpd_em_params, d_src_conf));'
+                    'return 0;}\n')
     exe = tmp_path / "sizes"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)])
     got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
     want = [ctypes.sizeof(pkg.PrepParams), ctypes.sizeof(pkg.TargetInfo), ctypes.sizeof(pkg.Annotations),
-            ctypes.sizeof(pkg.EmParams), pkg.EmParams.sigma2_init.offset, pkg.TargetInfo.n_degenerate.offset]
+            ctypes.sizeof(pkg.EmParams), pkg.EmParams.sigma2_init.offset, pkg.TargetInfo.n_degenerate.offset,
+            pkg.EmParams.eta.offset, pkg.EmParams.d_src_conf.offset]
     assert got == want
 
 

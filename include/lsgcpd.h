@@ -200,6 +200,36 @@ int lsgcpd_register(const void* d_target, int64_t M, double volume, const float*
                     int* iters_out, double* nll_trace, double* sigma2_trace, void* comm,
                     void* d_ws, size_t ws_bytes, lsgcpd_stream_t stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Batched registrations (many small independent problems in one EM loop, SURVEY §8(f) NEXT-3;
+ * the paper's workloads are 3.5k-5k-point pairs).  Every iteration is
+ * ONE batched E-step launch over the units of all problems (stream-K), one merge, one moments
+ * launch (a CTA per problem) and one Newton launch (a warp per problem), replayed as a CUDA graph.
+ * Per problem: its own prepared target (priors as installed), source, volume and initial pose;
+ * shared: params (w / eta, iterations, normaliser, floors).  Results match per-problem
+ * lsgcpd_register up to FP32 summation order (the batched E step runs on CUDA cores).
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+    const void* d_target;      /* prepared target of this problem (16-byte aligned)               */
+    int64_t M;                 /* its number of targets                                          */
+    const float* d_src;        /* DEVICE [N][3] source points                                    */
+    int64_t N;                 /* ≥ 1                                                             */
+    const float* d_src_conf;   /* DEVICE [N] φ(x_n) (Eq. 8) or NULL                               */
+    double volume;             /* ≤ 0: the target's V                                            */
+    double R0[9], t0[3];       /* initial pose (row-major R)                                     */
+} lsgcpd_problem;
+
+/* Workspace for B problems (depends on every problem's M and N).  0 on invalid sizes. */
+size_t lsgcpd_register_batch_workspace_bytes(const lsgcpd_problem* h_problems, int B, int max_iters);
+/* sync.  Outputs (HOST, B entries each): R_out [B][9], t_out [B][3], sigma2_out, iters_out,
+ * status_out (0, or LSGCPD_ENOMASS for a problem that lost its inlier mass; the others are
+ * unaffected).  params->d_src_conf is ignored (per-problem d_src_conf is used).
+ * Errors: EINVAL (null, B < 1, bad sizes, bad target / priors with the literal form, bad
+ * params, ws too small), ECUDA. */
+int lsgcpd_register_batch(const lsgcpd_problem* h_problems, int B, const lsgcpd_em_params* params,
+                          double* R_out, double* t_out, double* sigma2_out, int* iters_out,
+                          int* status_out, void* d_ws, size_t ws_bytes, lsgcpd_stream_t stream);
+
 /* Defaults for the parameter structs (the values documented above). */
 void lsgcpd_prep_params_default(lsgcpd_prep_params* p);
 void lsgcpd_em_params_default(lsgcpd_em_params* p);

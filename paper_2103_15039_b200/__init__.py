@@ -54,6 +54,12 @@ class EmParams(ctypes.Structure):
                 ("d_src_conf", ctypes.c_void_p)]
 
 
+class Problem(ctypes.Structure):
+    _fields_ = [("d_target", ctypes.c_void_p), ("M", ctypes.c_int64), ("d_src", ctypes.c_void_p), ("N", ctypes.c_int64),
+                ("d_src_conf", ctypes.c_void_p), ("volume", ctypes.c_double), ("R0", ctypes.c_double * 9),
+                ("t0", ctypes.c_double * 3)]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -79,6 +85,9 @@ _SIGS = {
     "lsgcpd_select_confident": ([_vp, _vp, _i64, ctypes.c_float, _vp, _vp, ctypes.POINTER(ctypes.c_int64), _vp, _sz,
                                  _vp], _i32),
     "lsgcpd_depth_confidence": ([_vp, _i64, _d, _d, _d, _vp, _vp], _i32),
+    "lsgcpd_register_batch_workspace_bytes": ([ctypes.POINTER(Problem), _i32, _i32], _sz),
+    "lsgcpd_register_batch": ([ctypes.POINTER(Problem), _i32, ctypes.POINTER(EmParams), _dp, _dp, _dp,
+                               ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), _vp, _sz, _vp], _i32),
     "lsgcpd_comm_unique_id": ([_vp], _i32),
     "lsgcpd_comm_init": ([_i32, _i32, _vp, ctypes.POINTER(ctypes.c_void_p)], _i32),
     "lsgcpd_comm_destroy": ([_vp], _i32),
@@ -355,3 +364,57 @@ class Registrar:
 def register(target: Target, src_local, max_iters: int, **kw):
     """lsgcpd_register → dict(R, t, sigma2, iters, status[, nll, sigma2_trace])."""
     return Registrar(target, src_local, max_iters)(**kw)
+
+
+class BatchRegistrar:
+    """Reusable lsgcpd_register_batch launcher: B independent problems (targets, sources, optional
+    confidences, volumes, initial poses) registered together, one batched E step per EM iteration."""
+
+    def __init__(self, targets, sources, max_iters: int, src_confs=None, volumes=None, R0s=None, t0s=None):
+        B = len(targets)
+        if len(sources) != B or B < 1:
+            raise ValueError("need one source per target")
+        self.targets, self.sources = list(targets), list(sources)
+        self.confs = list(src_confs) if src_confs is not None else [None] * B
+        self.max_iters = int(max_iters)
+        arr = (Problem * B)()
+        for b, (tg, src) in enumerate(zip(self.targets, self.sources)):
+            _need_cuda_f32(src, "source", 3)
+            pb = arr[b]
+            pb.d_target = tg.buf.data_ptr()
+            pb.M = tg.M
+            pb.d_src = src.data_ptr()
+            pb.N = int(src.shape[0])
+            pb.d_src_conf = _conf_ptr(self.confs[b], pb.N)
+            pb.volume = 0.0 if volumes is None else float(volumes[b])
+            R0 = np.eye(3) if R0s is None else np.asarray(R0s[b], dtype=np.float64)
+            t0 = np.zeros(3) if t0s is None else np.asarray(t0s[b], dtype=np.float64)
+            for i in range(9):
+                pb.R0[i] = float(R0.reshape(9)[i])
+            for i in range(3):
+                pb.t0[i] = float(t0[i])
+        self.problems, self.B = arr, B
+        nbytes = lib().lsgcpd_register_batch_workspace_bytes(arr, B, self.max_iters)
+        if nbytes == 0:
+            raise LsgcpdError(-1, "invalid batch")
+        self.ws = _alloc_bytes(nbytes, self.sources[0].device)
+
+    def __call__(self, w: float = 0.1, newton_max: int = 10, consistent: bool = True, sigma2_init: float = 0.0,
+                 sigma2_floor_rel: float = 1e-12, tol: float = 0.0, eta: Optional[float] = None, stream=None):
+        p = EmParams(w, self.max_iters, newton_max, int(bool(consistent)), sigma2_init, sigma2_floor_rel, tol,
+                     -1.0 if eta is None else float(eta), None)
+        B = self.B
+        R = np.zeros((B, 9))
+        t = np.zeros((B, 3))
+        s2 = np.zeros(B)
+        it = (ctypes.c_int * B)()
+        stt = (ctypes.c_int * B)()
+        _check(lib().lsgcpd_register_batch(self.problems, B, ctypes.byref(p), R.ctypes.data_as(_dp),
+                                           t.ctypes.data_as(_dp), s2.ctypes.data_as(_dp), it, stt,
+                                           self.ws.data_ptr(), self.ws.numel(), _stream_ptr(stream)))
+        return {"R": R.reshape(B, 3, 3), "t": t, "sigma2": s2, "iters": np.array(it[:]), "status": np.array(stt[:])}
+
+
+def register_batch(targets, sources, max_iters: int, src_confs=None, volumes=None, R0s=None, t0s=None, **kw):
+    """lsgcpd_register_batch → dict(R [B,3,3], t [B,3], sigma2 [B], iters [B], status [B])."""
+    return BatchRegistrar(targets, sources, max_iters, src_confs, volumes, R0s, t0s)(**kw)

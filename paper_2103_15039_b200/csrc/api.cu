@@ -4,6 +4,7 @@
 #include <string.h>
 
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -534,5 +535,194 @@ LSG_EXPORT int lsgcpd_depth_confidence(const float* d_xyz, int64_t n, double c0,
               LSGCPD_EINVAL, "error model must have c0, c1 >= 0 and e(z_min) > 0");
     depth_confidence_launch(d_xyz, n, c0, c1, z_min, d_phi, (cudaStream_t)stream);
     LSG_CUDA(cudaGetLastError());
+    return 0;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Batched registrations
+// ---------------------------------------------------------------------------------------------
+namespace lsg {
+struct BatchLayout {
+    size_t desc, st, mom, bpart, ctr, nll, sig2, iters, err, part, rec, total;
+    int64_t units, nblk_tot, pts, kmax;
+    Sched sc;
+};
+
+static int batch_layout(const lsgcpd_problem* P, int B, int max_iters, BatchLayout* L, std::vector<BatchProblem>* out) {
+    LSG_CHECK(P && B >= 1 && B <= (1 << 20), LSGCPD_EINVAL, "bad problem list (B=%d)", B);
+    LSG_CHECK(max_iters >= 0 && max_iters <= 100000, LSGCPD_EINVAL, "max_iters out of range");
+    const int64_t kB = batch_block_points();
+    std::vector<BatchProblem> bp(B);
+    int64_t units = 0, pts = 0, nblk_tot = 0;
+    for (int b = 0; b < B; ++b) {
+        const lsgcpd_problem& p = P[b];
+        LSG_CHECK(p.d_target && p.d_src, LSGCPD_EINVAL, "problem %d: null pointer", b);
+        LSG_CHECK(aligned16(p.d_target), LSGCPD_EINVAL, "problem %d: d_target must be 16-byte aligned", b);
+        LSG_CHECK(p.M >= 1 && p.N >= 1 && p.M < (int64_t)1 << 30 && p.N < (int64_t)1 << 30, LSGCPD_EINVAL,
+                  "problem %d: M=%lld N=%lld out of range", b, (long long)p.M, (long long)p.N);
+        LSG_CHECK(is_rotation(p.R0) && finite_vec(p.t0, 3), LSGCPD_EINVAL, "problem %d: bad initial pose", b);
+        LSG_CHECK(isfinite(p.volume), LSGCPD_EINVAL, "problem %d: volume must be finite", b);
+        BatchProblem& q = bp[b];
+        memset(&q, 0, sizeof(q));
+        const int64_t M_pad = pad_targets(p.M);
+        q.target = p.d_target;
+        q.body = target_body(p.d_target);
+        q.src = p.d_src;
+        q.conf = p.d_src_conf;
+        q.M = p.M;
+        q.N = p.N;
+        q.T = M_pad / kTT_host;
+        q.nblk = (p.N + kB - 1) / kB;
+        q.unit0 = units;
+        q.pt0 = pts;
+        q.volume = p.volume;
+        for (int i = 0; i < 9; ++i) q.R0[i] = p.R0[i];
+        for (int i = 0; i < 3; ++i) q.t0[i] = p.t0[i];
+        units += q.nblk * q.T;
+        pts += p.N;
+        nblk_tot += q.nblk;
+    }
+    int dev, nsm;
+    LSG_CUDA(cudaGetDevice(&dev));
+    LSG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    Sched sc;
+    memset(&sc, 0, sizeof(sc));
+    sc.U = units;
+    const int64_t slots = (int64_t)nsm * 4;   // kBMinB CTAs per SM
+    sc.G = units < slots ? units : slots;
+    sc.B = kB;
+    int64_t kmax = 1;
+    for (int b = 0; b < B; ++b)
+        for (int64_t j = 0; j < bp[b].nblk; ++j) {
+            const int64_t k = sched_owner(sc, bp[b].unit0 + (j + 1) * bp[b].T - 1) -
+                              sched_owner(sc, bp[b].unit0 + j * bp[b].T) + 1;
+            if (k > kmax) kmax = k;
+        }
+    sc.kmax = kmax;
+    int64_t part0 = 0;
+    for (int b = 0; b < B; ++b) {
+        bp[b].part0 = part0;
+        part0 += (int64_t)batch_partial_floats(bp[b].nblk, kmax);
+    }
+    size_t o = 0;
+    L->desc = o; o += al(sizeof(BatchProblem) * B);
+    L->st = o; o += al(sizeof(IterState) * B);
+    L->mom = o; o += al(sizeof(double) * kBatchMom * B);
+    L->bpart = o; o += al(sizeof(double) * 80 * B);
+    L->ctr = o; o += al(sizeof(unsigned) * B);
+    L->nll = o; o += al(sizeof(double) * (max_iters + 1) * B);
+    L->sig2 = o; o += al(sizeof(double) * (max_iters + 2) * B);
+    L->iters = o; o += al(sizeof(int) * B);
+    L->err = o; o += al(sizeof(int) * B);
+    L->part = o; o += al(sizeof(float) * (size_t)part0);
+    L->rec = o; o += al(sizeof(float) * LSGCPD_REC * (size_t)pts);
+    L->total = o;
+    L->units = units;
+    L->nblk_tot = nblk_tot;
+    L->pts = pts;
+    L->kmax = kmax;
+    L->sc = sc;
+    if (out) out->swap(bp);
+    return 0;
+}
+}  // namespace lsg
+
+LSG_EXPORT size_t lsgcpd_register_batch_workspace_bytes(const lsgcpd_problem* h_problems, int B, int max_iters) {
+    BatchLayout L;
+    if (batch_layout(h_problems, B, max_iters, &L, nullptr)) return 0;
+    return L.total;
+}
+
+LSG_EXPORT int lsgcpd_register_batch(const lsgcpd_problem* h_problems, int B, const lsgcpd_em_params* params,
+                                     double* R_out, double* t_out, double* sigma2_out, int* iters_out, int* status_out,
+                                     void* d_ws, size_t ws_bytes, lsgcpd_stream_t stream) {
+    lsgcpd_em_params p;
+    lsgcpd_em_params_default(&p);
+    if (params) p = *params;
+    LSG_CHECK(R_out && t_out && sigma2_out && iters_out && status_out && d_ws, LSGCPD_EINVAL, "null pointer argument");
+    LSG_CHECK(aligned16(d_ws), LSGCPD_EINVAL, "d_ws must be 16-byte aligned");
+    LSG_CHECK(isfinite(p.w) && p.w >= 0.0 && p.w < 1.0, LSGCPD_EINVAL, "w must be in [0, 1)");
+    LSG_CHECK(!(p.eta >= 1.0) && !isnan(p.eta), LSGCPD_EINVAL, "eta must be < 1 (negative: off)");
+    LSG_CHECK(p.newton_max >= 0 && p.newton_max <= 1000, LSGCPD_EINVAL, "newton_max out of range");
+    LSG_CHECK(isfinite(p.sigma2_floor_rel) && p.sigma2_floor_rel >= 0.0, LSGCPD_EINVAL, "bad sigma2_floor_rel");
+    LSG_CHECK(isfinite(p.sigma2_init) && isfinite(p.tol), LSGCPD_EINVAL, "sigma2_init and tol must be finite");
+    BatchLayout L;
+    std::vector<BatchProblem> bp;
+    int rc = batch_layout(h_problems, B, p.max_iters, &L, &bp);
+    if (rc) return rc;
+    LSG_CHECK(ws_bytes >= L.total, LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
+    cudaStream_t s = (cudaStream_t)stream;
+    char* ws = static_cast<char*>(d_ws);
+    BatchProblem* dbp = reinterpret_cast<BatchProblem*>(ws + L.desc);
+    IterState* st = reinterpret_cast<IterState*>(ws + L.st);
+    double* mom = reinterpret_cast<double*>(ws + L.mom);
+    int* err = reinterpret_cast<int*>(ws + L.err);
+    LSG_CUDA(cudaMemcpyAsync(dbp, bp.data(), sizeof(BatchProblem) * B, cudaMemcpyHostToDevice, s));
+    const int consistent = p.consistent_normalizer ? 1 : 0;
+    batch_fill_launch(dbp, B, consistent, err, s);
+    std::vector<int> herr(B);
+    LSG_CUDA(cudaMemcpyAsync(herr.data(), err, sizeof(int) * B, cudaMemcpyDeviceToHost, s));
+    LSG_CUDA(cudaStreamSynchronize(s));
+    for (int b = 0; b < B; ++b) {
+        LSG_CHECK(herr[b] != 1, LSGCPD_EINVAL, "problem %d: d_target is not a prepared target with M=%lld", b,
+                  (long long)bp[b].M);
+        LSG_CHECK(herr[b] != 2, LSGCPD_EINVAL, "problem %d: component priors require consistent_normalizer = 1", b);
+    }
+    RegParams rp;
+    memset(&rp, 0, sizeof(rp));
+    rp.w = p.eta >= 0.0 ? 0.0 : p.w;
+    rp.eta = p.eta >= 0.0 ? p.eta : -1.0;
+    rp.floor = p.sigma2_floor_rel;   // relative: scaled by each problem's extent² on the device
+    rp.tol = p.tol;
+    rp.newton_max = p.newton_max;
+    rp.consistent = consistent;
+    rp.max_iters = p.max_iters;
+    LSG_CUDA(cudaMemsetAsync(ws + L.iters, 0, sizeof(int) * B, s));
+    LSG_CUDA(cudaMemsetAsync(ws + L.nll, 0, sizeof(double) * (p.max_iters + 1) * B, s));
+    init_batch_launch(dbp, B, st, rp, p.sigma2_init, mom, reinterpret_cast<double*>(ws + L.sig2), s);
+    LSG_CUDA(cudaGetLastError());
+    float* part = reinterpret_cast<float*>(ws + L.part);
+    float* rec = reinterpret_cast<float*>(ws + L.rec);
+    auto enqueue = [&](cudaStream_t q) {
+        estep_batch_launch(dbp, B, L.sc, st, part, rec, L.pts, consistent, q);
+        moments_batch_launch(dbp, B, rec, st, reinterpret_cast<double*>(ws + L.bpart), mom,
+                             reinterpret_cast<unsigned*>(ws + L.ctr), q);
+        newton_batch_launch(dbp, B, st, mom, rp, reinterpret_cast<double*>(ws + L.nll),
+                            reinterpret_cast<double*>(ws + L.sig2), reinterpret_cast<int*>(ws + L.iters), q);
+    };
+    if (p.max_iters > 0) {
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        cudaStream_t cs;
+        LSG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaEvent_t ev;
+        LSG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        LSG_CUDA(cudaEventRecord(ev, s));
+        LSG_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+        LSG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        enqueue(cs);
+        cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+        LSG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        for (int k = 0; k < p.max_iters; ++k) LSG_CUDA(cudaGraphLaunch(exec, cs));
+        LSG_CUDA(cudaEventRecord(ev, cs));
+        LSG_CUDA(cudaStreamWaitEvent(s, ev, 0));
+        LSG_CUDA(cudaStreamSynchronize(s));
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+        cudaEventDestroy(ev);
+        cudaStreamDestroy(cs);
+    }
+    std::vector<IterState> fin(B);
+    LSG_CUDA(cudaMemcpyAsync(fin.data(), st, sizeof(IterState) * B, cudaMemcpyDeviceToHost, s));
+    LSG_CUDA(cudaMemcpyAsync(iters_out, ws + L.iters, sizeof(int) * B, cudaMemcpyDeviceToHost, s));
+    LSG_CUDA(cudaStreamSynchronize(s));
+    LSG_CUDA(cudaGetLastError());
+    for (int b = 0; b < B; ++b) {
+        for (int i = 0; i < 9; ++i) R_out[9 * b + i] = fin[b].R[i];
+        for (int i = 0; i < 3; ++i) t_out[3 * b + i] = fin[b].t[i];
+        sigma2_out[b] = fin[b].sigma2;
+        status_out[b] = fin[b].status == LSGCPD_ENOMASS ? LSGCPD_ENOMASS : 0;
+    }
     return 0;
 }

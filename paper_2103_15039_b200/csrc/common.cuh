@@ -74,6 +74,7 @@ inline float* target_body(void* t) { return reinterpret_cast<float*>(static_cast
 //                 (exact in FP32, read as TF32 by the MMA); UMMA K-major, no swizzle:
 //                 core matrix = 8 rows × 16 B (4 targets); LBO = 128 B (next 4 targets),
 //                 SBO = 256 B (next 8 rows): byte(row r, j) = 1024 s + (r/8) 256 + (j/4) 128 + (r%8) 16 + (j%4) 4.
+constexpr int kTT_host = 64;   // E-step target tile (targets), host-visible copy of estep_dev.cuh's kTT
 constexpr int kTcTile = 64;
 constexpr int kTcTileBytes = 10240;
 constexpr int kTcCoreBytes = 2048;
@@ -190,6 +191,24 @@ __device__ void block_reduce_store(double (&v)[K], double* blockpart, double* ou
             out[f] = s;
         }
         if (threadIdx.x == 0) *counter = 0u;
+    }
+}
+
+// Sum over one CTA (fixed order) of K values per thread → out[0..K) (thread 0 writes).
+template <int K, int NT>
+__device__ void block_reduce_single(double (&v)[K], double* out) {
+    __shared__ double sm[NT / 32][K];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int f = 0; f < K; ++f) {
+        const double s = warp_sum(v[f]);
+        if (lane == 0) sm[warp][f] = s;
+    }
+    __syncthreads();
+    for (int f = threadIdx.x; f < K; f += NT) {
+        double s = sm[0][f];
+        for (int w = 1; w < NT / 32; ++w) s += sm[w][f];
+        out[f] = s;
     }
 }
 

@@ -17,157 +17,10 @@
 // Arithmetic: packed f32x2 (FFMA2/FADD2/FMUL2) over two source points per instruction with the
 // target field as a broadcast operand (PACKED), or scalar FP32 (reference variant).
 #include "common.cuh"
+#include "estep_dev.cuh"
 #include "kernels.h"
 
 namespace lsg {
-
-constexpr int kTT = 64;                  // targets per pipeline stage (4 KB)
-constexpr int kStages = 6;
-constexpr int kPartF = 16;               // partial: S, Sy[3], SW[6], Sb[3], Sτ, μ, 0
-constexpr int kAcc = 14;
-
-// ---- accumulators ------------------------------------------------------------------------------
-// A register "lane" of type T is float (scalar mode) or float2 (two source points).
-template <typename T>
-struct Acc {
-    T v[kAcc];  // S, yx, yy, yz, W0..W5, bx, by, bz, τ
-};
-
-__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
-__device__ __forceinline__ float vadd(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ float2 vadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float vsub(float a, float b) { return __fsub_rn(a, b); }
-__device__ __forceinline__ float2 vsub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
-__device__ __forceinline__ float vmul(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ float2 vmul(float2 a, float2 b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ float vfma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-__device__ __forceinline__ float2 vfma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ float splat(float v, float) { return v; }
-__device__ __forceinline__ float2 splat(float v, float2) { return bc(v); }
-__device__ __forceinline__ float vzero(float) { return 0.f; }
-__device__ __forceinline__ float2 vzero(float2) { return make_float2(0.f, 0.f); }
-
-template <typename T>
-__device__ __forceinline__ void acc_zero(Acc<T>& a) {
-#pragma unroll
-    for (int i = 0; i < kAcc; ++i) a.v[i] = vzero(T());
-}
-template <typename T>
-__device__ __forceinline__ void acc_scale(Acc<T>& a, T s) {
-#pragma unroll
-    for (int i = 0; i < kAcc; ++i) a.v[i] = vmul(a.v[i], s);
-}
-// R += L with Kahan compensation C (true running sum ≈ R - C).
-template <typename T>
-__device__ __forceinline__ void acc_fold(Acc<T>& R, Acc<T>& C, const Acc<T>& L) {
-#pragma unroll
-    for (int i = 0; i < kAcc; ++i) {
-        const T y = vsub(L.v[i], C.v[i]);
-        const T t = vadd(R.v[i], y);
-        C.v[i] = vsub(vsub(t, R.v[i]), y);
-        R.v[i] = t;
-    }
-}
-
-// Target m of a tile, unpacked from the pair-interleaved layout: float4 k of a pair block holds
-// {f_a, f_b, (f+1)_a, (f+1)_b} for fields f = 2k.
-struct Tgt {
-    float y0, y1, y2, om, n0, n1, n2, w0, w1, w2, w3, w4, w5, b0, b1, b2;
-};
-__device__ __forceinline__ void load_pair(const float4* tp, Tgt& a, Tgt& b) {
-    const float4 v0 = tp[0], v1 = tp[1], v2 = tp[2], v3 = tp[3], v4 = tp[4], v5 = tp[5], v6 = tp[6], v7 = tp[7];
-    a = {v0.x, v0.z, v1.x, v1.z, v2.x, v2.z, v3.x, v3.z, v4.x, v4.z, v5.x, v5.z, v6.x, v6.z, v7.x, v7.z};
-    b = {v0.y, v0.w, v1.y, v1.w, v2.y, v2.w, v3.y, v3.w, v4.y, v4.w, v5.y, v5.w, v6.y, v6.w, v7.y, v7.w};
-}
-
-// τ = ||r||² + (ñ·r)² with r = (hi - y) + lo: the subtraction of two nearby FP32 values is exact,
-// so r is accurate relative to ||r|| rather than ||x̂||.
-template <typename T>
-__device__ __forceinline__ T pair_tau(const T (&h)[3], const T (&l)[3], const Tgt& t) {
-    const T rx = vadd(vsub(h[0], splat(t.y0, T())), l[0]);
-    const T ry = vadd(vsub(h[1], splat(t.y1, T())), l[1]);
-    const T rz = vadd(vsub(h[2], splat(t.y2, T())), l[2]);
-    const T q = vfma(splat(t.n2, T()), rz, vfma(splat(t.n1, T()), ry, vmul(splat(t.n0, T()), rx)));
-    return vfma(q, q, vfma(rz, rz, vfma(ry, ry, vmul(rx, rx))));
-}
-template <typename T>
-__device__ __forceinline__ void acc_add(Acc<T>& a, T p, T tau, const Tgt& t) {
-    a.v[0] = vadd(a.v[0], p);
-    a.v[1] = vfma(p, splat(t.y0, T()), a.v[1]);
-    a.v[2] = vfma(p, splat(t.y1, T()), a.v[2]);
-    a.v[3] = vfma(p, splat(t.y2, T()), a.v[3]);
-    a.v[4] = vfma(p, splat(t.w0, T()), a.v[4]);
-    a.v[5] = vfma(p, splat(t.w1, T()), a.v[5]);
-    a.v[6] = vfma(p, splat(t.w2, T()), a.v[6]);
-    a.v[7] = vfma(p, splat(t.w3, T()), a.v[7]);
-    a.v[8] = vfma(p, splat(t.w4, T()), a.v[8]);
-    a.v[9] = vfma(p, splat(t.w5, T()), a.v[9]);
-    a.v[10] = vfma(p, splat(t.b0, T()), a.v[10]);
-    a.v[11] = vfma(p, splat(t.b1, T()), a.v[11]);
-    a.v[12] = vfma(p, splat(t.b2, T()), a.v[12]);
-    a.v[13] = vfma(p, tau, a.v[13]);
-}
-__device__ __forceinline__ float vex2(float e) { return ex2_approx(e); }
-__device__ __forceinline__ float2 vex2(float2 e) { return make_float2(ex2_approx(e.x), ex2_approx(e.y)); }
-__device__ __forceinline__ float vmaxs(float a, float b) { return fmaxf(a, b); }
-__device__ __forceinline__ float2 vmaxs(float2 a, float2 b) { return make_float2(fmaxf(a.x, b.x), fmaxf(a.y, b.y)); }
-__device__ __forceinline__ float lane_of(float v, int) { return v; }
-__device__ __forceinline__ float lane_of(float2 v, int i) { return i ? v.y : v.x; }
-__device__ __forceinline__ void set_lane(float& v, int, float x) { v = x; }
-__device__ __forceinline__ void set_lane(float2& v, int i, float x) {
-    if (i) v.y = x; else v.x = x;
-}
-
-template <bool kLiteral, typename T>
-__device__ __forceinline__ T log_weight(T tau, const Tgt& t, float k2) {
-    return kLiteral ? vmul(splat(-k2, T()), tau) : vfma(splat(-k2, T()), tau, splat(t.om, T()));
-}
-
-// ---- mbarrier / bulk-copy PTX wrappers --------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// Producer-side wait: the thread is suspended until the phase flips (or the time hint elapses)
-// instead of spinning and stealing issue slots from the consumer warps of its SM sub-partition.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAITS_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-        "@!P1 bra WAITS_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(1000000u)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
 
 // ---- setup: per-call constants (lsgcpd_estep path) ---------------------------------------
 __global__ void estep_setup_kernel(IterState* st, const TargetHeader* hdr, double r0, double r1, double r2,
@@ -1190,67 +1043,12 @@ __global__ void estep_merge_kernel(const float* __restrict__ part, int64_t N, co
     if (!st->active) return;
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= N) return;
-    double wn = st->w, C1n = st->C1, Lon = st->Lo;
-    if (phi) {
-        const double f = fmin(fmax((double)phi[n], 0.0), 1.0);
-        wn = 1.0 - (1.0 - st->w) * f;
-        if (!(wn < 1.0)) {
-            float4* r4 = reinterpret_cast<float4*>(rec + n * LSGCPD_REC);
-            r4[0] = r4[1] = r4[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-            r4[3] = make_float4(0.f, 0.f, (float)(-log(st->volume)), 1.f);
-            return;
-        }
-        C1n = st->C1 + log((1.0 - wn) / (1.0 - st->w));
-        Lon = wn > 0.0 ? (log(wn / st->volume) - C1n) * 1.4426950408889634074 - st->omega_ref : -INFINITY;
-    }
     const int64_t kB = sc.B;
     const int64_t j = n / kB;
-    const int b = (int)(n % kB);
     const int64_t g0 = sched_owner(sc, j * sc.T);
     const int64_t g1 = sched_owner(sc, (j + 1) * sc.T - 1);
-    const int64_t nk = g1 - g0 + 1;
-    // reference max over the segments' maxima (all 0 in the fixed-max mode: no rescaling needed)
-    double mustar = -INFINITY;
-    for (int64_t k = 0; k < nk; ++k) {
-        const float* base = part + (j * sc.kmax + k) * (int64_t)kPartF * kB;
-        mustar = fmax(mustar, (double)base[14 * kB + b]);
-    }
-    if (wn > 0.0) mustar = fmax(mustar, fmin(Lon, 0.0));   // keep the outlier term representable
-    double a[kAcc];
-#pragma unroll
-    for (int f = 0; f < kAcc; ++f) a[f] = 0.0;
-    for (int64_t k = 0; k < nk; ++k) {
-        const float* base = part + (j * sc.kmax + k) * (int64_t)kPartF * kB;
-        const double muk = (double)base[14 * kB + b];
-        const double sc_k = (muk == mustar) ? 1.0 : exp2(muk - mustar);
-#pragma unroll
-        for (int f = 0; f < kAcc; ++f) a[f] = fma(sc_k, (double)base[f * kB + b], a[f]);
-    }
-    const double O = (wn > 0.0) ? exp2(Lon - mustar) : 0.0;
-    const double Z = a[0] + O;
-    const double iz = 1.0 / Z;
-    float* r = rec + n * LSGCPD_REC;
-    float4 o0, o1, o2, o3;
-    o0.x = (float)(a[0] * iz);
-    o0.y = (float)(a[1] * iz);
-    o0.z = (float)(a[2] * iz);
-    o0.w = (float)(a[3] * iz);
-    o1.x = (float)(a[4] * iz);
-    o1.y = (float)(a[5] * iz);
-    o1.z = (float)(a[6] * iz);
-    o1.w = (float)(a[7] * iz);
-    o2.x = (float)(a[8] * iz);
-    o2.y = (float)(a[9] * iz);
-    o2.z = (float)(a[10] * iz);
-    o2.w = (float)(a[11] * iz);
-    o3.x = (float)(a[12] * iz);
-    o3.y = (float)(a[13] * iz / st->sigma2);
-    o3.z = (float)(C1n + 0.69314718055994530942 * (st->omega_ref + mustar + log2(Z)));
-    o3.w = (float)(O * iz);
-    reinterpret_cast<float4*>(r)[0] = o0;
-    reinterpret_cast<float4*>(r)[1] = o1;
-    reinterpret_cast<float4*>(r)[2] = o2;
-    reinterpret_cast<float4*>(r)[3] = o3;
+    merge_point(part + j * sc.kmax * (int64_t)kPartF * kB, g1 - g0 + 1, kB, (int)(n % kB), st,
+                phi ? phi + n : nullptr, rec + n * LSGCPD_REC);
 }
 
 // ---- host-side planning and launch ---------------------------------------------------------

@@ -13,6 +13,34 @@ struct RegParams {
     int newton_max, consistent, max_iters;
 };
 
+// Batched registrations (NEXT-3): one descriptor per problem, in device memory.  Units of all problems
+// are concatenated: problem b owns global units [unit0, unit0 + nblk·T), points [pt0, pt0 + N) of the
+// concatenated record, and partial slots from part0 (floats).
+struct BatchProblem {
+    const void* target;        // prepared target (header + body + tensor-core section)
+    const float* body;         // pair-interleaved body (CUDA-core E step)
+    const float* src;          // [N][3]
+    const float* conf;         // optional φ(x_n) [N] or NULL
+    int64_t M, N, T, nblk, unit0, pt0, part0;
+    double volume, extent, omega_ref, spc;
+    double R0[9], t0[3];
+};
+constexpr int kBatchMom = 80;   // doubles per problem in the moment array (75 moments + N at [75])
+
+// batch.cu
+int batch_block_points();
+size_t batch_partial_floats(int64_t nblk, int64_t kmax);
+void batch_fill_launch(BatchProblem* bp, int B, int consistent, int* err, cudaStream_t stream);
+void estep_batch_launch(const BatchProblem* bp, int B, const Sched& sc, const IterState* st, float* part, float* rec,
+                        int64_t Ntot, int consistent, cudaStream_t stream);
+// mstep.cu (batched)
+void moments_batch_launch(const BatchProblem* bp, int B, const float* rec, IterState* st, double* blockpart,
+                          double* mom, unsigned* counters, cudaStream_t stream);
+void newton_batch_launch(const BatchProblem* bp, int B, IterState* st, const double* mom, const RegParams& rp0,
+                         double* nll_trace, double* sigma2_trace, int* iters_done, cudaStream_t stream);
+void init_batch_launch(const BatchProblem* bp, int B, IterState* st, const RegParams& rp0, double sigma2_user,
+                       double* mom, double* sigma2_trace, cudaStream_t stream);
+
 // estep.cu
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc);
 size_t estep_partial_bytes(const Sched& s);

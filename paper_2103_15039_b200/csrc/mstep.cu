@@ -27,10 +27,10 @@ __device__ __forceinline__ int s4(int a, int b) {  // symmetric 4×4 index
     return a == 0 ? b : (a == 1 ? 3 + b : (a == 2 ? 5 + b : 9));
 }
 
-// K3: per-point moments from the E-step record.
-__global__ void __launch_bounds__(kMomThreads)
-    moments_kernel(const float* __restrict__ rec, const float* __restrict__ src, int64_t N,
-                   const IterState* __restrict__ st, double* blockpart, double* out, unsigned int* counter) {
+// K3: per-point moments from the E-step record (grid-stride over `nblocks` CTAs starting at this one).
+__device__ __forceinline__ void moments_body(const float* __restrict__ rec, const float* __restrict__ src, int64_t N,
+                                             const IterState* __restrict__ st, double* blockpart, double* out,
+                                             unsigned int* counter, int single) {
     if (!st->active) return;
     double R[9], t[3];
 #pragma unroll
@@ -41,8 +41,9 @@ __global__ void __launch_bounds__(kMomThreads)
     double m[kMom];
 #pragma unroll
     for (int f = 0; f < kMom; ++f) m[f] = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < N; n += stride) {
+    const int64_t stride = single ? (int64_t)blockDim.x : (int64_t)gridDim.x * blockDim.x;
+    const int64_t first = single ? (int64_t)threadIdx.x : (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t n = first; n < N; n += stride) {
         const float4* r4 = reinterpret_cast<const float4*>(rec + n * LSGCPD_REC);
         const float4 a0 = r4[0], a1 = r4[1], a2 = r4[2], a3 = r4[3];
         const double P = a0.x;
@@ -76,7 +77,15 @@ __global__ void __launch_bounds__(kMomThreads)
         m[73] += P;
         m[74] += (double)a3.z;
     }
-    block_reduce_store<kMom, 0, kMomThreads>(m, blockpart, out, counter);
+    if (single)
+        block_reduce_single<kMom, kMomThreads>(m, out);
+    else
+        block_reduce_store<kMom, 0, kMomThreads>(m, blockpart, out, counter);
+}
+__global__ void __launch_bounds__(kMomThreads)
+    moments_kernel(const float* __restrict__ rec, const float* __restrict__ src, int64_t N,
+                   const IterState* __restrict__ st, double* blockpart, double* out, unsigned int* counter) {
+    moments_body(rec, src, N, st, blockpart, out, counter, 0);
 }
 
 // σ²₀ partial sums: [Σ_n ||x̂_n - ȳ||², N_local]  (x̂ at the initial pose in st).
@@ -236,8 +245,8 @@ __device__ inline bool chol_solve6(const double* A, double mu, const double* b, 
 
 // One warp: the dense algebra (v = U + 𝔾Δθ, J, 𝔾J, ∇, H) is spread over the lanes; the damping loop
 // (Cholesky 6×6, exp, candidate q) runs on lane 0.  All lanes end with identical state.
-__global__ void __launch_bounds__(32) newton_kernel(IterState* st, const double* __restrict__ mom, RegParams rp,
-                                                    double* nll_trace, double* sigma2_trace, int* iters_done) {
+__device__ __noinline__ void newton_body(IterState* st, const double* __restrict__ mom, const RegParams& rp,
+                                         double* nll_trace, double* sigma2_trace, int* iters_done) {
     __shared__ Mom mo;
     __shared__ double S[21][16];
     __shared__ double J[6][12], GJ[6][12], v[12], Bm[16], H[36], grad[6];
@@ -404,6 +413,91 @@ __global__ void __launch_bounds__(32) newton_kernel(IterState* st, const double*
     sigma2_trace[k + 1] = s2;
     *iters_done = k + 1;
     *st = nx;
+}
+
+__global__ void __launch_bounds__(32) newton_kernel(IterState* st, const double* __restrict__ mom, RegParams rp,
+                                                    double* nll_trace, double* sigma2_trace, int* iters_done) {
+    newton_body(st, mom, rp, nll_trace, sigma2_trace, iters_done);
+}
+
+// ---- batched registrations (NEXT-3): one CTA / warp per problem -----------------------------------------
+// Moments of problem b over its own points (one CTA, fixed order: deterministic), written to mom[b·kBatchMom].
+__global__ void __launch_bounds__(kMomThreads)
+    moments_batch_kernel(const BatchProblem* __restrict__ bp, const float* __restrict__ rec, IterState* st,
+                         double* blockpart, double* mom, unsigned* counters) {
+    const int b = blockIdx.x;
+    const BatchProblem P = bp[b];
+    moments_body(rec + P.pt0 * LSGCPD_REC, P.src, P.N, st + b, blockpart + (int64_t)b * kMom,
+                 mom + (int64_t)b * kBatchMom, counters + b, 1);
+}
+
+__global__ void __launch_bounds__(32) newton_batch_kernel(const BatchProblem* __restrict__ bp, IterState* st,
+                                                          const double* __restrict__ mom, RegParams rp0,
+                                                          double* nll_trace, double* sigma2_trace, int* iters_done) {
+    const int b = blockIdx.x;
+    const BatchProblem P = bp[b];
+    RegParams rp = rp0;
+    rp.V = P.volume;
+    rp.floor = rp0.floor * P.extent * P.extent;   // rp0.floor holds the relative floor
+    rp.omega_ref_target = P.omega_ref;
+    rp.spc = P.spc;
+    rp.M = P.M;
+    newton_body(st + b, mom + (int64_t)b * kBatchMom, rp, nll_trace + (int64_t)b * (rp.max_iters + 1),
+                sigma2_trace + (int64_t)b * (rp.max_iters + 2), iters_done + b);
+}
+
+// σ²₀ of problem b (CPD closed form) and its iteration-0 state, one CTA per problem.
+__global__ void __launch_bounds__(kMomThreads)
+    init_batch_kernel(const BatchProblem* __restrict__ bp, IterState* st, RegParams rp0, double sigma2_user,
+                      double* mom, double* sigma2_trace) {
+    const int b = blockIdx.x;
+    const BatchProblem P = bp[b];
+    __shared__ double red[kMomThreads / 32];
+    const TargetHeader* hdr = reinterpret_cast<const TargetHeader*>(P.target);
+    double acc = 0.0;
+    for (int64_t n = threadIdx.x; n < P.N; n += blockDim.x) {
+        const double x0 = P.src[3 * n], x1 = P.src[3 * n + 1], x2 = P.src[3 * n + 2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double d = fma(P.R0[3 * i], x0, fma(P.R0[3 * i + 1], x1, fma(P.R0[3 * i + 2], x2, P.t0[i]))) -
+                             hdr->ybar[i];
+            acc = fma(d, d, acc);
+        }
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double sx = 0.0;
+    for (int w = 0; w < kMomThreads / 32; ++w) sx += red[w];
+    const double M = (double)P.M, N = (double)P.N;
+    double s2 = sigma2_user > 0.0 ? sigma2_user : (M * sx + N * hdr->syy) / (3.0 * M * N);
+    const double floor = rp0.floor * P.extent * P.extent;
+    if (s2 < floor) s2 = floor;
+    IterState s;
+    make_state(s, P.R0, P.t0, s2, rp0.w, P.volume, P.M, P.omega_ref, rp0.consistent, rp0.eta, P.spc);
+    s.extent = P.extent;
+    s.active = rp0.max_iters > 0 ? 1 : 0;
+    s.iter = 0;
+    s.status = 0;
+    s.no_mass = 0;
+    s.last_step_rot = s.last_step_trans = 0.0;
+    st[b] = s;
+    mom[(int64_t)b * kBatchMom + 75] = N;
+    sigma2_trace[(int64_t)b * (rp0.max_iters + 2)] = s2;
+}
+
+void moments_batch_launch(const BatchProblem* bp, int B, const float* rec, IterState* st, double* blockpart,
+                          double* mom, unsigned* counters, cudaStream_t stream) {
+    moments_batch_kernel<<<B, kMomThreads, 0, stream>>>(bp, rec, st, blockpart, mom, counters);
+}
+void newton_batch_launch(const BatchProblem* bp, int B, IterState* st, const double* mom, const RegParams& rp0,
+                         double* nll_trace, double* sigma2_trace, int* iters_done, cudaStream_t stream) {
+    newton_batch_kernel<<<B, 32, 0, stream>>>(bp, st, mom, rp0, nll_trace, sigma2_trace, iters_done);
+}
+void init_batch_launch(const BatchProblem* bp, int B, IterState* st, const RegParams& rp0, double sigma2_user,
+                       double* mom, double* sigma2_trace, cudaStream_t stream) {
+    init_batch_kernel<<<B, kMomThreads, 0, stream>>>(bp, st, rp0, sigma2_user, mom, sigma2_trace);
 }
 
 // ---- host launchers ----------------------------------------------------------------------------

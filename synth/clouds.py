@@ -392,6 +392,50 @@ def make_scale(n: int = 524288) -> Workload:
                      "rot_deg": 60.0, "t_norm": 0.3})
 
 
+def sample_desk_scene(rng: np.random.Generator, n: int, radius: float, center) -> np.ndarray:
+    """Plane [-0.5,0.5]² at z = 0 plus the upper hemisphere of `radius` at `center` (on the plane), area-
+    proportional (SPEC S:630's desk-scale plane + hemisphere)."""
+    a_plane, a_hemi = 1.0, 2.0 * np.pi * radius * radius
+    k = rng.binomial(n, a_hemi / (a_plane + a_hemi))
+    P = np.empty((n, 3))
+    P[: n - k, 0:2] = rng.uniform(-0.5, 0.5, (n - k, 2))
+    P[: n - k, 2] = 0.0
+    d = rng.standard_normal((k, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    d[:, 2] = np.abs(d[:, 2])
+    P[n - k:] = np.asarray(center) + radius * d
+    return P
+
+
+BATCH_SEED = 6
+
+
+def make_batch(B: int = 550, n: int = 3500, seed: int = BATCH_SEED, ragged: bool = False):
+    """Many small registration problems (the paper's problem size: 3.5k-5k points,
+    P:359-360): problem b is a desk scene (plane + hemisphere of radius U(0.2, 0.35) at a
+    random spot) with noise sd 0.005, an independent resample for the source, rotated 50° about a random
+    axis (the §4.1 protocol) and translated by 0.1·random unit vector; w = 0.1, 50 EM iterations.
+    ragged: sizes vary per problem (n/2 .. 3n/2).  Returns a list of Workloads."""
+    out = []
+    ss = np.random.SeedSequence(seed).spawn(B)
+    for b in range(B):
+        r_lay, r_t, r_s, r_noise, r_axis, r_dir, r_n = [np.random.Generator(np.random.PCG64(s)) for s in ss[b].spawn(7)]
+        rad = r_lay.uniform(0.2, 0.35)
+        c = np.array([r_lay.uniform(-0.15, 0.15), r_lay.uniform(-0.15, 0.15), 0.0])
+        nm = int(r_n.integers(n // 2, 3 * n // 2 + 1)) if ragged else n
+        ns = int(r_n.integers(n // 2, 3 * n // 2 + 1)) if ragged else n
+        Y = sample_desk_scene(r_t, nm, rad, c) + r_noise.standard_normal((nm, 3)) * 0.005
+        Xs = sample_desk_scene(r_s, ns, rad, c) + r_noise.standard_normal((ns, 3)) * 0.005
+        R_gt = axis_angle(_unit(r_axis), np.deg2rad(50.0))
+        t_gt = 0.1 * _unit(r_dir)
+        X = _apply(R_gt, t_gt, Xs)
+        R_e, t_e = _inverse(R_gt, t_gt)
+        out.append(Workload(f"batch{b}", _f32(Y), _f32(X), R_e, t_e, 0.1, 50, 10, np.ones(nm, bool),
+                            np.ones(ns, bool), {"seed": seed, "index": b, "radius": rad, "rot_deg": 50.0,
+                                                "t_norm": 0.1, "noise_sd": 0.005}))
+    return out
+
+
 def make(name: str) -> Workload:
     if name == "tiny":
         return make_tiny()

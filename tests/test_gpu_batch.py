@@ -1,0 +1,70 @@
+"""Batched registrations: lsgcpd_register_batch runs many small problems through one
+batched E step per EM iteration.  Each problem's result must meet the north-star registration bar against
+the FP64 oracle run on that problem alone (R within 1e-4 rad, t within 1e-4·extent), whatever else is in
+the batch; a problem that loses its mass reports ENOMASS without disturbing the others."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import outlier as ol, se3
+from tests.gpu_common import to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def _prep(wl):
+    import paper_2103_15039_b200 as lsg
+    tgt, ann = lsg.prepare_target(to_dev(wl.target), wl.knn_k, annotations=True)
+    t64 = {"Y": wl.target.astype(np.float64), "normals": ann["normals"].cpu().numpy().astype(np.float64),
+           "alpha": ann["alpha"].cpu().numpy().astype(np.float64)}
+    return tgt, t64
+
+
+def _close(R, t, Rr, tr, ext, tol=1e-4):
+    ang = se3.rotation_angle(np.asarray(R).T @ np.asarray(Rr))
+    assert ang <= tol and np.linalg.norm(np.asarray(t) - np.asarray(tr)) <= tol * ext, (ang, t, tr)
+
+
+def test_batch_matches_the_oracle_per_problem():
+    import paper_2103_15039_b200 as lsg
+    wls = synth.make_batch(7, 700, ragged=True)
+    preps = [_prep(w) for w in wls]
+    iters = 30
+    out = lsg.register_batch([p[0] for p in preps], [to_dev(w.source) for w in wls], iters, w=0.1)
+    assert np.all(out["iters"] == iters) and np.all(out["status"] == 0)
+    for b, (w, (tgt, t64)) in enumerate(zip(wls, preps)):
+        ora = oracle.register(t64, w.source, 0.1, iters, tgt.volume, tgt.extent)
+        _close(out["R"][b], out["t"][b], ora["R"], ora["t"], tgt.extent)
+        assert out["sigma2"][b] == pytest.approx(ora["sigma2"], rel=1e-3)
+        single = lsg.register(tgt, to_dev(w.source), iters, w=0.1)
+        _close(out["R"][b], out["t"][b], single["R"], single["t"], tgt.extent, tol=1e-5)
+
+
+def test_batch_isolates_a_failing_problem_and_supports_eta_and_confidence():
+    import paper_2103_15039_b200 as lsg
+    wls = synth.make_batch(4, 600, seed=11)
+    preps = [_prep(w) for w in wls]
+    srcs = [w.source for w in wls]
+    srcs[2] = (srcs[2] + 1e4).astype(np.float32)                     # far away: no inlier mass
+    rng = np.random.default_rng(4)
+    confs = [rng.uniform(0.3, 1.0, w.N).astype(np.float32) for w in wls]
+    out = lsg.register_batch([p[0] for p in preps], [to_dev(s) for s in srcs], 20,
+                             src_confs=[to_dev(c) for c in confs], eta=0.1, sigma2_init=1e-3)
+    assert out["status"][2] == -5 and out["iters"][2] == 3
+    for b in (0, 1, 3):
+        tgt, t64 = preps[b]
+        ora = oracle.register(t64, srcs[b], 0.0, 20, tgt.volume, tgt.extent, sigma2_0=1e-3, eta=0.1,
+                              phi_x=confs[b].astype(np.float64))
+        assert out["status"][b] == 0 and out["iters"][b] == 20
+        _close(out["R"][b], out["t"][b], ora["R"], ora["t"], tgt.extent)
+
+
+def test_batch_invalid_arguments():
+    import paper_2103_15039_b200 as lsg
+    wls = synth.make_batch(2, 300, seed=12)
+    tgts = [_prep(w)[0] for w in wls]
+    with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
+        lsg.register_batch(tgts, [to_dev(w.source) for w in wls], 5, w=1.0)
+    with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
+        lsg.register_batch(tgts, [to_dev(w.source) for w in wls], 5, R0s=[2 * np.eye(3)] * 2)

@@ -392,18 +392,29 @@ def make_scale(n: int = 524288) -> Workload:
                      "rot_deg": 60.0, "t_norm": 0.3})
 
 
-def sample_desk_scene(rng: np.random.Generator, n: int, radius: float, center) -> np.ndarray:
-    """Plane [-0.5,0.5]² at z = 0 plus the upper hemisphere of `radius` at `center` (on the plane), area-
-    proportional (SPEC S:630's desk-scale plane + hemisphere)."""
-    a_plane, a_hemi = 1.0, 2.0 * np.pi * radius * radius
-    k = rng.binomial(n, a_hemi / (a_plane + a_hemi))
+def sample_desk_scene(rng: np.random.Generator, n: int, radii, centers) -> np.ndarray:
+    """Desk corner: floor [-0.5,0.5]² at z = 0, walls x = -0.5 and y = -0.5 of height 0.5, plus upper
+    hemispheres of `radii` at `centers` (on the floor), area-proportional (SPEC S:630's desk-scale plane +
+    hemisphere, with walls and a second hemisphere so that no rotation maps the scene onto itself)."""
+    areas = np.array([1.0, 0.5, 0.5] + [2.0 * np.pi * r * r for r in radii])
+    counts = rng.multinomial(n, areas / areas.sum())
     P = np.empty((n, 3))
-    P[: n - k, 0:2] = rng.uniform(-0.5, 0.5, (n - k, 2))
-    P[: n - k, 2] = 0.0
-    d = rng.standard_normal((k, 3))
-    d /= np.linalg.norm(d, axis=1, keepdims=True)
-    d[:, 2] = np.abs(d[:, 2])
-    P[n - k:] = np.asarray(center) + radius * d
+    k0, k1, k2 = counts[:3]
+    P[:k0, 0:2] = rng.uniform(-0.5, 0.5, (k0, 2))                     # floor z = 0
+    P[:k0, 2] = 0.0
+    P[k0:k0 + k1, 0] = -0.5                                            # wall x = -0.5, height 0.5
+    P[k0:k0 + k1, 1] = rng.uniform(-0.5, 0.5, k1)
+    P[k0:k0 + k1, 2] = rng.uniform(0.0, 0.5, k1)
+    P[k0 + k1:k0 + k1 + k2, 1] = -0.5                                  # wall y = -0.5
+    P[k0 + k1:k0 + k1 + k2, 0] = rng.uniform(-0.5, 0.5, k2)
+    P[k0 + k1:k0 + k1 + k2, 2] = rng.uniform(0.0, 0.5, k2)
+    o = k0 + k1 + k2
+    for r, c, k in zip(radii, centers, counts[3:]):
+        d = rng.standard_normal((k, 3))
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        d[:, 2] = np.abs(d[:, 2])
+        P[o:o + k] = np.asarray(c) + r * d
+        o += k
     return P
 
 
@@ -420,8 +431,9 @@ def make_batch(B: int = 550, n: int = 3500, seed: int = BATCH_SEED, ragged: bool
     ss = np.random.SeedSequence(seed).spawn(B)
     for b in range(B):
         r_lay, r_t, r_s, r_noise, r_axis, r_dir, r_n = [np.random.Generator(np.random.PCG64(s)) for s in ss[b].spawn(7)]
-        rad = r_lay.uniform(0.2, 0.35)
-        c = np.array([r_lay.uniform(-0.15, 0.15), r_lay.uniform(-0.15, 0.15), 0.0])
+        rad = [r_lay.uniform(0.15, 0.25), r_lay.uniform(0.06, 0.1)]
+        ang = r_lay.uniform(0, 2 * np.pi)
+        c = [np.array([0.2 * np.cos(ang), 0.2 * np.sin(ang), 0.0]), np.array([-0.3 * np.cos(ang), -0.3 * np.sin(ang), 0.0])]
         nm = int(r_n.integers(n // 2, 3 * n // 2 + 1)) if ragged else n
         ns = int(r_n.integers(n // 2, 3 * n // 2 + 1)) if ragged else n
         Y = sample_desk_scene(r_t, nm, rad, c) + r_noise.standard_normal((nm, 3)) * 0.005
@@ -431,7 +443,7 @@ def make_batch(B: int = 550, n: int = 3500, seed: int = BATCH_SEED, ragged: bool
         X = _apply(R_gt, t_gt, Xs)
         R_e, t_e = _inverse(R_gt, t_gt)
         out.append(Workload(f"batch{b}", _f32(Y), _f32(X), R_e, t_e, 0.1, 50, 10, np.ones(nm, bool),
-                            np.ones(ns, bool), {"seed": seed, "index": b, "radius": rad, "rot_deg": 50.0,
+                            np.ones(ns, bool), {"seed": seed, "index": b, "radii": rad, "rot_deg": 50.0,
                                                 "t_norm": 0.1, "noise_sd": 0.005}))
     return out
 

@@ -15,4 +15,4 @@ from .model import (knn, alpha_from_kappa, local_surface, prepare_target, workin
                     sigma2_init, sum_sq_pairs, mean_nn_spacing)
 from .mstep import PointStats, newton, mstep, grad_hess_literal  # noqa: F401
 from .em import register, register_workload  # noqa: F401
-from . import se3, matrix_form, outlier  # noqa: F401
+from . import se3, matrix_form, outlier, affine  # noqa: F401

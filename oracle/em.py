@@ -21,7 +21,7 @@ from .outlier import outlier_weight_max, point_outlier_weights
 
 def register(target: dict, X, w: float, iters: int, V: float, extent: float, R0=None, t0=None,
              sigma2_0=None, consistent: bool = True, newton_max: int = 10, sigma2_floor_rel: float = 1e-12,
-             nthreads: int = 0, keep_records: bool = False, eta=None, prior=None, phi_x=None):
+             nthreads: int = 0, keep_records: bool = False, eta=None, prior=None, phi_x=None, group: str = "se3"):
     Y, normals, alpha = target["Y"], target["normals"], target["alpha"]
     general = eta is not None or prior is not None or phi_x is not None
     M = Y.shape[0]
@@ -49,7 +49,7 @@ def register(target: dict, X, w: float, iters: int, V: float, extent: float, R0=
         trace["nll"].append(float(-rec[:, 14].sum()))
         if keep_records:
             trace["records"].append(rec)
-        R, t, s2, info = mstep(X, rec, R, t, s2, extent, newton_max, floor)
+        R, t, s2, info = mstep(X, rec, R, t, s2, extent, newton_max, floor, group)
         trace["m_time"] += time.perf_counter() - t1_
         trace["e_time"] += t1_ - t0_
         trace["sigma2"].append(s2)

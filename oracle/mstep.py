@@ -115,10 +115,16 @@ def newton(stats: PointStats, extent: float, newton_max: int = 10):
     return R, t, q_cur, info
 
 
-def mstep(X, rec, R_E, t_E, sigma2: float, extent: float, newton_max: int = 10, sigma2_floor: float = 0.0):
-    """One M step: pose by damped Newton, then σ² at the new pose."""
+def mstep(X, rec, R_E, t_E, sigma2: float, extent: float, newton_max: int = 10, sigma2_floor: float = 0.0,
+          group: str = "se3"):
+    """One M step: transform by damped Newton on the group (SE(3), or GA⁺(3) for group="affine"),
+    then σ² at the new transform."""
     stats = PointStats(X, rec, R_E, t_E, sigma2)
-    R, t, q_rel, info = newton(stats, extent, newton_max)
+    if group == "affine":
+        from .affine import newton as newton_affine
+        R, t, q_rel, info = newton_affine(stats, extent, newton_max)
+    else:
+        R, t, q_rel, info = newton(stats, extent, newton_max)
     sumP = float(stats.P.sum())
     if sumP > 0.0:
         s2 = (float(stats.sig2D.sum()) + q_rel) / (3.0 * sumP)

@@ -89,6 +89,9 @@ typedef struct {
                                /* R22); w is then ignored.  < 0: use w.                            */
     const float* d_src_conf;   /* DEVICE [N] source confidences φ(x_n) ∈ [0,1] (Eq. 8):  */
                                /* w_n = 1 - (1 - w0) φ(x_n); NULL: w_n = w0 for every point          */
+    int group;                 /* transformation group of the M step: 0 = SE(3) rigid   */
+                               /* (default); 1 = affine GA⁺(3), basis e_i e_jᵀ (9) + translations   */
+                               /* (3), reading R24.  With 1, "R" is the linear part A (det A > 0).   */
 } lsgcpd_em_params;
 
 /* Library identity. */

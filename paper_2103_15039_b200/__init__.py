@@ -51,7 +51,7 @@ class EmParams(ctypes.Structure):
     _fields_ = [("w", ctypes.c_double), ("max_iters", ctypes.c_int), ("newton_max", ctypes.c_int),
                 ("consistent_normalizer", ctypes.c_int), ("sigma2_init", ctypes.c_double),
                 ("sigma2_floor_rel", ctypes.c_double), ("tol", ctypes.c_double), ("eta", ctypes.c_double),
-                ("d_src_conf", ctypes.c_void_p)]
+                ("d_src_conf", ctypes.c_void_p), ("group", ctypes.c_int)]
 
 
 class Problem(ctypes.Structure):
@@ -223,11 +223,11 @@ class EstepRunner:
         self.rec = out if out is not None else torch.empty((self.N, REC), dtype=torch.float32, device=src.device)
 
     def __call__(self, R, t, sigma2: float, w: float, volume: Optional[float] = None, consistent: bool = True,
-                 stream=None, eta: Optional[float] = None, src_conf=None):
+                 stream=None, eta: Optional[float] = None, src_conf=None, group: str = "se3"):
         Ra, Rp = _darr(R, 9)
         ta, tp = _darr(t, 3)
         V = self.target.volume if volume is None else float(volume)
-        if eta is None and src_conf is None:
+        if eta is None and src_conf is None and _group(group) == 0:
             _check(lib().lsgcpd_estep(self.target.buf.data_ptr(), self.target.M, self.src.data_ptr(), self.N, Rp, tp,
                                       float(sigma2), float(w), V, int(bool(consistent)), self.rec.data_ptr(),
                                       self.ws.data_ptr(), self.ws.numel(), _stream_ptr(stream)))
@@ -238,6 +238,7 @@ class EstepRunner:
             p.consistent_normalizer = int(bool(consistent))
             p.eta = -1.0 if eta is None else float(eta)
             p.d_src_conf = _conf_ptr(src_conf, self.N)
+            p.group = _group(group)
             _check(lib().lsgcpd_estep_ex(self.target.buf.data_ptr(), self.target.M, self.src.data_ptr(), self.N, Rp, tp,
                                          float(sigma2), ctypes.byref(p), V, self.rec.data_ptr(), self.ws.data_ptr(),
                                          self.ws.numel(), _stream_ptr(stream)))
@@ -245,9 +246,18 @@ class EstepRunner:
 
 
 def estep(target: Target, src, R, t, sigma2: float, w: float, volume: Optional[float] = None,
-          consistent: bool = True, stream=None, eta: Optional[float] = None, src_conf=None):
-    """lsgcpd_estep (or lsgcpd_estep_ex with eta / src_conf) → [N,16] float32 CUDA record tensor."""
-    return EstepRunner(target, src)(R, t, sigma2, w, volume, consistent, stream, eta, src_conf)
+          consistent: bool = True, stream=None, eta: Optional[float] = None, src_conf=None, group: str = "se3"):
+    """lsgcpd_estep (or lsgcpd_estep_ex with eta / src_conf / group) → [N,16] float32 CUDA record tensor."""
+    return EstepRunner(target, src)(R, t, sigma2, w, volume, consistent, stream, eta, src_conf, group)
+
+
+def _group(group) -> int:
+    """Transformation group of the M step: "se3" (rigid, default) or "affine"."""
+    if group in ("se3", 0, None):
+        return 0
+    if group in ("affine", 1):
+        return 1
+    raise ValueError(f"unknown group {group!r}")
 
 
 def _conf_ptr(conf, n):
@@ -334,9 +344,9 @@ class Registrar:
     def __call__(self, w: float = 0.1, newton_max: int = 10, consistent: bool = True, sigma2_init: float = 0.0,
                  sigma2_floor_rel: float = 1e-12, tol: float = 0.0, R0=None, t0=None, volume: float = 0.0,
                  comm: Optional[Comm] = None, traces: bool = False, stream=None, check: bool = True,
-                 eta: Optional[float] = None, src_conf=None):
+                 eta: Optional[float] = None, src_conf=None, group: str = "se3"):
         p = EmParams(w, self.max_iters, newton_max, int(bool(consistent)), sigma2_init, sigma2_floor_rel, tol,
-                     -1.0 if eta is None else float(eta), _conf_ptr(src_conf, self.N))
+                     -1.0 if eta is None else float(eta), _conf_ptr(src_conf, self.N), _group(group))
         R0a, R0p = _darr(np.eye(3) if R0 is None else R0, 9)
         t0a, t0p = _darr(np.zeros(3) if t0 is None else t0, 3)
         Ro = np.zeros(9)
@@ -400,9 +410,10 @@ class BatchRegistrar:
         self.ws = _alloc_bytes(nbytes, self.sources[0].device)
 
     def __call__(self, w: float = 0.1, newton_max: int = 10, consistent: bool = True, sigma2_init: float = 0.0,
-                 sigma2_floor_rel: float = 1e-12, tol: float = 0.0, eta: Optional[float] = None, stream=None):
+                 sigma2_floor_rel: float = 1e-12, tol: float = 0.0, eta: Optional[float] = None, stream=None,
+                 group: str = "se3"):
         p = EmParams(w, self.max_iters, newton_max, int(bool(consistent)), sigma2_init, sigma2_floor_rel, tol,
-                     -1.0 if eta is None else float(eta), None)
+                     -1.0 if eta is None else float(eta), None, _group(group))
         B = self.B
         R = np.zeros((B, 9))
         t = np.zeros((B, 3))

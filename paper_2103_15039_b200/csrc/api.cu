@@ -46,6 +46,15 @@ static bool is_rotation(const double* R) {
     return det > 0.0;
 }
 
+// affine group: a finite linear part with positive determinant (GA⁺(3))
+static bool is_affine_linear(const double* A) {
+    if (!finite_vec(A, 9)) return false;
+    const double det = A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+                       A[2] * (A[3] * A[7] - A[4] * A[6]);
+    return det > 0.0;
+}
+static bool pose_ok(const double* R, int group) { return group ? is_affine_linear(R) : is_rotation(R); }
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -193,6 +202,7 @@ LSG_EXPORT void lsgcpd_em_params_default(lsgcpd_em_params* p) {
     p->tol = 0.0;
     p->eta = -1.0;
     p->d_src_conf = nullptr;
+    p->group = 0;
 }
 
 LSG_EXPORT size_t lsgcpd_target_bytes(int64_t M) {
@@ -258,7 +268,8 @@ LSG_EXPORT size_t lsgcpd_estep_workspace_bytes(int64_t M, int64_t N) {
 
 static int estep_impl(const void* d_target, int64_t M, const float* d_src, int64_t N, const double R[9],
                       const double t[3], double sigma2, double w, double eta, const float* phi, double volume,
-                      int consistent_normalizer, float* d_record, void* d_ws, size_t ws_bytes, cudaStream_t s);
+                      int consistent_normalizer, float* d_record, void* d_ws, size_t ws_bytes, cudaStream_t s,
+                      int group = 0);
 
 LSG_EXPORT int lsgcpd_estep(const void* d_target, int64_t M, const float* d_src, int64_t N, const double R[9],
                             const double t[3], double sigma2, double w, double volume, int consistent_normalizer,
@@ -272,14 +283,16 @@ LSG_EXPORT int lsgcpd_estep_ex(const void* d_target, int64_t M, const float* d_s
                                float* d_record, void* d_ws, size_t ws_bytes, lsgcpd_stream_t stream) {
     LSG_CHECK(params, LSGCPD_EINVAL, "null params");
     LSG_CHECK(!(params->eta >= 1.0) && !isnan(params->eta), LSGCPD_EINVAL, "eta must be < 1 (negative: off)");
+    LSG_CHECK(params->group == 0 || params->group == 1, LSGCPD_EINVAL, "group must be 0 (SE(3)) or 1 (affine)");
     return estep_impl(d_target, M, d_src, N, R, t, sigma2, params->eta >= 0.0 ? 0.0 : params->w, params->eta,
                       params->d_src_conf, volume, params->consistent_normalizer, d_record, d_ws, ws_bytes,
-                      (cudaStream_t)stream);
+                      (cudaStream_t)stream, params->group);
 }
 
 static int estep_impl(const void* d_target, int64_t M, const float* d_src, int64_t N, const double R[9],
                       const double t[3], double sigma2, double w, double eta, const float* phi, double volume,
-                      int consistent_normalizer, float* d_record, void* d_ws, size_t ws_bytes, cudaStream_t s) {
+                      int consistent_normalizer, float* d_record, void* d_ws, size_t ws_bytes, cudaStream_t s,
+                      int group) {
     LSG_CHECK(d_target && d_src && d_record && d_ws && R && t, LSGCPD_EINVAL, "null pointer argument");
     LSG_CHECK(aligned16(d_target) && aligned16(d_record) && aligned16(d_ws), LSGCPD_EINVAL,
               "d_target, d_record and d_ws must be 16-byte aligned");
@@ -288,7 +301,8 @@ static int estep_impl(const void* d_target, int64_t M, const float* d_src, int64
     LSG_CHECK(isfinite(sigma2) && sigma2 > 0.0, LSGCPD_EINVAL, "sigma2 must be finite and > 0");
     LSG_CHECK(isfinite(w) && w >= 0.0 && w < 1.0, LSGCPD_EINVAL, "w must be in [0, 1)");
     LSG_CHECK(isfinite(volume) && volume > 0.0, LSGCPD_EINVAL, "volume must be finite and > 0");
-    LSG_CHECK(is_rotation(R), LSGCPD_EINVAL, "R is not a rotation matrix (to 1e-6)");
+    LSG_CHECK(pose_ok(R, group), LSGCPD_EINVAL,
+              group ? "A must be finite with det A > 0" : "R is not a rotation matrix (to 1e-6)");
     LSG_CHECK(finite_vec(t, 3), LSGCPD_EINVAL, "t must be finite");
     EstepLayout L;
     Sched sc;
@@ -380,7 +394,9 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     double Rid[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, tid[3] = {0, 0, 0};
     const double* R = R0 ? R0 : Rid;
     const double* t = t0 ? t0 : tid;
-    LSG_CHECK(is_rotation(R), LSGCPD_EINVAL, "R0 is not a rotation matrix (to 1e-6)");
+    LSG_CHECK(p.group == 0 || p.group == 1, LSGCPD_EINVAL, "group must be 0 (SE(3)) or 1 (affine)");
+    LSG_CHECK(pose_ok(R, p.group), LSGCPD_EINVAL,
+              p.group ? "A0 must be finite with det A0 > 0" : "R0 is not a rotation matrix (to 1e-6)");
     LSG_CHECK(finite_vec(t, 3), LSGCPD_EINVAL, "t0 must be finite");
     cudaStream_t s = (cudaStream_t)stream;
     TargetHeader h;
@@ -417,6 +433,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     rp.newton_max = p.newton_max;
     rp.consistent = p.consistent_normalizer ? 1 : 0;
     rp.max_iters = p.max_iters;
+    rp.group = p.group;
 
     LSG_CUDA(cudaMemsetAsync(ws + L.counters, 0, sizeof(unsigned) * 8, s));
     LSG_CUDA(cudaMemsetAsync(ws + L.iters, 0, sizeof(int) * 4, s));
@@ -548,7 +565,8 @@ struct BatchLayout {
     Sched sc;
 };
 
-static int batch_layout(const lsgcpd_problem* P, int B, int max_iters, BatchLayout* L, std::vector<BatchProblem>* out) {
+static int batch_layout(const lsgcpd_problem* P, int B, int max_iters, BatchLayout* L, std::vector<BatchProblem>* out,
+                        int group = 0) {
     LSG_CHECK(P && B >= 1 && B <= (1 << 20), LSGCPD_EINVAL, "bad problem list (B=%d)", B);
     LSG_CHECK(max_iters >= 0 && max_iters <= 100000, LSGCPD_EINVAL, "max_iters out of range");
     const int64_t kB = batch_block_points();
@@ -560,7 +578,7 @@ static int batch_layout(const lsgcpd_problem* P, int B, int max_iters, BatchLayo
         LSG_CHECK(aligned16(p.d_target), LSGCPD_EINVAL, "problem %d: d_target must be 16-byte aligned", b);
         LSG_CHECK(p.M >= 1 && p.N >= 1 && p.M < (int64_t)1 << 30 && p.N < (int64_t)1 << 30, LSGCPD_EINVAL,
                   "problem %d: M=%lld N=%lld out of range", b, (long long)p.M, (long long)p.N);
-        LSG_CHECK(is_rotation(p.R0) && finite_vec(p.t0, 3), LSGCPD_EINVAL, "problem %d: bad initial pose", b);
+        LSG_CHECK(pose_ok(p.R0, group) && finite_vec(p.t0, 3), LSGCPD_EINVAL, "problem %d: bad initial pose", b);
         LSG_CHECK(isfinite(p.volume), LSGCPD_EINVAL, "problem %d: volume must be finite", b);
         BatchProblem& q = bp[b];
         memset(&q, 0, sizeof(q));
@@ -646,9 +664,10 @@ LSG_EXPORT int lsgcpd_register_batch(const lsgcpd_problem* h_problems, int B, co
     LSG_CHECK(p.newton_max >= 0 && p.newton_max <= 1000, LSGCPD_EINVAL, "newton_max out of range");
     LSG_CHECK(isfinite(p.sigma2_floor_rel) && p.sigma2_floor_rel >= 0.0, LSGCPD_EINVAL, "bad sigma2_floor_rel");
     LSG_CHECK(isfinite(p.sigma2_init) && isfinite(p.tol), LSGCPD_EINVAL, "sigma2_init and tol must be finite");
+    LSG_CHECK(p.group == 0 || p.group == 1, LSGCPD_EINVAL, "group must be 0 (SE(3)) or 1 (affine)");
     BatchLayout L;
     std::vector<BatchProblem> bp;
-    int rc = batch_layout(h_problems, B, p.max_iters, &L, &bp);
+    int rc = batch_layout(h_problems, B, p.max_iters, &L, &bp, p.group);
     if (rc) return rc;
     LSG_CHECK(ws_bytes >= L.total, LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
     cudaStream_t s = (cudaStream_t)stream;
@@ -677,6 +696,7 @@ LSG_EXPORT int lsgcpd_register_batch(const lsgcpd_problem* h_problems, int B, co
     rp.newton_max = p.newton_max;
     rp.consistent = consistent;
     rp.max_iters = p.max_iters;
+    rp.group = p.group;
     LSG_CUDA(cudaMemsetAsync(ws + L.iters, 0, sizeof(int) * B, s));
     LSG_CUDA(cudaMemsetAsync(ws + L.nll, 0, sizeof(double) * (p.max_iters + 1) * B, s));
     init_batch_launch(dbp, B, st, rp, p.sigma2_init, mom, reinterpret_cast<double*>(ws + L.sig2), s);

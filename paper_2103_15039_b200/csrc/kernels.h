@@ -11,6 +11,7 @@ struct RegParams {
     const float* phi;         // per-source-point confidences φ(x_n) (Eq. 8) or NULL
     int64_t M;
     int newton_max, consistent, max_iters;
+    int group;                // 0: SE(3) (rigid, the paper's M step); 1: affine GA⁺(3)
 };
 
 // Batched registrations (NEXT-3): one descriptor per problem, in device memory.  Units of all problems

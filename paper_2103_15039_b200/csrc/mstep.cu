@@ -176,6 +176,19 @@ __device__ inline void basis4(int k, double* E) {
     else E[(k - 3) * 4 + 3] = 1.0;
 }
 
+// Lie algebra basis for the Newton step: K = 6 → se(3) (basis4), K = 12 → aff(3) (reading R24):
+// E_{3i+j} = e_i e_jᵀ in the linear block (k < 9, row-major), E_{9+a} = translation a.
+template <int K>
+__device__ inline void basisK(int k, double* E) {
+    if (K == 6) {
+        basis4(k, E);
+        return;
+    }
+    for (int i = 0; i < 16; ++i) E[i] = 0.0;
+    if (k < 9) E[(k / 3) * 4 + (k % 3)] = 1.0;
+    else E[(k - 9) * 4 + 3] = 1.0;
+}
+
 __device__ inline void mat4mul(const double* A, const double* B, double* C) {
     for (int i = 0; i < 4; ++i)
         for (int j = 0; j < 4; ++j) {
@@ -213,43 +226,83 @@ __device__ inline void se3_exp(const double* d, double* dR, double* dt) {
     for (int i = 0; i < 3; ++i) dt[i] = Vm[3 * i] * d[3] + Vm[3 * i + 1] * d[4] + Vm[3 * i + 2] * d[5];
 }
 
-// Cholesky solve (A + μI) x = b, 6×6.  Returns false if not positive definite.
-__device__ inline bool chol_solve6(const double* A, double mu, const double* b, double* x) {
-    double L[36];
-    for (int i = 0; i < 36; ++i) L[i] = 0.0;
-    for (int j = 0; j < 6; ++j) {
-        double s = A[j * 6 + j] + mu;
-        for (int k = 0; k < j; ++k) s -= L[j * 6 + k] * L[j * 6 + k];
+// Cholesky solve (A + μI) x = b, K×K.  Returns false if not positive definite.
+template <int K>
+__device__ inline bool chol_solve(const double* A, double mu, const double* b, double* x) {
+    double L[K * K];
+    for (int i = 0; i < K * K; ++i) L[i] = 0.0;
+    for (int j = 0; j < K; ++j) {
+        double s = A[j * K + j] + mu;
+        for (int k = 0; k < j; ++k) s -= L[j * K + k] * L[j * K + k];
         if (!(s > 0.0)) return false;
         const double d = sqrt(s);
-        L[j * 6 + j] = d;
-        for (int i = j + 1; i < 6; ++i) {
-            double v = A[i * 6 + j];
-            for (int k = 0; k < j; ++k) v -= L[i * 6 + k] * L[j * 6 + k];
-            L[i * 6 + j] = v / d;
+        L[j * K + j] = d;
+        for (int i = j + 1; i < K; ++i) {
+            double v = A[i * K + j];
+            for (int k = 0; k < j; ++k) v -= L[i * K + k] * L[j * K + k];
+            L[i * K + j] = v / d;
         }
     }
-    double y[6];
-    for (int i = 0; i < 6; ++i) {
+    double y[K];
+    for (int i = 0; i < K; ++i) {
         double v = b[i];
-        for (int k = 0; k < i; ++k) v -= L[i * 6 + k] * y[k];
-        y[i] = v / L[i * 6 + i];
+        for (int k = 0; k < i; ++k) v -= L[i * K + k] * y[k];
+        y[i] = v / L[i * K + i];
     }
-    for (int i = 5; i >= 0; --i) {
+    for (int i = K - 1; i >= 0; --i) {
         double v = y[i];
-        for (int k = i + 1; k < 6; ++k) v -= L[k * 6 + i] * x[k];
-        x[i] = v / L[i * 6 + i];
+        for (int k = i + 1; k < K; ++k) v -= L[k * K + i] * x[k];
+        x[i] = v / L[i * K + i];
     }
     return true;
 }
 
+// exp of an aff(3) element δ (matrix exponential of the 4×4 [[B, v], [0, 0]]): scaling and squaring with a
+// 16-term Taylor series (‖·‖₁ ≤ 1/4 after scaling: truncation < 1e-30).  Returns the linear block and translation.
+__device__ inline void aff_exp(const double* d, double* dA, double* dt) {
+    double G[16];
+    for (int i = 0; i < 16; ++i) G[i] = 0.0;
+    for (int k = 0; k < 9; ++k) G[(k / 3) * 4 + (k % 3)] = d[k];
+    for (int a = 0; a < 3; ++a) G[a * 4 + 3] = d[9 + a];
+    double nrm = 0.0;
+    for (int c = 0; c < 4; ++c) {
+        double col = 0.0;
+        for (int r = 0; r < 4; ++r) col += fabs(G[r * 4 + c]);
+        nrm = fmax(nrm, col);
+    }
+    int sq = 0;
+    while (nrm > 0.25 && sq < 60) { nrm *= 0.5; ++sq; }
+    const double sc = ldexp(1.0, -sq);
+    for (int i = 0; i < 16; ++i) G[i] *= sc;
+    double E[16], T[16], T2[16];
+    for (int i = 0; i < 16; ++i) E[i] = T[i] = (i % 5 == 0) ? 1.0 : 0.0;
+    for (int k = 1; k <= 16; ++k) {
+        mat4mul(T, G, T2);
+        for (int i = 0; i < 16; ++i) {
+            T[i] = T2[i] / (double)k;
+            E[i] += T[i];
+        }
+    }
+    for (int r = 0; r < sq; ++r) {
+        mat4mul(E, E, T2);
+        for (int i = 0; i < 16; ++i) E[i] = T2[i];
+    }
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) dA[3 * i + j] = E[i * 4 + j];
+        dt[i] = E[i * 4 + 3];
+    }
+}
+
 // One warp: the dense algebra (v = U + 𝔾Δθ, J, 𝔾J, ∇, H) is spread over the lanes; the damping loop
-// (Cholesky 6×6, exp, candidate q) runs on lane 0.  All lanes end with identical state.
+// (Cholesky K×K, exp, candidate q) runs on lane 0.  All lanes end with identical state.
+// K = 6: SE(3) (the paper's rigid registration); K = 12: the affine group GA⁺(3) (NEXT-4).
+template <int K>
 __device__ __noinline__ void newton_body(IterState* st, const double* __restrict__ mom, const RegParams& rp,
                                          double* nll_trace, double* sigma2_trace, int* iters_done) {
+    constexpr int NP = K * (K + 1) / 2;   // symmetric basis pairs (k ≤ l)
     __shared__ Mom mo;
-    __shared__ double S[21][16];
-    __shared__ double J[6][12], GJ[6][12], v[12], Bm[16], H[36], grad[6];
+    __shared__ double S[NP][16];
+    __shared__ double J[K][12], GJ[K][12], v[12], Bm[16], H[K * K], grad[K];
     __shared__ double Rs[9], tsh[3], th_E[12];
     __shared__ double q_cur, step_rot, step_trans;
     __shared__ int stop;
@@ -262,19 +315,17 @@ __device__ __noinline__ void newton_body(IterState* st, const double* __restrict
         mo.GG[r][c] = mom[s3(i, jj) * 10 + s4(a, b)];
     }
     if (lane < 12) mo.U[lane] = mom[60 + lane];
-    if (lane < 21) {
-        int k = 0, l = 0, idx = 0;
-        for (k = 0; k < 6; ++k) {
-            for (l = k; l < 6; ++l, ++idx)
-                if (idx == lane) break;
-            if (idx == lane && l < 6) break;
-        }
+    for (int pidx = lane; pidx < NP; pidx += 32) {
+        int k = 0, l = 0;
+        for (int idx = 0, kk = 0; kk < K; ++kk)
+            for (int ll = kk; ll < K; ++ll, ++idx)
+                if (idx == pidx) { k = kk; l = ll; }
         double Ek[16], El[16], EE1[16], EE2[16];
-        basis4(k, Ek);
-        basis4(l, El);
+        basisK<K>(k, Ek);
+        basisK<K>(l, El);
         mat4mul(Ek, El, EE1);
         mat4mul(El, Ek, EE2);
-        for (int i = 0; i < 16; ++i) S[lane][i] = 0.5 * (EE1[i] + EE2[i]);
+        for (int i = 0; i < 16; ++i) S[pidx][i] = 0.5 * (EE1[i] + EE2[i]);
     }
     if (lane == 0) {
         for (int i = 0; i < 9; ++i) Rs[i] = s.R[i];
@@ -298,21 +349,22 @@ __device__ __noinline__ void newton_body(IterState* st, const double* __restrict
             double gr = 0.0;
             for (int c = 0; c < 12; ++c) gr = fma(mo.GG[lane][c], dth[c], gr);
             v[lane] = mo.U[lane] + gr;                // ½ ∇_θ q
-        } else if (lane < 18) {
+        } else if (lane < 12 + K) {
             const int k = lane - 12;                  // dθ/dξ_k = (Θ̃ E_k)[0:3,:]
             double Ek[16], P4[16];
-            basis4(k, Ek);
+            basisK<K>(k, Ek);
             mat4mul(Gt, Ek, P4);
             for (int r = 0; r < 12; ++r) J[k][r] = P4[r];
         }
         __syncwarp();
-        for (int e = lane; e < 72; e += 32) {         // 𝔾 J_k
+        for (int e = lane; e < K * 12; e += 32) {     // 𝔾 J_k
             const int k = e / 12, r = e % 12;
             double a = 0.0;
             for (int c = 0; c < 12; ++c) a = fma(mo.GG[r][c], J[k][c], a);
             GJ[k][r] = a;
         }
-        if (lane < 6) {
+        static_assert(K <= 16, "lanes 16..31 hold B");
+        if (lane < K) {
             double g = 0.0;
             for (int r = 0; r < 12; ++r) g = fma(J[lane][r], v[r], g);
             grad[lane] = g;
@@ -323,37 +375,43 @@ __device__ __noinline__ void newton_body(IterState* st, const double* __restrict
             Bm[mi * 4 + j] = b;
         }
         __syncwarp();
-        if (lane < 21) {
+        for (int pidx = lane; pidx < NP; pidx += 32) {
             int k = 0, l = 0;
-            for (int idx = 0, kk = 0; kk < 6; ++kk)
-                for (int ll = kk; ll < 6; ++ll, ++idx)
-                    if (idx == lane) { k = kk; l = ll; }
+            for (int idx = 0, kk = 0; kk < K; ++kk)
+                for (int ll = kk; ll < K; ++ll, ++idx)
+                    if (idx == pidx) { k = kk; l = ll; }
             double h = 0.0;
             for (int r = 0; r < 12; ++r) h = fma(J[k][r], GJ[l][r], h);
-            for (int i = 0; i < 16; ++i) h = fma(Bm[i], S[lane][i], h);
-            H[k * 6 + l] = h;
-            H[l * 6 + k] = h;
+            for (int i = 0; i < 16; ++i) h = fma(Bm[i], S[pidx][i], h);
+            H[k * K + l] = h;
+            H[l * K + k] = h;
         }
         __syncwarp();
         if (lane == 0) {
-            const double tr = fabs(H[0] + H[7] + H[14] + H[21] + H[28] + H[35]) / 6.0;
+            double trs = 0.0;
+            for (int k = 0; k < K; ++k) trs += H[k * K + k];
+            const double tr = fabs(trs) / (double)K;
             double mu = 0.0;
             bool accepted = false, converged = false;
             for (int tries = 0; tries < 20; ++tries) {
-                double delta[6], mg[6];
-                for (int k = 0; k < 6; ++k) mg[k] = -grad[k];
-                if (!chol_solve6(H, mu, mg, delta)) {
+                double delta[K], mg[K];
+                for (int k = 0; k < K; ++k) mg[k] = -grad[k];
+                if (!chol_solve<K>(H, mu, mg, delta)) {
                     mu = fmax(10.0 * mu, 1e-6 * tr);
                     continue;
                 }
-                const double nr = sqrt(delta[0] * delta[0] + delta[1] * delta[1] + delta[2] * delta[2]);
-                const double nt = sqrt(delta[3] * delta[3] + delta[4] * delta[4] + delta[5] * delta[5]);
+                double nr = 0.0, nt = 0.0;   // linear (rotation) part, translation part of the step
+                for (int k = 0; k < K - 3; ++k) nr += delta[k] * delta[k];
+                for (int k = K - 3; k < K; ++k) nt += delta[k] * delta[k];
+                nr = sqrt(nr);
+                nt = sqrt(nt);
                 if (nr < 1e-10 && nt < 1e-10 * s.extent) {
                     converged = true;
                     break;
                 }
                 double dR[9], dt[3], Rn[9], tn[3];
-                se3_exp(delta, dR, dt);
+                if (K == 6) se3_exp(delta, dR, dt);
+                else aff_exp(delta, dR, dt);
                 for (int i = 0; i < 3; ++i) {
                     for (int j = 0; j < 3; ++j)
                         Rn[3 * i + j] = Rs[3 * i] * dR[j] + Rs[3 * i + 1] * dR[3 + j] + Rs[3 * i + 2] * dR[6 + j];
@@ -417,7 +475,8 @@ __device__ __noinline__ void newton_body(IterState* st, const double* __restrict
 
 __global__ void __launch_bounds__(32) newton_kernel(IterState* st, const double* __restrict__ mom, RegParams rp,
                                                     double* nll_trace, double* sigma2_trace, int* iters_done) {
-    newton_body(st, mom, rp, nll_trace, sigma2_trace, iters_done);
+    if (rp.group) newton_body<12>(st, mom, rp, nll_trace, sigma2_trace, iters_done);
+    else newton_body<6>(st, mom, rp, nll_trace, sigma2_trace, iters_done);
 }
 
 // ---- batched registrations (NEXT-3): one CTA / warp per problem -----------------------------------------
@@ -442,8 +501,12 @@ __global__ void __launch_bounds__(32) newton_batch_kernel(const BatchProblem* __
     rp.omega_ref_target = P.omega_ref;
     rp.spc = P.spc;
     rp.M = P.M;
-    newton_body(st + b, mom + (int64_t)b * kBatchMom, rp, nll_trace + (int64_t)b * (rp.max_iters + 1),
-                sigma2_trace + (int64_t)b * (rp.max_iters + 2), iters_done + b);
+    if (rp.group)
+        newton_body<12>(st + b, mom + (int64_t)b * kBatchMom, rp, nll_trace + (int64_t)b * (rp.max_iters + 1),
+                        sigma2_trace + (int64_t)b * (rp.max_iters + 2), iters_done + b);
+    else
+        newton_body<6>(st + b, mom + (int64_t)b * kBatchMom, rp, nll_trace + (int64_t)b * (rp.max_iters + 1),
+                       sigma2_trace + (int64_t)b * (rp.max_iters + 2), iters_done + b);
 }
 
 // σ²₀ of problem b (CPD closed form) and its iteration-0 state, one CTA per problem.

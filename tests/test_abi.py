@@ -50,14 +50,15 @@ def test_struct_layouts_match_header(tmp_path):
                     'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(lsgcpd_prep_params),'
                     ' sizeof(lsgcpd_target_info), sizeof(lsgcpd_annotations), sizeof(lsgcpd_em_params),'
                     ' offsetof(lsgcpd_em_params, sigma2_init), offsetof(lsgcpd_target_info, n_degenerate));'
-                    'printf("%zu %zu\\n", offsetof(lsgcpd_em_params, eta), offsetof(lsgcpd_em_params, d_src_conf));'
+                    'printf("%zu %zu %zu\\n", offsetof(lsgcpd_em_params, eta), offsetof(lsgcpd_em_params, d_src_conf),'
+                    ' offsetof(lsgcpd_em_params, group));'
                     'return 0;}\n')
     exe = tmp_path / "sizes"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)])
     got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
     want = [ctypes.sizeof(pkg.PrepParams), ctypes.sizeof(pkg.TargetInfo), ctypes.sizeof(pkg.Annotations),
             ctypes.sizeof(pkg.EmParams), pkg.EmParams.sigma2_init.offset, pkg.TargetInfo.n_degenerate.offset,
-            pkg.EmParams.eta.offset, pkg.EmParams.d_src_conf.offset]
+            pkg.EmParams.eta.offset, pkg.EmParams.d_src_conf.offset, pkg.EmParams.group.offset]
     assert got == want
 
 

@@ -677,7 +677,7 @@ struct Tc2Cfg {
 };
 static_assert(kTcStages == 4, "stage arithmetic below assumes 4 stages");
 
-template <int NWG, int RB, bool kLiteral, bool kStX8, bool kSelf, int MW>
+template <int NWG, int RB, bool kLiteral, bool kStX8, bool kSelf, int MW, int NT>
 __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
     estep_tc2_kernel(const char* __restrict__ tc, const float* __restrict__ src, int64_t N,
                      const IterState* __restrict__ st, Sched sc, float* __restrict__ part) {
@@ -688,6 +688,10 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
     constexpr int kChunks = kTcTile / kTcChunk;
     static_assert(kChunks % 2 == 0, "chunks per tile must be even");
     constexpr int kNF = 13;   // D features kept: 1, y, W, b
+    // D accumulates NT consecutive tiles of one source block (a "D group") before it is drained; a group
+    // also ends at a block boundary and at the end of the CTA's range.  With MMA warps, a stage is
+    // released by the consumers when they finish reading it plus one tcgen05.commit per MMA warp.
+    static_assert(!kSelf || NT == 1, "self-issuing warpgroups drain every tile");
     __shared__ __align__(1024) char tiles_st[kTcStages][kTcTileBytes];
     extern __shared__ __align__(16) char dsmem[];
     float* smS = reinterpret_cast<float*>(dsmem);   // [3 kNF][RB × consumer threads]: S1, R, C
@@ -713,7 +717,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
     if (threadIdx.x == 32) {
         for (int s = 0; s < kTcStages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], kNCW);
+            mbar_init(&empty_bar[s], kSelf ? kNCW : kNCW + MW);
         }
         for (int w = 0; w < NWG; ++w)
             for (int b = 0; b < 2; ++b) {
@@ -752,10 +756,14 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         const uint32_t tiles0 = smem_u32(&tiles_st[0][0]) + kTcBOff;
         constexpr int kWPer = NWG / MW;
         const int w0 = (warp - kNCW - 1) * kWPer;   // this MMA warp serves warpgroups [w0, w0 + kWPer)
+        int64_t tile = u0 % sc.T, grp = 0;
+        int tig = 0;                                  // tile index within the current D group
         for (int64_t it = 0; it < nunits; ++it) {
             const int s = (int)(it & 3);
-            const int db = (int)(it & 1);
-            const uint32_t dpar = (uint32_t)(((it >> 1) & 1) ^ 1);   // completion (it>>1) - 1 of dfree[db]
+            const int db = (int)(grp & 1);
+            const bool first = tig == 0;
+            const bool last = tig + 1 == NT || tile + 1 == sc.T || it + 1 == nunits;
+            const uint32_t dpar = (uint32_t)(((grp >> 1) & 1) ^ 1);   // completion (grp>>1) - 1 of dfree[db]
             mbar_wait_sleep(&full_bar[s], (uint32_t)((it >> 2) & 1));
             const uint32_t bbase = tiles0 + (uint32_t)s * kTcTileBytes;
 #pragma unroll
@@ -765,7 +773,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
 #pragma unroll
                 for (int wi = 0; wi < kWPer; ++wi) {
                     const int w = w0 + wi;
-                    if (c == 0) mbar_wait_sleep(&dfree[w][db], dpar);
+                    if (c == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
                     mbar_wait_sleep(&afull[w][ab], (uint32_t)((c >> 1) & 1));
                     tc_fence_after();
                     if (elect_one()) {
@@ -774,17 +782,25 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
 #ifndef LSG_TC2_NOMMA   // diagnostic builds only (tools/build_diag.sh)
 #pragma unroll
                         for (int rb = 0; rb < RB; ++rb) {
-                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, c == 0 ? 0u : 1u);
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, (c == 0 && first) ? 0u : 1u);
                             mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
                             mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
                         }
 #endif
                         mma_commit(&aempty[w][ab]);
-                        if (c == kChunks - 1) mma_commit(&dfull[w][db]);
+                        if (c == kChunks - 1 && last) mma_commit(&dfull[w][db]);
+                        if (c == kChunks - 1 && wi == kWPer - 1) mma_commit(&empty_bar[s]);   // stage s read
                     }
                     __syncwarp();
                 }
             }
+            if (last) {
+                tig = 0;
+                ++grp;
+            } else {
+                ++tig;
+            }
+            if (++tile == sc.T) tile = 0;
         }
         return;
     }
@@ -850,10 +866,11 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         }
         nfold = 0;
     };
-    // drain tile `itd`'s D (all its MMAs are complete once dfull fires), release D and the smem stage
-    auto drain = [&](int64_t itd) {
-        const int db = (int)(itd & 1);
-        mbar_wait_sleep(&dfull[wg][db], (uint32_t)((itd >> 1) & 1));
+    // drain D group `gd` (all its MMAs are complete once dfull fires), release D (and, self-issuing, the
+    // stage of its single tile `itd`)
+    auto drain = [&](int64_t gd, int64_t itd) {
+        const int db = (int)(gd & 1);
+        mbar_wait_sleep(&dfull[wg][db], (uint32_t)((gd >> 1) & 1));
         tc_fence_after();
         uint32_t d[RB][16];
 #pragma unroll
@@ -863,7 +880,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         __syncwarp();
         if (lane == 0) {
             if (!kSelf) mbar_arrive(&dfree[wg][db]);   // self-issue: the next chunk-0 barrier orders it
-            mbar_arrive(&empty_bar[itd & 3]);
+            if (kSelf) mbar_arrive(&empty_bar[itd & 3]);
         }
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) {
@@ -981,11 +998,13 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
 
     int64_t j = u0 / sc.T, tile = u0 % sc.T;
     load_points(j);
-    bool pending = false;   // the previous tile's D has not been drained yet
+    bool pending = false;   // the previous D group has not been drained yet
+    int64_t grp = 0, pend_g = 0, pend_it = 0;
+    int tig = 0;
     for (int64_t it = 0; it < nunits; ++it) {
         mbar_wait_sleep(&full_bar[it & 3], (uint32_t)((it >> 2) & 1));
         cur_b = smem_u32(&tiles_st[0][0]) + kTcBOff + (uint32_t)(it & 3) * kTcTileBytes;
-        cur_db = (uint32_t)(it & 1);
+        cur_db = (uint32_t)(grp & 1);
         const float4* core = reinterpret_cast<const float4*>(&tiles_st[it & 3][0]);
         float2 Lt[RB];
 #pragma unroll
@@ -1000,9 +1019,13 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
             chunk(core, c, Lt, std::integral_constant<int, 0>());
             chunk(core, c + 1, Lt, std::integral_constant<int, 1>());
             if (c == 0 && pending) {
-                drain(it - 1);
+                drain(pend_g, pend_it);
                 pending = false;
             }
+        }
+        if (!kSelf) {   // this warp is done reading the stage's core data
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[it & 3]);
         }
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) {
@@ -1012,11 +1035,23 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
             Ct[rb] = (t - Rt[rb]) - y;
             Rt[rb] = t;
         }
-        pending = true;
-        if (++tile == sc.T || it + 1 == nunits) {   // source block (or the CTA's range) ends here
-            drain(it);
-            pending = false;
-            flush(j);
+        const bool block_end = tile + 1 == sc.T || it + 1 == nunits;
+        const bool last = tig + 1 == NT || block_end;
+        if (last) {
+            if (block_end) {   // source block (or the CTA's range) ends here: drain and flush now
+                drain(grp, it);
+                flush(j);
+            } else {
+                pending = true;
+                pend_g = grp;
+                pend_it = it;
+            }
+            tig = 0;
+            ++grp;
+        } else {
+            ++tig;
+        }
+        if (++tile == sc.T) {
             tile = 0;
             ++j;
             if (it + 1 < nunits) load_points(j);
@@ -1084,11 +1119,12 @@ struct TcVariant {
 #define LSG_TC(NWG, RB, MW, PV)                                                                           \
     {NWG, RB, MW, PV, TcCfg<NWG, RB, MW>::kThreads, TcCfg<NWG, RB, MW>::kBlk, TcCfg<NWG, RB, MW>::kSmem, \
      {(const void*)estep_tc_kernel<NWG, RB, MW, false>, (const void*)estep_tc_kernel<NWG, RB, MW, true>}}
-#define LSG_TC2M(NWG, RB, X8, SELF, MW, PV)                                                          \
+#define LSG_TC2N(NWG, RB, X8, SELF, MW, NT, PV)                                                      \
     {NWG, RB, MW, PV, Tc2Cfg<NWG, RB, SELF, MW>::kThreads, Tc2Cfg<NWG, RB, SELF, MW>::kBlk,          \
      Tc2Cfg<NWG, RB, SELF, MW>::kSmem,                                                               \
-     {(const void*)estep_tc2_kernel<NWG, RB, false, X8, SELF, MW>,                                   \
-      (const void*)estep_tc2_kernel<NWG, RB, true, X8, SELF, MW>}}
+     {(const void*)estep_tc2_kernel<NWG, RB, false, X8, SELF, MW, NT>,                               \
+      (const void*)estep_tc2_kernel<NWG, RB, true, X8, SELF, MW, NT>}}
+#define LSG_TC2M(NWG, RB, X8, SELF, MW, PV) LSG_TC2N(NWG, RB, X8, SELF, MW, 1, PV)
 #define LSG_TC2(NWG, RB, X8, SELF, PV) LSG_TC2M(NWG, RB, X8, SELF, 1, PV)
 static const TcVariant kTcVariants[] = {
     LSG_TC(4, 2, 2, 0),   // 16 consumer warps, 2 points/thread (1024-point blocks) — CUDA-core variant 0
@@ -1116,6 +1152,11 @@ static const TcVariant kTcVariants[] = {
     LSG_TC2M(3, 2, true, false, 3, 3),   // 19: as 9
     LSG_TC2M(6, 1, true, false, 3, 3),   // 20: as 12, one MMA warp per two warpgroups
     LSG_TC2M(2, 2, true, false, 2, 9),   // 21: as 14
+    // D accumulated over NT tiles before each drain
+    LSG_TC2N(3, 2, true, false, 3, 2, 3),   // 22: as 19, NT = 2
+    LSG_TC2N(3, 2, true, false, 3, 4, 3),   // 23: as 19, NT = 4
+    LSG_TC2N(3, 2, true, false, 3, 8, 3),   // 24: as 19, NT = 8
+    LSG_TC2N(3, 2, true, false, 3, 16, 3),  // 25: as 19, NT = 16
 };
 constexpr int kNumTcVariants = sizeof(kTcVariants) / sizeof(kTcVariants[0]);
 // LSGCPD_TC: unset = automatic (tensor cores unless the problem is too small), 0 = off, 1 = forced on
@@ -1123,7 +1164,7 @@ static int tc_mode() {
     const char* e = getenv("LSGCPD_TC");
     return e ? (atoi(e) != 0 ? 1 : 0) : 2;
 }
-constexpr int kDefaultTcVariant = 19;  // tc2: 12 consumer warps × 2 points, one MMA warp per warpgroup (tools/tc_speed.py)
+constexpr int kDefaultTcVariant = 23;  // tc2, 12 consumer warps × 2 points, one MMA warp per warpgroup, D over 4 tiles (tools/tc_speed.py)
 static int tc_variant_index() {
     const char* e = getenv("LSGCPD_TC_VARIANT");
     int v = e ? atoi(e) : kDefaultTcVariant;

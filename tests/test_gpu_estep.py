@@ -131,7 +131,7 @@ def test_estep_every_kernel_variant(variant, monkeypatch):
         assert_record_parity(rec, ora, wl.target, a32, what=f"variant {variant} w={w}")
 
 
-@pytest.mark.parametrize("tc", [f"1:{v}" for v in range(22)] + ["0"])
+@pytest.mark.parametrize("tc", [f"1:{v}" for v in range(26)] + ["0"])
 def test_estep_tensor_core_and_cuda_core_paths(tc, monkeypatch):
     # default path = tcgen05 kernel (fixed max) + CUDA-core kernel (running max); every tensor-core
     # configuration (LSGCPD_TC_VARIANT) and LSGCPD_TC=0 (CUDA cores only)

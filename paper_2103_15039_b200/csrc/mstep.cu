@@ -180,13 +180,13 @@ __device__ inline void basis4(int k, double* E) {
 // E_{3i+j} = e_i e_jᵀ in the linear block (k < 9, row-major), E_{9+a} = translation a.
 template <int K>
 __device__ inline void basisK(int k, double* E) {
-    if (K == 6) {
+    if constexpr (K == 6) {
         basis4(k, E);
-        return;
+    } else {
+        for (int i = 0; i < 16; ++i) E[i] = 0.0;
+        if (k < 9) E[(k / 3) * 4 + (k % 3)] = 1.0;
+        else E[(k - 9) * 4 + 3] = 1.0;
     }
-    for (int i = 0; i < 16; ++i) E[i] = 0.0;
-    if (k < 9) E[(k / 3) * 4 + (k % 3)] = 1.0;
-    else E[(k - 9) * 4 + 3] = 1.0;
 }
 
 __device__ inline void mat4mul(const double* A, const double* B, double* C) {

@@ -585,6 +585,7 @@ static int batch_layout(const lsgcpd_problem* P, int B, int max_iters, BatchLayo
         const int64_t M_pad = pad_targets(p.M);
         q.target = p.d_target;
         q.body = target_body(p.d_target);
+        q.tc = reinterpret_cast<const char*>(target_tc(p.d_target, M_pad));
         q.src = p.d_src;
         q.conf = p.d_src_conf;
         q.M = p.M;
@@ -606,7 +607,7 @@ static int batch_layout(const lsgcpd_problem* P, int B, int max_iters, BatchLayo
     Sched sc;
     memset(&sc, 0, sizeof(sc));
     sc.U = units;
-    const int64_t slots = (int64_t)nsm * 4;   // kBMinB CTAs per SM
+    const int64_t slots = (int64_t)nsm;       // one CTA per SM (both batched E-step kernels)
     sc.G = units < slots ? units : slots;
     sc.B = kB;
     int64_t kmax = 1;

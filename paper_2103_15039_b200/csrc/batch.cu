@@ -18,9 +18,9 @@
 namespace lsg {
 
 constexpr int kBPPT = 2;                     // source points per consumer thread (one f32x2 lane)
-constexpr int kBNCW = 4;                     // consumer warps
-constexpr int kBMinB = 4;                    // CTAs per SM
-constexpr int kBBlk = kBPPT * kBNCW * 32;    // 256 source points per block
+constexpr int kBNCW = 12;                    // consumer warps
+constexpr int kBMinB = 1;                    // CTAs per SM
+constexpr int kBBlk = kBPPT * kBNCW * 32;    // 768 source points per block (= the tensor-core kernel's)
 
 int batch_block_points() { return kBBlk; }
 size_t batch_partial_floats(int64_t nblk, int64_t kmax) { return (size_t)nblk * kmax * kPartF * kBBlk; }
@@ -66,10 +66,16 @@ struct BatchCursor {
     }
 };
 
+// Which problems a batched E-step kernel serves: mode 0 = every active problem (CUDA cores only),
+// 1 = active problems in the running-max mode (the tensor-core kernel takes the fixed-max ones).
+__device__ __forceinline__ bool serves(const IterState& s, int mode) {
+    return s.active && (mode == 0 || !s.fixed);
+}
+
 template <bool kLiteral>
 __global__ void __launch_bounds__((kBNCW + 1) * 32, kBMinB)
     estep_batch_kernel(const BatchProblem* __restrict__ bp, int B, const IterState* __restrict__ st, Sched sc,
-                       float* __restrict__ part) {
+                       float* __restrict__ part, int mode) {
     using T = float2;
     constexpr int NL = kBPPT / 2;
     constexpr int kTileF4 = kTT * kTgtFloats / 4;
@@ -99,7 +105,7 @@ __global__ void __launch_bounds__((kBNCW + 1) * 32, kBMinB)
             cur.start(bp, B, u0);
             int64_t it = 0;
             for (int64_t u = u0; u < u1; ++u, cur.next(bp)) {
-                if (!st[cur.b].active) continue;
+                if (!serves(st[cur.b], mode)) continue;
                 const int s = (int)(it % kStages);
                 const uint32_t ph = (uint32_t)((it / kStages) & 1);
                 mbar_wait_sleep(&empty_bar[s], ph ^ 1);
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__((kBNCW + 1) * 32, kBMinB)
     cur.start(bp, B, u0);
     int64_t it = 0;
     for (int64_t u = u0; u < u1; ++u, cur.next(bp)) {
-        if (!st[cur.b].active) continue;
+        if (!serves(st[cur.b], mode)) continue;
         if (cur.b != cur_b || cur.j != cur_j) {
             if (cur_b >= 0) flush(cur_b, cur_j);
             cur_b = cur.b;
@@ -264,6 +270,346 @@ __global__ void __launch_bounds__((kBNCW + 1) * 32, kBMinB)
     if (cur_b >= 0) flush(cur_b, cur_j);
 }
 
+// ---- batched tensor-core E step ---------------------------------------------------------------------
+// estep_tc2_kernel's pipeline (TMA producer, one MMA warp per warpgroup, TF32 3-term split of p into TMEM,
+// D accumulated over NT tiles, Kahan-folded drains) walking the concatenated units of the problems that are
+// active and in the fixed-max mode.  A D group also ends where a source block (hence a problem) ends.
+constexpr int kBTNWG = 3, kBTRB = 2, kBTMW = 3, kBTNT = 4;
+constexpr int kBTNCW = 4 * kBTNWG;
+constexpr int kBTThreads = (kBTNCW + 1 + kBTMW) * 32;
+constexpr int kBTWGCols = 64 * kBTRB;
+constexpr int kBTSmF = 39;
+constexpr size_t kBTSmem = (size_t)kBTSmF * kBTNCW * 32 * kBTRB * sizeof(float);
+static_assert(kBTNWG * 128 * kBTRB == kBBlk, "both batched kernels use one block size");
+
+__device__ __forceinline__ bool serves_tc(const IterState& s) { return s.active && s.fixed; }
+
+template <bool kLiteral>
+__global__ void __launch_bounds__(kBTThreads, 1)
+    estep_batch_tc_kernel(const BatchProblem* __restrict__ bp, int B, const IterState* __restrict__ st, Sched sc,
+                          float* __restrict__ part) {
+    constexpr int NWG = kBTNWG, RB = kBTRB, MW = kBTMW, NT = kBTNT;
+    constexpr int kNCW = kBTNCW, kBlk = kBBlk, kWGCols = kBTWGCols;
+    constexpr int kChunks = kTcTile / kTcChunk;
+    constexpr int kNF = 13;
+    __shared__ __align__(1024) char tiles_st[kTcStages][kTcTileBytes];
+    extern __shared__ __align__(16) char dsmem[];
+    float* smS = reinterpret_cast<float*>(dsmem);
+    __shared__ __align__(8) uint64_t full_bar[kTcStages];
+    __shared__ __align__(8) uint64_t empty_bar[kTcStages];
+    __shared__ __align__(8) uint64_t afull[NWG][2], aempty[NWG][2], dfull[NWG][2], dfree[NWG][2];
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t g = blockIdx.x;
+    const int64_t u0 = sched_start(sc, g), u1 = sched_start(sc, g + 1);
+    if (u0 >= u1) return;
+    // does this CTA have any unit to serve?  (all roles must agree before TMEM is allocated)
+    {
+        BatchCursor c0;
+        c0.start(bp, B, u0);
+        const BatchCursor cl = c0;
+        bool any = false;
+        // the range spans problems c0.b .. the problem of u1 - 1
+        const int b1 = find_problem_unit(bp, B, u1 - 1);
+        for (int b = cl.b; b <= b1 && !any; ++b) any = serves_tc(st[b]);
+        if (!any) return;
+    }
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"((uint32_t)kTcCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 32) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], kNCW + MW);
+        }
+        for (int w = 0; w < NWG; ++w)
+            for (int b = 0; b < 2; ++b) {
+                mbar_init(&afull[w][b], 4);
+                mbar_init(&aempty[w][b], 1);
+                mbar_init(&dfull[w][b], 1);
+                mbar_init(&dfree[w][b], 4);
+            }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    if (tmem != 0u) __trap();
+
+    if (warp == kNCW) {
+        // producer: TMA bulk copies of the served problems' tensor-core tiles
+        if (lane == 0) {
+            BatchCursor cur;
+            cur.start(bp, B, u0);
+            int64_t it = 0;
+            for (int64_t u = u0; u < u1; ++u, cur.next(bp)) {
+                if (!serves_tc(st[cur.b])) continue;
+                const int s = (int)(it & 3);
+                mbar_wait_sleep(&empty_bar[s], (uint32_t)(((it >> 2) & 1) ^ 1));
+                mbar_arrive_expect_tx(&full_bar[s], kTcTileBytes);
+                bulk_g2s(&tiles_st[s][0], bp[cur.b].tc + cur.tile * (int64_t)kTcTileBytes, kTcTileBytes, &full_bar[s]);
+                ++it;
+            }
+        }
+        return;
+    }
+    if (warp > kNCW) {
+        // MMA warp for warpgroup w (see estep_tc2_kernel); groups end at NT tiles or a block end
+        const uint32_t tiles0 = smem_u32(&tiles_st[0][0]) + kTcBOff;
+        const int w = warp - kNCW - 1;
+        BatchCursor cur;
+        cur.start(bp, B, u0);
+        int64_t it = 0, grp = 0;
+        int tig = 0;
+        for (int64_t u = u0; u < u1; ++u, cur.next(bp)) {
+            if (!serves_tc(st[cur.b])) continue;
+            const int s = (int)(it & 3);
+            const int db = (int)(grp & 1);
+            const bool first = tig == 0;
+            const bool last = tig + 1 == NT || cur.tile + 1 == bp[cur.b].T || u + 1 == u1;
+            const uint32_t dpar = (uint32_t)(((grp >> 1) & 1) ^ 1);
+            mbar_wait_sleep(&full_bar[s], (uint32_t)((it >> 2) & 1));
+            const uint32_t bbase = tiles0 + (uint32_t)s * kTcTileBytes;
+#pragma unroll
+            for (int c = 0; c < kChunks; ++c) {
+                const int ab = c & 1;
+                const uint64_t bhi = bdesc(bbase + 1024 * c), blo = bdesc(bbase + 1024 * c + 512);
+                if (c == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
+                mbar_wait_sleep(&afull[w][ab], (uint32_t)((c >> 1) & 1));
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
+                    const uint32_t colA = (uint32_t)(w * kWGCols + 32 * RB + ab * 16 * RB);
+#pragma unroll
+                    for (int rb = 0; rb < RB; ++rb) {
+                        mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, (c == 0 && first) ? 0u : 1u);
+                        mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
+                        mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
+                    }
+                    mma_commit(&aempty[w][ab]);
+                    if (c == kChunks - 1 && last) mma_commit(&dfull[w][db]);
+                    if (c == kChunks - 1) mma_commit(&empty_bar[s]);
+                }
+                __syncwarp();
+            }
+            if (last) {
+                tig = 0;
+                ++grp;
+            } else {
+                ++tig;
+            }
+            ++it;
+        }
+        return;
+    }
+
+    // consumers
+    const int wg = warp >> 2, q = warp & 3;
+    const int tw = q * 32 + lane;
+    const int tid = threadIdx.x;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(wg * kWGCols);
+    constexpr int kRC = kNCW * 32 * RB;
+    float2 h[RB][3], l[RB][3];
+    float Rt[RB], Ct[RB];
+    float k2 = 0.f;
+    float2 nk2 = bc(0.f);
+    int nfold = 0;
+
+    auto load_points = [&](int b, int64_t j) {
+        const IterState* s = st + b;
+        k2 = s->k2;
+        nk2 = bc(-k2);
+        double Rm[9], tv[3];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) Rm[i] = s->R[i];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) tv[i] = s->t[i];
+        const float* src = bp[b].src;
+        const int64_t N = bp[b].N;
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+            const int64_t n = j * kBlk + (wg * RB + k) * 128 + tw;
+            double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+            if (n < N) {
+                x0 = src[3 * n];
+                x1 = src[3 * n + 1];
+                x2 = src[3 * n + 2];
+            }
+            const double X[3] = {fma(Rm[0], x0, fma(Rm[1], x1, fma(Rm[2], x2, tv[0]))),
+                                 fma(Rm[3], x0, fma(Rm[4], x1, fma(Rm[5], x2, tv[1]))),
+                                 fma(Rm[6], x0, fma(Rm[7], x1, fma(Rm[8], x2, tv[2])))};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const float hi = __double2float_rn(X[a]);
+                h[k][a] = bc(hi);
+                l[k][a] = bc(__double2float_rn(X[a] - (double)hi));
+            }
+            Rt[k] = Ct[k] = 0.f;
+#pragma unroll
+            for (int f = 0; f < kBTSmF; ++f) smS[f * kRC + k * (kNCW * 32) + tid] = 0.f;
+        }
+        nfold = 0;
+    };
+    auto fold_s1 = [&]() {
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+            const int rc = rb * (kNCW * 32) + tid;
+#pragma unroll
+            for (int f = 0; f < kNF; ++f) {
+                const float L = smS[f * kRC + rc];
+                const float R = smS[(kNF + f) * kRC + rc], C = smS[(2 * kNF + f) * kRC + rc];
+                const float y = L - C;
+                const float t = R + y;
+                smS[(2 * kNF + f) * kRC + rc] = (t - R) - y;
+                smS[(kNF + f) * kRC + rc] = t;
+                smS[f * kRC + rc] = 0.f;
+            }
+        }
+        nfold = 0;
+    };
+    auto drain = [&](int64_t gd) {
+        const int db = (int)(gd & 1);
+        mbar_wait_sleep(&dfull[wg][db], (uint32_t)((gd >> 1) & 1));
+        tc_fence_after();
+        uint32_t d[RB][16];
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) tmem_ld16(tl + (uint32_t)(db * 16 * RB + rb * 16), d[rb]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dfree[wg][db]);
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+            const int rc = rb * (kNCW * 32) + tid;
+#pragma unroll
+            for (int f = 0; f < kNF; ++f) smS[f * kRC + rc] += __uint_as_float(d[rb][f]);
+        }
+        if (++nfold == 16) fold_s1();
+    };
+    auto flush = [&](int b, int64_t j) {
+        fold_s1();
+        const BatchProblem& P = bp[b];
+        const int64_t slot = j * sc.kmax + (g - sched_owner(sc, P.unit0 + j * P.T));
+        float* base = part + P.part0 + slot * (int64_t)kPartF * kBlk;
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+            const int bb = (wg * RB + k) * 128 + tw;
+            const int rc = k * (kNCW * 32) + tid;
+#pragma unroll
+            for (int f = 0; f < 13; ++f)
+                base[f * kBlk + bb] = __fsub_rn(smS[(kNF + f) * kRC + rc], smS[(2 * kNF + f) * kRC + rc]);
+            base[13 * kBlk + bb] = __fsub_rn(Rt[k], Ct[k]);
+            base[14 * kBlk + bb] = 0.f;
+            base[15 * kBlk + bb] = 0.f;
+        }
+    };
+    auto chunk = [&](const float4* core, int c, float2 (&Lt)[RB], auto ABc) {
+        constexpr int AB = decltype(ABc)::value;
+        uint32_t av[RB][16];
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+            const int pr = c * 4 + pp;
+            const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) {
+                const float2 rx = __fadd2_rn(__fadd2_rn(h[rb][0], make_float2(-v0.x, -v0.y)), l[rb][0]);
+                const float2 ry = __fadd2_rn(__fadd2_rn(h[rb][1], make_float2(-v0.z, -v0.w)), l[rb][1]);
+                const float2 rz = __fadd2_rn(__fadd2_rn(h[rb][2], make_float2(-v1.x, -v1.y)), l[rb][2]);
+                const float2 qv = __ffma2_rn(make_float2(v3.x, v3.y), rz,
+                                             __ffma2_rn(make_float2(v2.z, v2.w), ry, __fmul2_rn(make_float2(v2.x, v2.y), rx)));
+                const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
+                const float2 e = kLiteral ? __fmul2_rn(nk2, tau) : __ffma2_rn(nk2, tau, make_float2(v1.z, v1.w));
+                const float2 p = make_float2(ex2_approx(e.x), ex2_approx(e.y));
+                Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
+                const uint32_t hx = __float_as_uint(p.x) & 0xFFFFE000u, hy = __float_as_uint(p.y) & 0xFFFFE000u;
+                const float2 lo = __fadd2_rn(p, make_float2(-__uint_as_float(hx), -__uint_as_float(hy)));
+                av[rb][2 * pp] = hx;
+                av[rb][2 * pp + 1] = hy;
+                av[rb][8 + 2 * pp] = __float_as_uint(lo.x);
+                av[rb][8 + 2 * pp + 1] = __float_as_uint(lo.y);
+            }
+        }
+        mbar_wait_sleep(&aempty[wg][AB], (uint32_t)(((c >> 1) & 1) ^ 1));
+        tc_fence_after();
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) tmem_st16(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16), av[rb]);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[wg][AB]);
+    };
+
+    BatchCursor cur;
+    cur.start(bp, B, u0);
+    int cur_b = -1;
+    int64_t cur_j = -1, it = 0, grp = 0, pend_g = 0;
+    int tig = 0;
+    bool pending = false;
+    for (int64_t u = u0; u < u1; ++u, cur.next(bp)) {
+        if (!serves_tc(st[cur.b])) continue;
+        if (cur.b != cur_b || cur.j != cur_j) {   // previous block fully drained and flushed at its end
+            cur_b = cur.b;
+            cur_j = cur.j;
+            load_points(cur_b, cur_j);
+        }
+        const int s = (int)(it & 3);
+        mbar_wait_sleep(&full_bar[s], (uint32_t)((it >> 2) & 1));
+        const float4* core = reinterpret_cast<const float4*>(&tiles_st[s][0]);
+        float2 Lt[RB];
+#pragma unroll
+        for (int k = 0; k < RB; ++k) Lt[k] = make_float2(0.f, 0.f);
+#pragma unroll 1
+        for (int c = 0; c < kChunks; c += 2) {
+            chunk(core, c, Lt, std::integral_constant<int, 0>());
+            chunk(core, c + 1, Lt, std::integral_constant<int, 1>());
+            if (c == 0 && pending) {
+                drain(pend_g);
+                pending = false;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[s]);
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+            const float L = Lt[rb].x + Lt[rb].y;
+            const float y = L - Ct[rb];
+            const float t = Rt[rb] + y;
+            Ct[rb] = (t - Rt[rb]) - y;
+            Rt[rb] = t;
+        }
+        const bool block_end = cur.tile + 1 == bp[cur.b].T || u + 1 == u1;
+        const bool last = tig + 1 == NT || block_end;
+        if (last) {
+            if (block_end) {
+                drain(grp);
+                flush(cur_b, cur_j);
+            } else {
+                pending = true;
+                pend_g = grp;
+            }
+            tig = 0;
+            ++grp;
+        } else {
+            ++tig;
+        }
+        ++it;
+    }
+    tc_fence_before();
+    named_bar_sync(1, kNCW * 32);
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)kTcCols)
+                     : "memory");
+    }
+}
+
 // merge: one thread per point of the concatenated record
 __global__ void estep_batch_merge_kernel(const BatchProblem* __restrict__ bp, int B, const IterState* __restrict__ st,
                                          Sched sc, const float* __restrict__ part, float* __restrict__ rec,
@@ -302,12 +648,32 @@ void batch_fill_launch(BatchProblem* bp, int B, int consistent, int* err, cudaSt
     batch_fill_kernel<<<(B + 127) / 128, 128, 0, stream>>>(bp, B, consistent, err);
 }
 
+static int batch_tc_mode() {   // LSGCPD_TC: unset / 1 = tensor cores for fixed-max problems, 0 = CUDA cores only
+    const char* e = getenv("LSGCPD_TC");
+    return e ? (atoi(e) != 0) : 1;
+}
+
 void estep_batch_launch(const BatchProblem* bp, int B, const Sched& sc, const IterState* st, float* part, float* rec,
                         int64_t Ntot, int consistent, cudaStream_t stream) {
+    const int tc = batch_tc_mode();
+    if (tc) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute((const void*)estep_batch_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kBTSmem);
+            cudaFuncSetAttribute((const void*)estep_batch_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kBTSmem);
+            attr = true;
+        }
+        if (consistent)
+            estep_batch_tc_kernel<false><<<(unsigned)sc.G, kBTThreads, kBTSmem, stream>>>(bp, B, st, sc, part);
+        else
+            estep_batch_tc_kernel<true><<<(unsigned)sc.G, kBTThreads, kBTSmem, stream>>>(bp, B, st, sc, part);
+    }
     if (consistent)
-        estep_batch_kernel<false><<<(unsigned)sc.G, (kBNCW + 1) * 32, 0, stream>>>(bp, B, st, sc, part);
+        estep_batch_kernel<false><<<(unsigned)sc.G, (kBNCW + 1) * 32, 0, stream>>>(bp, B, st, sc, part, tc);
     else
-        estep_batch_kernel<true><<<(unsigned)sc.G, (kBNCW + 1) * 32, 0, stream>>>(bp, B, st, sc, part);
+        estep_batch_kernel<true><<<(unsigned)sc.G, (kBNCW + 1) * 32, 0, stream>>>(bp, B, st, sc, part, tc);
     const int mt = 256;
     estep_batch_merge_kernel<<<(unsigned)((Ntot + mt - 1) / mt), mt, 0, stream>>>(bp, B, st, sc, part, rec, Ntot);
 }

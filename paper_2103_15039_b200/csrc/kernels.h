@@ -20,6 +20,7 @@ struct RegParams {
 struct BatchProblem {
     const void* target;        // prepared target (header + body + tensor-core section)
     const float* body;         // pair-interleaved body (CUDA-core E step)
+    const char* tc;            // tensor-core section (tensor-core E step)
     const float* src;          // [N][3]
     const float* conf;         // optional φ(x_n) [N] or NULL
     int64_t M, N, T, nblk, unit0, pt0, part0;

@@ -7,7 +7,7 @@ import pytest
 
 import oracle
 import synth
-from oracle import outlier as ol, se3
+from oracle import se3
 from tests.gpu_common import to_dev
 
 pytestmark = pytest.mark.gpu
@@ -41,22 +41,37 @@ def test_batch_matches_the_oracle_per_problem():
         _close(out["R"][b], out["t"][b], single["R"], single["t"], tgt.extent, tol=1e-5)
 
 
-def test_batch_isolates_a_failing_problem_and_supports_eta_and_confidence():
+def test_batch_isolates_a_failing_problem():
+    # a problem that loses its inlier mass stops with ENOMASS after 3 iterations; every other problem lands
+    # where its single-problem lsgcpd_register lands (that one runs the small-problem CUDA-core E step, the
+    # batch the tensor-core one: equal up to FP32 summation order)
     import paper_2103_15039_b200 as lsg
     wls = synth.make_batch(4, 600, seed=11)
-    preps = [_prep(w) for w in wls]
+    tgts = [_prep(w)[0] for w in wls]
     srcs = [w.source for w in wls]
     srcs[2] = (srcs[2] + 1e4).astype(np.float32)                     # far away: no inlier mass
-    rng = np.random.default_rng(4)
-    confs = [rng.uniform(0.3, 1.0, w.N).astype(np.float32) for w in wls]
-    out = lsg.register_batch([p[0] for p in preps], [to_dev(s) for s in srcs], 20,
-                             src_confs=[to_dev(c) for c in confs], eta=0.1, sigma2_init=1e-3)
+    out = lsg.register_batch(tgts, [to_dev(s) for s in srcs], 20, w=0.1, sigma2_init=1e-3)
     assert out["status"][2] == -5 and out["iters"][2] == 3
     for b in (0, 1, 3):
-        tgt, t64 = preps[b]
-        ora = oracle.register(t64, srcs[b], 0.0, 20, tgt.volume, tgt.extent, sigma2_0=1e-3, eta=0.1,
-                              phi_x=confs[b].astype(np.float64))
+        single = lsg.register(tgts[b], to_dev(srcs[b]), 20, w=0.1, sigma2_init=1e-3)
         assert out["status"][b] == 0 and out["iters"][b] == 20
+        _close(out["R"][b], out["t"][b], single["R"], single["t"], tgts[b].extent, tol=1e-5)
+        assert out["sigma2"][b] == pytest.approx(single["sigma2"], rel=1e-5)
+
+
+def test_batch_with_eta_and_confidence_vs_oracle():
+    import paper_2103_15039_b200 as lsg
+    wls = synth.make_batch(4, 1000, seed=11)
+    preps = [_prep(w) for w in wls]
+    rng = np.random.default_rng(4)
+    confs = [rng.uniform(0.3, 1.0, w.N).astype(np.float32) for w in wls]
+    out = lsg.register_batch([p[0] for p in preps], [to_dev(w.source) for w in wls], 30,
+                             src_confs=[to_dev(c) for c in confs], eta=0.1)
+    for b, w in enumerate(wls):
+        tgt, t64 = preps[b]
+        ora = oracle.register(t64, w.source, 0.0, 30, tgt.volume, tgt.extent, eta=0.1,
+                              phi_x=confs[b].astype(np.float64))
+        assert out["status"][b] == 0 and out["iters"][b] == 30
         _close(out["R"][b], out["t"][b], ora["R"], ora["t"], tgt.extent)
 
 

@@ -166,7 +166,9 @@ __global__ void pack_tc_kernel(const float* __restrict__ xyz, const float* __res
         const int off = kTcBOff + 1024 * s + (f / 8) * 256 + (j / 4) * 128 + (f % 8) * 16 + (j % 4) * 4;
         const float hi = tf32_rna(F[f]);
         *reinterpret_cast<float*>(base + off) = hi;              // rows 0-15 of the K-step block: F_hi
-        *reinterpret_cast<float*>(base + off + 512) = F[f] - hi; // rows 16-31: F_lo
+        // rows 16-31: F_lo = F - F_hi (exact in FP32), rounded to nearest TF32 so that the MMA (which reads
+        // TF32 operands truncated) sees it exactly: no truncation bias on the lo product
+        *reinterpret_cast<float*>(base + off + 512) = tf32_rna(F[f] - hi);
     }
 }
 

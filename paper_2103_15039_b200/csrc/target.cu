@@ -11,6 +11,23 @@ namespace lsg {
 constexpr int kRedThreads = 256;
 constexpr int kRedBlocks = 148;
 constexpr int kMaxK = 32;
+#ifndef LSG_KNN_COARSE
+#define LSG_KNN_COARSE 4
+#endif
+#ifndef LSG_KNN_RMAX
+#define LSG_KNN_RMAX 4
+#endif
+#ifndef LSG_KNN_FINE
+#define LSG_KNN_FINE 4
+#endif
+// Grid sizing (tools/prep_speed.py, round 1, ms on one B200 — object / rgbd / lidar / scale):
+//   one grid, cell = (AABB volume / M)^{1/3}:                 0.5 / 101.9 / 38.4 / 3.6
+//   + a 4× coarser fallback grid after 4 fine rings:          0.5 /   3.5 / 36.4 / 3.6
+//   + fine cell a quarter of that (the default):              1.0 /   3.8 / 27.3 / 2.3
+// The AABB-volume estimate is far too coarse for surface clouds with outliers (rgbd, lidar), whose
+// isolated points then scanned O(r³) cells; LiDAR's remaining cost is its near-sensor density.
+constexpr int kCoarse = LSG_KNN_COARSE;         // coarse cell = kCoarse³ fine cells
+constexpr int kFineRings = LSG_KNN_RMAX;        // fine rings searched before the coarse grid takes over
 
 // ---- reductions over the raw cloud -------------------------------------------------------------
 // stats1: [max(-x), max(-y), max(-z), max x, max y, max z, Σx, Σy, Σz]
@@ -238,22 +255,18 @@ __device__ inline void jacobi3(double A[3][3], double V[3][3]) {
     }
 }
 
-__global__ void __launch_bounds__(128)
-    knn_surface_kernel(const float* __restrict__ xyz, int64_t M, Grid g, const int* __restrict__ sids,
-                       const int* __restrict__ cstart, const int* __restrict__ cend, int k, float alpha_max,
-                       float lambda, float* __restrict__ nrm_out, float* __restrict__ kappa_out,
-                       float* __restrict__ alpha_out, int* __restrict__ knn_out, float* __restrict__ nnd_out,
-                       int* __restrict__ degen_out) {
-    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= M) return;
-    const double p0 = xyz[3 * m], p1 = xyz[3 * m + 1], p2 = xyz[3 * m + 2];
+// Exact k nearest neighbours of p (self included, ties → lower id) by ring search over the cells of `g`:
+// rings r = 0, 1, … until the k-th distance is below the distance to the unsearched region.  Gives up
+// (returns false) after ring rmax; the caller then restarts on a coarser grid.
+__device__ __forceinline__ bool ring_search(const float* __restrict__ xyz, double p0, double p1, double p2,
+                                            const Grid& g, const int* __restrict__ sids,
+                                            const int* __restrict__ cstart, const int* __restrict__ cend, int k,
+                                            int rmax, double* bd, int* bi, int& cnt) {
     const int c0 = cell_coord(p0, g.lo[0], g.h, g.dim[0]);
     const int c1 = cell_coord(p1, g.lo[1], g.h, g.dim[1]);
     const int c2 = cell_coord(p2, g.lo[2], g.h, g.dim[2]);
-    double bd[kMaxK];
-    int bi[kMaxK];
-    int cnt = 0;
-    for (int r = 0;; ++r) {
+    cnt = 0;
+    for (int r = 0; r <= rmax; ++r) {
         const int x0 = c0 - r, x1 = c0 + r, y0 = c1 - r, y1 = c1 + r, z0 = c2 - r, z1 = c2 + r;
         for (int cx = max(x0, 0); cx <= min(x1, g.dim[0] - 1); ++cx)
             for (int cy = max(y0, 0); cy <= min(y1, g.dim[1] - 1); ++cy) {
@@ -297,9 +310,31 @@ __global__ void __launch_bounds__(128)
                 all_covered = false;
             }
         }
-        if (all_covered) break;
-        if (cnt == k && bd[k - 1] < bound * bound) break;
+        if (all_covered) return true;
+        if (cnt == k && bd[k - 1] < bound * bound) return true;
     }
+    return false;
+}
+
+// Two grids: the fine one (≈ one point per cell for a volume-filling cloud) serves dense regions in ≤ 3
+// rings; points in sparse regions (isolated outliers, far LiDAR returns) restart on a grid 4× coarser
+// instead of scanning O(r³) fine cells.  Both searches are exact, so the result does not depend on which
+// one finished.
+__global__ void __launch_bounds__(128)
+    knn_surface_kernel(const float* __restrict__ xyz, int64_t M, Grid g, const int* __restrict__ sids,
+                       const int* __restrict__ cstart, const int* __restrict__ cend, Grid gc,
+                       const int* __restrict__ sids_c, const int* __restrict__ cstart_c,
+                       const int* __restrict__ cend_c, int k, float alpha_max, float lambda,
+                       float* __restrict__ nrm_out, float* __restrict__ kappa_out, float* __restrict__ alpha_out,
+                       int* __restrict__ knn_out, float* __restrict__ nnd_out, int* __restrict__ degen_out) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    const double p0 = xyz[3 * m], p1 = xyz[3 * m + 1], p2 = xyz[3 * m + 2];
+    double bd[kMaxK];
+    int bi[kMaxK];
+    int cnt = 0;
+    if (!ring_search(xyz, p0, p1, p2, g, sids, cstart, cend, k, kFineRings, bd, bi, cnt))
+        ring_search(xyz, p0, p1, p2, gc, sids_c, cstart_c, cend_c, k, 1 << 20, bd, bi, cnt);
     // neighbour ids, nearest other point distance
     double nn = 0.0;
     for (int i = 0; i < k; ++i) {
@@ -356,9 +391,11 @@ __global__ void __launch_bounds__(128)
 struct PrepLayout {
     size_t blockpart, stats1, stats2, counter, keys, ids, skeys, sids, cstart, cend, nrm, kappa, alpha, nnd,
         degen, cub_tmp, cub_bytes, total;
+    size_t skeys_c, sids_c, cstart_c, cend_c;   // the 4× coarser grid of the kNN search
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int64_t kMaxCells = 1 << 22;
+constexpr int64_t kMaxCellsCoarse = 2 * kMaxCells / (kCoarse * kCoarse * kCoarse);   // with rounding slack
 
 static size_t cub_sort_bytes(int64_t M) {
     size_t bytes = 0;
@@ -386,10 +423,15 @@ static PrepLayout prep_layout(int64_t M, bool with_knn) {
         L.sids = o; o += al(sizeof(int) * M);
         L.cstart = o; o += al(sizeof(int) * kMaxCells);
         L.cend = o; o += al(sizeof(int) * kMaxCells);
+        L.skeys_c = o; o += al(sizeof(int) * M);
+        L.sids_c = o; o += al(sizeof(int) * M);
+        L.cstart_c = o; o += al(sizeof(int) * kMaxCellsCoarse);
+        L.cend_c = o; o += al(sizeof(int) * kMaxCellsCoarse);
         L.cub_bytes = cub_sort_bytes(M);
         L.cub_tmp = o; o += al(L.cub_bytes);
     } else {
         L.keys = L.ids = L.skeys = L.sids = L.cstart = L.cend = L.cub_tmp = L.cub_bytes = 0;
+        L.skeys_c = L.sids_c = L.cstart_c = L.cend_c = 0;
     }
     L.total = o;
     return L;
@@ -466,7 +508,7 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     }
     LSG_CHECK(maxe > 0.0 && isfinite(maxe), LSGCPD_EDEGENERATE, "degenerate target: all points coincide");
     const double floor_e = maxe * 1e-3;
-    double h = cbrt(fmax(ext[0], floor_e) * fmax(ext[1], floor_e) * fmax(ext[2], floor_e) / (double)M);
+    double h = cbrt(fmax(ext[0], floor_e) * fmax(ext[1], floor_e) * fmax(ext[2], floor_e) / (double)M) / LSG_KNN_FINE;
     for (;;) {
         int64_t cells = 1;
         for (int a = 0; a < 3; ++a) {
@@ -491,15 +533,32 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     LSG_CUDA(cudaMemsetAsync(cstart, 0xff, sizeof(int) * ncells, stream));
     LSG_CUDA(cudaMemsetAsync(cend, 0xff, sizeof(int) * ncells, stream));
     cell_ranges_kernel<<<nb, 256, 0, stream>>>(skeys, M, cstart, cend);
+    // the coarse grid (keys and ids scratch reused: the fine sort has consumed them)
+    Grid gc = g;
+    gc.h = g.h * kCoarse;
+    for (int a = 0; a < 3; ++a) gc.dim[a] = (g.dim[a] + kCoarse - 1) / kCoarse;
+    int* skeys_c = reinterpret_cast<int*>(ws + L.skeys_c);
+    int* sids_c = reinterpret_cast<int*>(ws + L.sids_c);
+    int* cstart_c = reinterpret_cast<int*>(ws + L.cstart_c);
+    int* cend_c = reinterpret_cast<int*>(ws + L.cend_c);
+    cell_keys_kernel<<<nb, 256, 0, stream>>>(d_xyz, M, gc, keys, ids);
+    cub_bytes = L.cub_bytes;
+    LSG_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.cub_tmp, cub_bytes, keys, skeys_c, ids, sids_c, (int)M, 0, 22,
+                                             stream));
+    const int64_t ncells_c = (int64_t)gc.dim[0] * gc.dim[1] * gc.dim[2];
+    LSG_CHECK(ncells_c <= kMaxCellsCoarse, LSGCPD_EINVAL, "coarse grid too large (%lld cells)", (long long)ncells_c);
+    LSG_CUDA(cudaMemsetAsync(cstart_c, 0xff, sizeof(int) * ncells_c, stream));
+    LSG_CUDA(cudaMemsetAsync(cend_c, 0xff, sizeof(int) * ncells_c, stream));
+    cell_ranges_kernel<<<nb, 256, 0, stream>>>(skeys_c, M, cstart_c, cend_c);
     float* nrm = ann && ann->d_normals ? ann->d_normals : reinterpret_cast<float*>(ws + L.nrm);
     float* kap = ann && ann->d_kappa ? ann->d_kappa : reinterpret_cast<float*>(ws + L.kappa);
     float* alp = ann && ann->d_alpha ? ann->d_alpha : reinterpret_cast<float*>(ws + L.alpha);
     int* knn = ann ? ann->d_knn : nullptr;
     float* nnd = reinterpret_cast<float*>(ws + L.nnd);
     int* degen = reinterpret_cast<int*>(ws + L.degen);
-    knn_surface_kernel<<<(unsigned)((M + 127) / 128), 128, 0, stream>>>(d_xyz, M, g, sids, cstart, cend, p.knn_k,
-                                                                        p.alpha_max, p.lambda, nrm, kap, alp, knn,
-                                                                        nnd, degen);
+    knn_surface_kernel<<<(unsigned)((M + 127) / 128), 128, 0, stream>>>(d_xyz, M, g, sids, cstart, cend, gc, sids_c,
+                                                                        cstart_c, cend_c, p.knn_k, p.alpha_max,
+                                                                        p.lambda, nrm, kap, alp, knn, nnd, degen);
     LSG_CUDA(cudaGetLastError());
     return finish_target(d_xyz, nrm, alp, nnd, degen, M, p.volume_margin, ws, L, d_target, info, stream);
 }

@@ -72,6 +72,70 @@ void run(int warps, const float4* gt, float* out, long long* cyc, int nsm) {
            pairs / avg, pairs / avg * 1.965e9 * nsm, nsm);
 }
 
+
+// Variant: f32x2 over TWO SOURCE POINTS per instruction with the target's fields broadcast (the
+// CUDA-core kernel's packing), RBP point pairs per thread; same per-pair math as mode 0.
+template <int RBP>
+__global__ void pairloop_pts(const float4* __restrict__ gt, float* out, long long* cyc, float k2) {
+    __shared__ float4 core[kTgt / 2 * 4];
+    for (int i = threadIdx.x; i < kTgt / 2 * 4; i += blockDim.x) core[i] = gt[i];
+    __syncthreads();
+    float2 h[RBP][3], l[RBP][3];
+    for (int rb = 0; rb < RBP; ++rb)
+        for (int a = 0; a < 3; ++a) {
+            h[rb][a] = make_float2(0.01f * (threadIdx.x % 7 + a + rb), 0.011f * (threadIdx.x % 5 + a));
+            l[rb][a] = make_float2(1e-9f * a, 2e-9f * a);
+        }
+    float2 Lt[RBP];
+    for (int rb = 0; rb < RBP; ++rb) Lt[rb] = make_float2(0.f, 0.f);
+    unsigned sink = 0;
+    const float2 nk2 = bc(-k2);
+    long long t0 = clock64();
+    for (int rep = 0; rep < kReps; ++rep) {
+#pragma unroll 2
+        for (int pr = 0; pr < kTgt / 2; ++pr) {
+            const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
+#pragma unroll
+            for (int ts = 0; ts < 2; ++ts) {   // the two targets of the pair block
+                const float y0 = ts ? v0.y : v0.x, y1 = ts ? v0.w : v0.z, y2 = ts ? v1.y : v1.x, om = ts ? v1.w : v1.z;
+                const float n0 = ts ? v2.y : v2.x, n1 = ts ? v2.w : v2.z, n2 = ts ? v3.y : v3.x;
+#pragma unroll
+                for (int rb = 0; rb < RBP; ++rb) {
+                    const float2 rx = __fadd2_rn(__fadd2_rn(h[rb][0], bc(-y0)), l[rb][0]);
+                    const float2 ry = __fadd2_rn(__fadd2_rn(h[rb][1], bc(-y1)), l[rb][1]);
+                    const float2 rz = __fadd2_rn(__fadd2_rn(h[rb][2], bc(-y2)), l[rb][2]);
+                    const float2 qv = __ffma2_rn(bc(n2), rz, __ffma2_rn(bc(n1), ry, __fmul2_rn(bc(n0), rx)));
+                    const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
+                    const float2 e = __ffma2_rn(nk2, tau, bc(om));
+                    const float2 p = make_float2(ex2a(e.x), ex2a(e.y));
+                    Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
+                    const unsigned hx = __float_as_uint(p.x) & 0xFFFFE000u, hy = __float_as_uint(p.y) & 0xFFFFE000u;
+                    const float2 lo = __fadd2_rn(p, make_float2(-__uint_as_float(hx), -__uint_as_float(hy)));
+                    sink ^= hx ^ hy ^ __float_as_uint(lo.x) ^ __float_as_uint(lo.y);
+                }
+            }
+        }
+    }
+    long long t1 = clock64();
+    float s = 0.f;
+    for (int rb = 0; rb < RBP; ++rb) s += Lt[rb].x + Lt[rb].y;
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s + (float)(sink & 1);
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int RBP>
+void run_pts(int warps, const float4* gt, float* out, long long* cyc, int nsm) {
+    const int thr = warps * 32;
+    for (int r = 0; r < 2; ++r) { pairloop_pts<RBP><<<nsm, thr>>>(gt, out, cyc, 721.f); cudaDeviceSynchronize(); }
+    long long c[1024];
+    cudaMemcpy(c, cyc, nsm * sizeof(long long), cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < nsm; ++i) avg += c[i];
+    avg /= nsm;
+    const double pairs = (double)thr * 2 * RBP * kTgt * kReps;
+    printf("points-packed RBP=%d warps=%2d  %.3f pairs/clk/SM\n", RBP, warps, pairs / avg);
+}
+
 int main() {
     int nsm;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -87,5 +151,7 @@ int main() {
     for (int w : {8, 12, 16}) run<4, 0>(w, gt, out, cyc, nsm);
     for (int w : {12, 16}) run<2, 1>(w, gt, out, cyc, nsm);
     for (int w : {12, 16}) run<2, 2>(w, gt, out, cyc, nsm);
+    for (int w : {12, 16}) run_pts<1>(w, gt, out, cyc, nsm);
+    for (int w : {8, 12}) run_pts<2>(w, gt, out, cyc, nsm);
     return 0;
 }

@@ -195,7 +195,8 @@ int lsgcpd_comm_destroy(void* comm);
  * target; all ranks return bit-identical R, t, σ².  volume ≤ 0 uses the target's V.
  * Optional host traces (may be NULL): nll_trace[max_iters] (NLL at each E step, Eq. 4),
  * sigma2_trace[max_iters+1] (σ²_0 … σ²_k).  sync.
- * Errors: EINVAL, ECUDA, ENCCL, ENOMASS (results still written). */
+ * Errors: EINVAL (also for a non-finite source coordinate, detected by the σ²₀ reduction), ECUDA,
+ * ENCCL, ENOMASS (results still written). */
 size_t lsgcpd_register_workspace_bytes(int64_t M, int64_t N_local, int max_iters);
 int lsgcpd_register(const void* d_target, int64_t M, double volume, const float* d_src_local,
                     int64_t N_local, const lsgcpd_em_params* params, const double R0[9],

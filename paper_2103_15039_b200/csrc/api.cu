@@ -503,6 +503,10 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
         set_error("no inlier mass (sum P <= 1e-12 N) for 3 consecutive iterations");
         return LSGCPD_ENOMASS;
     }
+    if (fin.status == LSGCPD_EINVAL) {
+        set_error("non-finite coordinate in the source cloud");
+        return LSGCPD_EINVAL;
+    }
     return 0;
 }
 

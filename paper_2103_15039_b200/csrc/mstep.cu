@@ -127,6 +127,10 @@ __global__ void sigma2_init_kernel(IterState* st, const TargetHeader* hdr, const
     s.status = 0;
     s.no_mass = 0;
     s.last_step_rot = s.last_step_trans = 0.0;
+    if (!isfinite(sums[0])) {   // a non-finite source coordinate: nothing to register (EINVAL on the host)
+        s.status = LSGCPD_EINVAL;
+        s.active = 0;
+    }
     *st = s;
     sigma2_trace[0] = s2;
     *ntot_out = N;

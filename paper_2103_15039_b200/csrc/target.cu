@@ -469,7 +469,8 @@ static int finish_target(const float* d_xyz, const float* nrm, const float* alph
         info->alpha_mean = h.alpha_sum / (double)M;
         info->n_degenerate = h.n_degenerate;
     }
-    LSG_CHECK(isfinite(h.extent), LSGCPD_EINVAL, "non-finite coordinate in the target cloud");
+    LSG_CHECK(isfinite(h.extent) && isfinite(h.ybar[0]) && isfinite(h.ybar[1]) && isfinite(h.ybar[2]), LSGCPD_EINVAL,
+              "non-finite coordinate in the target cloud");
     LSG_CHECK(h.extent > 0.0 || nnd == nullptr, LSGCPD_EDEGENERATE, "degenerate target: all points coincide");
     LSG_CHECK(isfinite(h.volume) && h.volume > 0.0, LSGCPD_EDEGENERATE, "degenerate target: zero working volume");
     return 0;
@@ -506,7 +507,10 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
         ext[a] = s1[3 + a] + s1[a];
         maxe = fmax(maxe, ext[a]);
     }
-    LSG_CHECK(maxe > 0.0 && isfinite(maxe), LSGCPD_EDEGENERATE, "degenerate target: all points coincide");
+    // fmax/fmin skip NaN, so a NaN coordinate shows only in the coordinate sums
+    LSG_CHECK(isfinite(s1[6]) && isfinite(s1[7]) && isfinite(s1[8]) && isfinite(maxe), LSGCPD_EINVAL,
+              "non-finite coordinate in the target cloud");
+    LSG_CHECK(maxe > 0.0, LSGCPD_EDEGENERATE, "degenerate target: all points coincide");
     const double floor_e = maxe * 1e-3;
     double h = cbrt(fmax(ext[0], floor_e) * fmax(ext[1], floor_e) * fmax(ext[2], floor_e) / (double)M) / LSG_KNN_FINE;
     for (;;) {

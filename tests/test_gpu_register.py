@@ -97,3 +97,29 @@ def test_register_no_mass_and_invalid():
     assert out["status"] == -5 and out["iters"] == 3
     with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
         lsg.register(tgt, to_dev(wl.source), 5, w=1.0)
+
+
+def test_register_degenerate_and_minimal_inputs():
+    # SURVEY §4 fault injection: non-finite coordinates → EINVAL; collinear target (two zero-extent axes)
+    # prepares with the floored volume; the minimal problem (M = 3 with k = 3, N = 1) runs
+    import paper_2103_15039_b200 as lsg
+    wl = workload("tiny")
+    bad = wl.target.copy()
+    bad[5, 1] = np.nan
+    with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
+        lsg.prepare_target(to_dev(bad), wl.knn_k)
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    src = wl.source.copy()
+    src[7, 2] = np.inf
+    with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
+        lsg.register(tgt, to_dev(src), 5, w=wl.w)
+    line = np.stack([np.linspace(0, 1, 40), np.zeros(40), np.zeros(40)], axis=1).astype(np.float32)
+    lt = lsg.prepare_target(to_dev(line), 10)
+    V, _ = oracle.working_volume(line)
+    assert lt.volume == pytest.approx(V, rel=1e-6)
+    out = lsg.register(lt, to_dev(line[:20] + np.float32(0.01)), 10, w=0.1)
+    assert out["status"] == 0 and np.all(np.isfinite(out["R"]))
+    tri = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], np.float32)
+    t3 = lsg.prepare_target(to_dev(tri), 3)
+    one = lsg.register(t3, to_dev(np.array([[0.3, 0.3, 0.05]], np.float32)), 5, w=0.1)
+    assert one["iters"] == 5 and np.all(np.isfinite(one["t"]))

@@ -6,6 +6,8 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for Nsight / ncu --nvtx
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -54,6 +56,12 @@ static bool is_affine_linear(const double* A) {
     return det > 0.0;
 }
 static bool pose_ok(const double* R, int group) { return group ? is_affine_linear(R) : is_rotation(R); }
+
+// RAII NVTX range (SURVEY §5 tracing): one per public call and per registration phase
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -237,6 +245,7 @@ LSG_EXPORT int lsgcpd_prepare_target(const float* d_xyz, int64_t M, const lsgcpd
     LSG_CHECK(isfinite(p.volume_margin) && p.volume_margin >= 0.0, LSGCPD_EINVAL, "volume_margin must be >= 0");
     LSG_CHECK(ws_bytes >= prepare_ws_bytes(M), LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes,
               prepare_ws_bytes(M));
+    NvtxRange r("lsgcpd_prepare_target");
     return prepare_target_impl(d_xyz, M, p, d_target, d_ws, h_info, annotations, (cudaStream_t)stream);
 }
 
@@ -315,6 +324,7 @@ static int estep_impl(const void* d_target, int64_t M, const float* d_src, int64
         if (rc) return rc;
         LSG_CHECK(!h.prior, LSGCPD_EINVAL, "component priors require consistent_normalizer = 1");
     }
+    NvtxRange r("lsgcpd_estep");
     char* ws = static_cast<char*>(d_ws);
     IterState* st = reinterpret_cast<IterState*>(ws + L.state);
     estep_launch_setup(st, d_target, R, t, sigma2, w, volume, M, consistent_normalizer ? 1 : 0, eta, s);
@@ -416,6 +426,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
         if (rc) return rc;
     }
 
+    NvtxRange r("lsgcpd_register");
     char* ws = static_cast<char*>(d_ws);
     IterState* st = reinterpret_cast<IterState*>(ws + L.state);
     double* mom = reinterpret_cast<double*>(ws + L.mom);
@@ -451,6 +462,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     LSG_CUDA(cudaGetLastError());
 
     // EM iterations: captured once into a CUDA graph and replayed (no host sync per iteration)
+    NvtxRange rem("EM iterations");
     const char* env = getenv("LSGCPD_NO_GRAPH");
     const bool use_graph = p.max_iters > 1 && !(env && env[0] == '1');
     if (use_graph) {
@@ -676,6 +688,7 @@ LSG_EXPORT int lsgcpd_register_batch(const lsgcpd_problem* h_problems, int B, co
     if (rc) return rc;
     LSG_CHECK(ws_bytes >= L.total, LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes, L.total);
     cudaStream_t s = (cudaStream_t)stream;
+    NvtxRange r("lsgcpd_register_batch");
     char* ws = static_cast<char*>(d_ws);
     BatchProblem* dbp = reinterpret_cast<BatchProblem*>(ws + L.desc);
     IterState* st = reinterpret_cast<IterState*>(ws + L.st);

@@ -123,3 +123,18 @@ def test_register_degenerate_and_minimal_inputs():
     t3 = lsg.prepare_target(to_dev(tri), 3)
     one = lsg.register(t3, to_dev(np.array([[0.3, 0.3, 0.05]], np.float32)), 5, w=0.1)
     assert one["iters"] == 5 and np.all(np.isfinite(one["t"]))
+
+
+def test_register_tolerance_stops_early_and_matches_a_fixed_count():
+    # tol > 0 (lsgcpd_em_params.tol): stop once |Δσ²|/σ² and the pose step fall below tol; the result is
+    # exactly the fixed-count registration with that many iterations (the stop only deactivates the loop)
+    import paper_2103_15039_b200 as lsg
+    wl = workload("tiny")
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    X = to_dev(wl.source)
+    early = lsg.register(tgt, X, 200, w=wl.w, tol=1e-3)
+    assert 1 < early["iters"] < 200 and early["status"] == 0
+    fixed = lsg.register(tgt, X, early["iters"], w=wl.w)
+    np.testing.assert_array_equal(early["R"], fixed["R"])
+    np.testing.assert_array_equal(early["t"], fixed["t"])
+    assert early["sigma2"] == fixed["sigma2"]

@@ -143,3 +143,34 @@ def test_estep_tensor_core_and_cuda_core_paths(tc, monkeypatch):
         for w, s2 in ((wl.w, 1e-3), (wl.w, 1e-5), (0.0, 1e-4)):
             rec, ora = _run_pair(wl.target, n32, a32, wl.source, wl.R_expected, wl.t_expected, s2, w, V)
             assert_record_parity(rec, ora, wl.target, a32, what=f"tc={tc} {name} w={w} s2={s2}")
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_estep_literal_normaliser_on_both_paths(tc, monkeypatch):
+    # Eq. 9-10 literal normaliser (reading R1, consistent = 0) through the tensor-core kernel's kLiteral
+    # instantiation (forced) and the CUDA-core one, at a size with many tiles and a ragged tail
+    monkeypatch.setenv("LSGCPD_TC", tc)
+    wl, n32, a32, V, ext = oracle_target32("object")
+    for s2 in (1e-3, 1e-5):
+        rec, ora = _run_pair(wl.target, n32, a32, wl.source, wl.R_expected, wl.t_expected, s2, wl.w, V, False)
+        assert_record_parity(rec, ora, wl.target, a32, what=f"literal tc={tc} s2={s2}")
+
+
+def test_estep_running_max_path_sampled_at_full_size():
+    # w = 0 (pure softmax: the per-point running-max CUDA-core kernel) at the rgbd config's full size
+    import paper_2103_15039_b200 as lsg
+    wl = workload("rgbd")
+    rng = np.random.default_rng(12)
+    Y = wl.target
+    n = rng.standard_normal(Y.shape)
+    n32 = (n / np.linalg.norm(n, axis=1, keepdims=True)).astype(np.float32)
+    a32 = rng.uniform(0, 50, Y.shape[0]).astype(np.float32)
+    V, _ = oracle.working_volume(Y)
+    tgt = _gpu_target(Y, n32, a32)
+    idx = np.sort(rng.choice(wl.N, 128, replace=False))
+    for s2 in (1e-2, 1e-4):
+        rec = lsg.estep(tgt, to_dev(wl.source), wl.R_expected, wl.t_expected, s2, 0.0, V).cpu().numpy()[idx]
+        ora = oracle.estep(Y, n32.astype(np.float64), a32.astype(np.float64), wl.source[idx], wl.R_expected,
+                           wl.t_expected, s2, 0.0, V)
+        assert_record_parity(rec, ora, Y, a32, what=f"rgbd w=0 s2={s2}")
+        np.testing.assert_allclose(rec[:, 0], 1.0, atol=2e-6)

@@ -226,8 +226,9 @@ typedef struct {
 /* Workspace for B problems (depends on every problem's M and N).  0 on invalid sizes. */
 size_t lsgcpd_register_batch_workspace_bytes(const lsgcpd_problem* h_problems, int B, int max_iters);
 /* sync.  Outputs (HOST, B entries each): R_out [B][9], t_out [B][3], sigma2_out, iters_out,
- * status_out (0, or LSGCPD_ENOMASS for a problem that lost its inlier mass; the others are
- * unaffected).  params->d_src_conf is ignored (per-problem d_src_conf is used).
+ * status_out (0; LSGCPD_ENOMASS for a problem that lost its inlier mass; LSGCPD_EINVAL for a
+ * problem whose source holds a non-finite coordinate, which is not iterated; the others are
+ * unaffected either way).  params->d_src_conf is ignored (per-problem d_src_conf is used).
  * Errors: EINVAL (null, B < 1, bad sizes, bad target / priors with the literal form, bad
  * params, ws too small), ECUDA. */
 int lsgcpd_register_batch(const lsgcpd_problem* h_problems, int B, const lsgcpd_em_params* params,

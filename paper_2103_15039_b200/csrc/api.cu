@@ -63,6 +63,20 @@ struct NvtxRange {
     ~NvtxRange() { nvtxRangePop(); }
 };
 
+// Owns the capture stream, event, graph and executable of one EM-loop replay; released on every exit path.
+struct GraphRun {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ~GraphRun() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        if (ev) cudaEventDestroy(ev);
+        if (cs) cudaStreamDestroy(cs);
+    }
+};
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -466,28 +480,21 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     const char* env = getenv("LSGCPD_NO_GRAPH");
     const bool use_graph = p.max_iters > 1 && !(env && env[0] == '1');
     if (use_graph) {
-        cudaGraph_t graph;
-        cudaGraphExec_t exec;
-        cudaStream_t cs;
-        LSG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        cudaEvent_t ev;
-        LSG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        LSG_CUDA(cudaEventRecord(ev, s));
-        LSG_CUDA(cudaStreamWaitEvent(cs, ev, 0));
-        LSG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        rc = enqueue_iteration(d_target, d_src_local, N_local, ws, L, sc, rp, c, cs);
-        cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        GraphRun g;
+        LSG_CUDA(cudaStreamCreateWithFlags(&g.cs, cudaStreamNonBlocking));
+        LSG_CUDA(cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming));
+        LSG_CUDA(cudaEventRecord(g.ev, s));
+        LSG_CUDA(cudaStreamWaitEvent(g.cs, g.ev, 0));
+        LSG_CUDA(cudaStreamBeginCapture(g.cs, cudaStreamCaptureModeThreadLocal));
+        rc = enqueue_iteration(d_target, d_src_local, N_local, ws, L, sc, rp, c, g.cs);
+        cudaError_t ce = cudaStreamEndCapture(g.cs, &g.graph);
         if (rc) return rc;
         if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
-        LSG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-        for (int k = 0; k < p.max_iters; ++k) LSG_CUDA(cudaGraphLaunch(exec, cs));
-        LSG_CUDA(cudaEventRecord(ev, cs));
-        LSG_CUDA(cudaStreamWaitEvent(s, ev, 0));
+        LSG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
+        for (int k = 0; k < p.max_iters; ++k) LSG_CUDA(cudaGraphLaunch(g.exec, g.cs));
+        LSG_CUDA(cudaEventRecord(g.ev, g.cs));
+        LSG_CUDA(cudaStreamWaitEvent(s, g.ev, 0));
         LSG_CUDA(cudaStreamSynchronize(s));
-        cudaGraphExecDestroy(exec);
-        cudaGraphDestroy(graph);
-        cudaEventDestroy(ev);
-        cudaStreamDestroy(cs);
     } else {
         for (int k = 0; k < p.max_iters; ++k) {
             rc = enqueue_iteration(d_target, d_src_local, N_local, ws, L, sc, rp, c, s);
@@ -729,27 +736,20 @@ LSG_EXPORT int lsgcpd_register_batch(const lsgcpd_problem* h_problems, int B, co
                             reinterpret_cast<double*>(ws + L.sig2), reinterpret_cast<int*>(ws + L.iters), q);
     };
     if (p.max_iters > 0) {
-        cudaGraph_t graph;
-        cudaGraphExec_t exec;
-        cudaStream_t cs;
-        LSG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-        cudaEvent_t ev;
-        LSG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        LSG_CUDA(cudaEventRecord(ev, s));
-        LSG_CUDA(cudaStreamWaitEvent(cs, ev, 0));
-        LSG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        enqueue(cs);
-        cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        GraphRun g;
+        LSG_CUDA(cudaStreamCreateWithFlags(&g.cs, cudaStreamNonBlocking));
+        LSG_CUDA(cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming));
+        LSG_CUDA(cudaEventRecord(g.ev, s));
+        LSG_CUDA(cudaStreamWaitEvent(g.cs, g.ev, 0));
+        LSG_CUDA(cudaStreamBeginCapture(g.cs, cudaStreamCaptureModeThreadLocal));
+        enqueue(g.cs);
+        cudaError_t ce = cudaStreamEndCapture(g.cs, &g.graph);
         if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
-        LSG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-        for (int k = 0; k < p.max_iters; ++k) LSG_CUDA(cudaGraphLaunch(exec, cs));
-        LSG_CUDA(cudaEventRecord(ev, cs));
-        LSG_CUDA(cudaStreamWaitEvent(s, ev, 0));
+        LSG_CUDA(cudaGraphInstantiate(&g.exec, g.graph, 0));
+        for (int k = 0; k < p.max_iters; ++k) LSG_CUDA(cudaGraphLaunch(g.exec, g.cs));
+        LSG_CUDA(cudaEventRecord(g.ev, g.cs));
+        LSG_CUDA(cudaStreamWaitEvent(s, g.ev, 0));
         LSG_CUDA(cudaStreamSynchronize(s));
-        cudaGraphExecDestroy(exec);
-        cudaGraphDestroy(graph);
-        cudaEventDestroy(ev);
-        cudaStreamDestroy(cs);
     }
     std::vector<IterState> fin(B);
     LSG_CUDA(cudaMemcpyAsync(fin.data(), st, sizeof(IterState) * B, cudaMemcpyDeviceToHost, s));
@@ -760,7 +760,7 @@ LSG_EXPORT int lsgcpd_register_batch(const lsgcpd_problem* h_problems, int B, co
         for (int i = 0; i < 9; ++i) R_out[9 * b + i] = fin[b].R[i];
         for (int i = 0; i < 3; ++i) t_out[3 * b + i] = fin[b].t[i];
         sigma2_out[b] = fin[b].sigma2;
-        status_out[b] = fin[b].status == LSGCPD_ENOMASS ? LSGCPD_ENOMASS : 0;
+        status_out[b] = (fin[b].status == LSGCPD_ENOMASS || fin[b].status == LSGCPD_EINVAL) ? fin[b].status : 0;
     }
     return 0;
 }

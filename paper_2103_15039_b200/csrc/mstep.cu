@@ -549,6 +549,10 @@ __global__ void __launch_bounds__(kMomThreads)
     s.status = 0;
     s.no_mass = 0;
     s.last_step_rot = s.last_step_trans = 0.0;
+    if (!isfinite(sx)) {   // a non-finite source coordinate: this problem is refused (EINVAL in status_out)
+        s.status = LSGCPD_EINVAL;
+        s.active = 0;
+    }
     st[b] = s;
     mom[(int64_t)b * kBatchMom + 75] = N;
     sigma2_trace[(int64_t)b * (rp0.max_iters + 2)] = s2;

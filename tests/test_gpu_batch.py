@@ -42,7 +42,8 @@ def test_batch_matches_the_oracle_per_problem():
 
 
 def test_batch_isolates_a_failing_problem():
-    # a problem that loses its inlier mass stops with ENOMASS after 3 iterations; every other problem lands
+    # a problem that loses its inlier mass stops with ENOMASS after 3 iterations, one with a NaN source is
+    # refused with EINVAL; every other problem lands
     # where its single-problem lsgcpd_register lands (that one runs the small-problem CUDA-core E step, the
     # batch the tensor-core one: equal up to FP32 summation order)
     import paper_2103_15039_b200 as lsg
@@ -50,9 +51,12 @@ def test_batch_isolates_a_failing_problem():
     tgts = [_prep(w)[0] for w in wls]
     srcs = [w.source for w in wls]
     srcs[2] = (srcs[2] + 1e4).astype(np.float32)                     # far away: no inlier mass
+    srcs[1] = srcs[1].copy()
+    srcs[1][17, 0] = np.nan                                          # refused: EINVAL, never iterated
     out = lsg.register_batch(tgts, [to_dev(s) for s in srcs], 20, w=0.1, sigma2_init=1e-3)
     assert out["status"][2] == -5 and out["iters"][2] == 3
-    for b in (0, 1, 3):
+    assert out["status"][1] == -1 and out["iters"][1] == 0
+    for b in (0, 3):
         single = lsg.register(tgts[b], to_dev(srcs[b]), 20, w=0.1, sigma2_init=1e-3)
         assert out["status"][b] == 0 and out["iters"][b] == 20
         _close(out["R"][b], out["t"][b], single["R"], single["t"], tgts[b].extent, tol=1e-5)

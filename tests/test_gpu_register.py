@@ -64,16 +64,24 @@ def test_register_noiseless_exact_recovery():
         _close(gpu["R"], gpu["t"], wl.R_expected, wl.t_expected, tgt.extent, tol=1e-5)
 
 
-def test_register_object_vs_golden():
+@pytest.mark.parametrize("name", ["object", "rgbd", "lidar"])
+def test_register_full_size_vs_golden(name):
+    # whole registrations at BASELINE.json's full sizes, GPU-prepared target, against the FP64 oracle's own
+    # full pipeline (prepare → V → σ²₀ → EM), run offline by oracle/make_golden.py (oracle only)
     import paper_2103_15039_b200 as lsg
-    path = os.path.join(GOLDEN, "object_oracle.json")
+    from oracle.make_golden import digest
+    path = os.path.join(GOLDEN, f"{name}_oracle.json")
     if not os.path.exists(path):
         pytest.skip("golden not generated")
     g = json.load(open(path))
-    wl = workload("object")
+    wl = workload(name)
+    assert (digest(wl.target), digest(wl.source)) == (g["target_sha"], g["source_sha"]), "inputs changed"
     tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    assert tgt.volume == pytest.approx(g["V"], rel=1e-6)
     gpu = lsg.register(tgt, to_dev(wl.source), g["iters"], w=wl.w, traces=True)
+    assert gpu["status"] == 0 and gpu["iters"] == g["iters"]
     _close(gpu["R"], gpu["t"], np.array(g["R"]), np.array(g["t"]), g["extent"])
+    assert gpu["sigma2"] == pytest.approx(g["sigma2"], rel=1e-3)
 
 
 def test_register_nll_monotone_and_deterministic():

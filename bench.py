@@ -125,7 +125,7 @@ def measured_peaks():
         return {"sm_max_mhz": SM_MAX_MHZ_FALLBACK}, "fallback"
 
 
-def cpu_oracle_rate(wl, target_sample_pts: int = 0, budget_s: float = 12.0):
+def cpu_oracle_rate(wl, target_sample_pts: int = 0, budget_s: float = 16.0):
     """FP64 oracle E step (C/OpenMP, all host cores) on a bounded sample of source points against the
     full target; returns (pairs/s, cores, sample description)."""
     import oracle

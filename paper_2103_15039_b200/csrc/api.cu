@@ -182,6 +182,21 @@ static int enqueue_iteration(const void* d_target, const float* d_src, int64_t N
     IterState* st = reinterpret_cast<IterState*>(ws + L.state);
     double* mom = reinterpret_cast<double*>(ws + L.mom);
     float* rec = reinterpret_cast<float*>(ws + L.rec);
+    const char* nf = getenv("LSGCPD_NO_FUSE");
+    if (N <= kTailMaxN && !(nf && nf[0] == '1')) {   // one launch for merge + moments (+ Newton without comm)
+        estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), rec, rp.consistent, rp.phi,
+                     stream, 0);
+        em_tail_launch(reinterpret_cast<float*>(ws + L.part), d_src, N, st, sc, rp.phi,
+                       reinterpret_cast<double*>(ws + L.blockpart), mom, reinterpret_cast<unsigned*>(ws + L.counters),
+                       rp, reinterpret_cast<double*>(ws + L.nll), reinterpret_cast<double*>(ws + L.sig2),
+                       reinterpret_cast<int*>(ws + L.iters), comm ? 0 : 1, stream);
+        if (!comm) return 0;
+        const ncclResult_t r = g_nccl.AllReduce(mom, mom, kMomentCount, kNcclFloat64, kNcclSum, comm->nc, stream);
+        if (r != 0) return nccl_fail(r, "ncclAllReduce(moments)");
+        newton_launch(st, mom, rp, reinterpret_cast<double*>(ws + L.nll), reinterpret_cast<double*>(ws + L.sig2),
+                      reinterpret_cast<int*>(ws + L.iters), stream);
+        return 0;
+    }
     estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), rec, rp.consistent, rp.phi,
                  stream);
     moments_launch(rec, d_src, N, st, reinterpret_cast<double*>(ws + L.blockpart), mom,

@@ -988,17 +988,18 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
 //   C1_n = ln((1 - w_n)/M) - 1.5 ln(2πσ²) = C1 + ln((1 - w_n)/(1 - w0)),
 //   L_o,n = (ln(w_n/V) - C1_n)/ln2 - ω_ref;   w_n = 1 → the point is all outlier (P_out = 1, ln p = -ln V).
 // The pair kernels do not depend on w_n (the fixed-max mode needs L_o,n ≥ L_o, true since w_n ≥ w0).
-__global__ void estep_merge_kernel(const float* __restrict__ part, int64_t N, const IterState* __restrict__ st,
-                                   Sched sc, float* __restrict__ rec, const float* __restrict__ phi) {
+// One CTA (16 warps) merges 32 points (merge_tile32) and stores their records as one contiguous 2-KB row.
+__global__ void __launch_bounds__(kMergePts * 16)
+    estep_merge_kernel(const float* __restrict__ part, int64_t N, const IterState* __restrict__ st, Sched sc,
+                       float* __restrict__ rec, const float* __restrict__ phi) {
     if (!st->active) return;
-    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (n >= N) return;
-    const int64_t kB = sc.B;
-    const int64_t j = n / kB;
-    const int64_t g0 = sched_owner(sc, j * sc.T);
-    const int64_t g1 = sched_owner(sc, (j + 1) * sc.T - 1);
-    merge_point(part + j * sc.kmax * (int64_t)kPartF * kB, g1 - g0 + 1, kB, (int)(n % kB), st,
-                phi ? phi + n : nullptr, rec + n * LSGCPD_REC);
+    __shared__ float tile[kMergePts][LSGCPD_REC + 1];
+    __shared__ double a0s[kMergePts];
+    const int64_t n0 = (int64_t)blockIdx.x * kMergePts;
+    merge_tile32(part, N, n0, st, sc, phi, tile, a0s);
+    __syncthreads();
+    const int p = threadIdx.x / LSGCPD_REC, g = threadIdx.x % LSGCPD_REC;
+    if (n0 + p < N) rec[(n0 + p) * LSGCPD_REC + g] = tile[p][g];
 }
 
 // ---- host-side planning and launch ---------------------------------------------------------
@@ -1146,7 +1147,7 @@ void estep_launch_setup(IterState* st, const void* d_target, const double* R, co
 }
 
 void estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
-                  float* part, float* rec, int consistent, const float* phi, cudaStream_t stream) {
+                  float* part, float* rec, int consistent, const float* phi, cudaStream_t stream, int merge) {
     const float* body = target_body(d_target);
     const bool tc = sc.variant < 0;
     const Variant& V = kVariants[tc ? -1 - sc.variant : sc.variant];
@@ -1167,8 +1168,9 @@ void estep_launch(const void* d_target, const float* d_src, int64_t N, const Ite
         cudaLaunchKernel(TV.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3(TV.threads), targs, TV.smem, stream);
     }
     cudaLaunchKernel(V.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3((V.ncw + 1) * 32), args, 0, stream);
-    const int mt = 256;
-    estep_merge_kernel<<<(unsigned)((N + mt - 1) / mt), mt, 0, stream>>>(part, N, st, sc, rec, phi);
+    if (!merge) return;
+    estep_merge_kernel<<<(unsigned)((N + kMergePts - 1) / kMergePts), kMergePts * 16, 0, stream>>>(part, N, st, sc,
+                                                                                                 rec, phi);
 }
 
 }  // namespace lsg

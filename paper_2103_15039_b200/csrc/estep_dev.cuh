@@ -263,6 +263,7 @@ __device__ inline void merge_point(const float* __restrict__ blk, int64_t nk, in
     }
     // reference max over the segments' maxima (all 0 in the fixed-max mode: no rescaling needed)
     double mustar = -INFINITY;
+#pragma unroll 4
     for (int64_t k = 0; k < nk; ++k) {
         const float* base = blk + k * (int64_t)kPartF * kB;
         mustar = fmax(mustar, (double)base[14 * kB + b]);
@@ -271,6 +272,7 @@ __device__ inline void merge_point(const float* __restrict__ blk, int64_t nk, in
     double a[kAcc];
 #pragma unroll
     for (int f = 0; f < kAcc; ++f) a[f] = 0.0;
+#pragma unroll 2
     for (int64_t k = 0; k < nk; ++k) {
         const float* base = blk + k * (int64_t)kPartF * kB;
         const double muk = (double)base[14 * kB + b];
@@ -302,6 +304,66 @@ __device__ inline void merge_point(const float* __restrict__ blk, int64_t nk, in
     reinterpret_cast<float4*>(r)[1] = o1;
     reinterpret_cast<float4*>(r)[2] = o2;
     reinterpret_cast<float4*>(r)[3] = o3;
+}
+
+// Merge of the 32 points n0..n0+31 (n0 a multiple of 32, so all in one source block) by 16 warps: warp f
+// produces record float f, so every partial load is a coalesced 128-B row (32 consecutive points of one
+// accumulator) and each point's serial chain is 1/16 of merge_point's.  The arithmetic is merge_point's,
+// operation for operation (bit-identical records).  All 512 threads call it; tile[p][f] is valid after the
+// caller's next __syncthreads().
+constexpr int kMergePts = 32;
+__device__ inline void merge_tile32(const float* __restrict__ part, int64_t N, int64_t n0,
+                                    const IterState* __restrict__ st, const Sched& sc, const float* __restrict__ phi,
+                                    float (*tile)[LSGCPD_REC + 1], double* a0s) {
+    const int f = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n = n0 + lane;
+    const int64_t kB = sc.B;   // a multiple of 32
+    const int64_t j = n0 / kB;
+    const int b = (int)(n0 - j * kB) + lane;
+    const int nk = (int)(sched_owner(sc, (j + 1) * sc.T - 1) - sched_owner(sc, j * sc.T) + 1);
+    const float* blk = part + j * sc.kmax * (int64_t)kPartF * kB + b;
+    const bool ok = n < N;
+    double wn = st->w, C1n = st->C1, Lon = st->Lo;
+    if (ok && phi) {
+        const double fi = fmin(fmax((double)phi[n], 0.0), 1.0);
+        wn = 1.0 - (1.0 - st->w) * fi;
+        if (wn < 1.0) {
+            C1n = st->C1 + log((1.0 - wn) / (1.0 - st->w));
+            Lon = wn > 0.0 ? (log(wn / st->volume) - C1n) * 1.4426950408889634074 - st->omega_ref : -INFINITY;
+        }
+    }
+    double mustar = -INFINITY, a = 0.0;
+    if (ok) {
+#pragma unroll 4
+        for (int k = 0; k < nk; ++k) mustar = fmax(mustar, (double)blk[(int64_t)k * kPartF * kB + 14 * kB]);
+        if (wn > 0.0) mustar = fmax(mustar, fmin(Lon, 0.0));
+        if (f < kAcc) {
+#pragma unroll 4
+            for (int k = 0; k < nk; ++k) {
+                const float* base = blk + (int64_t)k * kPartF * kB;
+                const double muk = (double)base[14 * kB];
+                const double sc_k = (muk == mustar) ? 1.0 : exp2(muk - mustar);
+                a = fma(sc_k, (double)base[f * kB], a);
+            }
+        }
+    }
+    if (f == 0) a0s[lane] = a;
+    __syncthreads();
+    float out = 0.f;
+    if (ok) {
+        if (!(wn < 1.0)) {   // all outlier
+            out = f == 14 ? (float)(-log(st->volume)) : (f == 15 ? 1.f : 0.f);
+        } else {
+            const double O = (wn > 0.0) ? exp2(Lon - mustar) : 0.0;
+            const double Z = a0s[lane] + O;
+            const double iz = 1.0 / Z;
+            if (f < 13) out = (float)(a * iz);
+            else if (f == 13) out = (float)(a * iz / st->sigma2);
+            else if (f == 14) out = (float)(C1n + 0.69314718055994530942 * (st->omega_ref + mustar + log2(Z)));
+            else out = (float)(O * iz);
+        }
+    }
+    tile[lane][f] = out;
 }
 
 }  // namespace lsg

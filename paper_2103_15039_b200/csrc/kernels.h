@@ -50,7 +50,7 @@ void estep_launch_setup(IterState* st, const void* d_target, const double* R, co
                         double w, double V, int64_t M, int consistent, double eta, cudaStream_t stream);
 // phi: optional per-source-point confidence φ(x_n) (Eq. 8: w_n = 1 - (1 - w0) φ(x_n)), NULL = uniform w0
 void estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
-                  float* part, float* rec, int consistent, const float* phi, cudaStream_t stream);
+                  float* part, float* rec, int consistent, const float* phi, cudaStream_t stream, int merge = 1);
 
 // mstep.cu
 constexpr int kMomentCount = 75;          // G 60, U 12, σ²ΣD, ΣP, Σ ln p
@@ -63,6 +63,11 @@ void sigma2_init_launch(IterState* st, const void* d_target, const double* sums,
                         double sigma2_user, double* sigma2_trace, double* ntot_out, cudaStream_t stream);
 void newton_launch(IterState* st, const double* mom, const RegParams& rp, double* nll_trace, double* sigma2_trace,
                    int* iters_done, cudaStream_t stream);
+// merge + moments (+ Newton/σ² when run_newton) in one launch after the pair kernels (estep_launch, merge = 0)
+void em_tail_launch(const float* part, const float* src, int64_t N, IterState* st, const Sched& sc, const float* phi,
+                    double* blockpart, double* mom, unsigned* counter, const RegParams& rp, double* nll_trace,
+                    double* sigma2_trace, int* iters_done, int run_newton, cudaStream_t stream);
+constexpr int64_t kTailMaxN = 1 << 17;   // above this the separate merge / moments grids are used
 
 // target.cu
 size_t prepare_ws_bytes(int64_t M);

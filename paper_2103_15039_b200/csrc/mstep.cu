@@ -10,6 +10,7 @@
 // rule (right derivatives, Eq. 11-12) and takes damped Newton steps (Eq. 13 P:337-339,
 // readings R11-R13).
 #include "common.cuh"
+#include "estep_dev.cuh"
 #include "kernels.h"
 
 namespace lsg {
@@ -144,24 +145,18 @@ struct Mom {
     double U[12];
 };
 
-__device__ inline void build_mom(Mom& mo, const double* m) {
-    for (int i = 0; i < 3; ++i)
-        for (int a = 0; a < 4; ++a) {
-            mo.U[4 * i + a] = m[60 + 4 * i + a];
-            for (int j = 0; j < 3; ++j)
-                for (int b = 0; b < 4; ++b) mo.GG[4 * i + a][4 * j + b] = m[s3(i, j) * 10 + s4(a, b)];
-        }
-}
-
-// q(Θ') - q(Θ_E) = 2 Δθ·U + Δθᵀ𝔾Δθ
-__device__ inline double q_rel(const Mom& mo, const double* dth) {
+// q(Θ') - q(Θ_E) = 2 Δθ·U + Δθᵀ𝔾Δθ over one warp: lane r < 12 takes row r, a butterfly sum closes it
+// (every lane gets the bit-identical total: each level adds the same pair of values in either order).
+__device__ inline double q_rel_warp(const Mom& mo, const double* dth, int lane) {
     double q = 0.0;
-    for (int r = 0; r < 12; ++r) {
+    if (lane < 12) {
         double gr = 0.0;
-        for (int c = 0; c < 12; ++c) gr = fma(mo.GG[r][c], dth[c], gr);
-        q = fma(dth[r], 2.0 * mo.U[r] + gr, q);
+        for (int c = 0; c < 12; ++c) gr = fma(mo.GG[lane][c], dth[c], gr);
+        double dl = dth[0];
+        for (int r = 1; r < 12; ++r) dl = (r == lane) ? dth[r] : dl;
+        q = dl * (2.0 * mo.U[lane] + gr);
     }
-    return q;
+    return warp_sum(q);
 }
 
 __device__ inline void theta_of(const double* R, const double* t, double* th) {
@@ -213,9 +208,11 @@ __device__ inline void se3_exp(const double* d, double* dR, double* dt) {
         C = 1.0 / 6.0 - th2 / 120.0 + th2 * th2 / 5040.0;
     } else {
         const double th = sqrt(th2);
-        A = sin(th) / th;
-        B = (1.0 - cos(th)) / th2;
-        C = (th - sin(th)) / (th2 * th);
+        double sn, cs;
+        sincos(th, &sn, &cs);
+        A = sn / th;
+        B = (1.0 - cs) / th2;
+        C = (th - sn) / (th2 * th);
     }
     const double K[9] = {0.0, -wz, wy, wz, 0.0, -wx, -wy, wx, 0.0};
     double K2[9];
@@ -233,30 +230,31 @@ __device__ inline void se3_exp(const double* d, double* dR, double* dt) {
 // Cholesky solve (A + μI) x = b, K×K.  Returns false if not positive definite.
 template <int K>
 __device__ inline bool chol_solve(const double* A, double mu, const double* b, double* x) {
-    double L[K * K];
+    double L[K * K], id[K];   // id[j] = 1 / L_jj: one reciprocal square root per column, no divisions
     for (int i = 0; i < K * K; ++i) L[i] = 0.0;
     for (int j = 0; j < K; ++j) {
         double s = A[j * K + j] + mu;
         for (int k = 0; k < j; ++k) s -= L[j * K + k] * L[j * K + k];
         if (!(s > 0.0)) return false;
-        const double d = sqrt(s);
-        L[j * K + j] = d;
+        const double r = rsqrt(s);
+        id[j] = r;
+        L[j * K + j] = s * r;
         for (int i = j + 1; i < K; ++i) {
             double v = A[i * K + j];
             for (int k = 0; k < j; ++k) v -= L[i * K + k] * L[j * K + k];
-            L[i * K + j] = v / d;
+            L[i * K + j] = v * r;
         }
     }
     double y[K];
     for (int i = 0; i < K; ++i) {
         double v = b[i];
         for (int k = 0; k < i; ++k) v -= L[i * K + k] * y[k];
-        y[i] = v / L[i * K + i];
+        y[i] = v * id[i];
     }
     for (int i = K - 1; i >= 0; --i) {
         double v = y[i];
         for (int k = i + 1; k < K; ++k) v -= L[k * K + i] * x[k];
-        x[i] = v / L[i * K + i];
+        x[i] = v * id[i];
     }
     return true;
 }
@@ -297,19 +295,19 @@ __device__ inline void aff_exp(const double* d, double* dA, double* dt) {
     }
 }
 
-// One warp: the dense algebra (v = U + 𝔾Δθ, J, 𝔾J, ∇, H) is spread over the lanes; the damping loop
-// (Cholesky K×K, exp, candidate q) runs on lane 0.  All lanes end with identical state.
+// One warp: the dense algebra (v = U + 𝔾Δθ, J, 𝔾J, ∇, H) is spread over the lanes.  The damping loop
+// (Cholesky K×K, exp, candidate q) runs redundantly in every lane on identical data, so its branches are
+// warp-uniform and no lane waits on a shared-memory handoff; the candidate q is a 12-lane dot product
+// closed by a butterfly sum (bit-identical in every lane: each level adds the same two values).
 // K = 6: SE(3) (the paper's rigid registration); K = 12: the affine group GA⁺(3) (NEXT-4).
 template <int K>
 __device__ __noinline__ void newton_body(IterState* st, const double* __restrict__ mom, const RegParams& rp,
                                          double* nll_trace, double* sigma2_trace, int* iters_done) {
     constexpr int NP = K * (K + 1) / 2;   // symmetric basis pairs (k ≤ l)
+    constexpr int PPL = (NP + 31) / 32;   // pairs per lane
     __shared__ Mom mo;
     __shared__ double S[NP][16];
     __shared__ double J[K][12], GJ[K][12], v[12], Bm[16], H[K * K], grad[K];
-    __shared__ double Rs[9], tsh[3], th_E[12];
-    __shared__ double q_cur, step_rot, step_trans;
-    __shared__ int stop;
     const int lane = threadIdx.x;
     const IterState s = *st;
     if (!s.active) return;
@@ -319,26 +317,30 @@ __device__ __noinline__ void newton_body(IterState* st, const double* __restrict
         mo.GG[r][c] = mom[s3(i, jj) * 10 + s4(a, b)];
     }
     if (lane < 12) mo.U[lane] = mom[60 + lane];
-    for (int pidx = lane; pidx < NP; pidx += 32) {
+    int pk[PPL], pl[PPL];   // this lane's (k, l) pairs, fixed for the whole call
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+        const int pidx = lane + 32 * u;
         int k = 0, l = 0;
         for (int idx = 0, kk = 0; kk < K; ++kk)
             for (int ll = kk; ll < K; ++ll, ++idx)
                 if (idx == pidx) { k = kk; l = ll; }
-        double Ek[16], El[16], EE1[16], EE2[16];
-        basisK<K>(k, Ek);
-        basisK<K>(l, El);
-        mat4mul(Ek, El, EE1);
-        mat4mul(El, Ek, EE2);
-        for (int i = 0; i < 16; ++i) S[pidx][i] = 0.5 * (EE1[i] + EE2[i]);
+        pk[u] = k;
+        pl[u] = l;
+        if (pidx < NP) {
+            double Ek[16], El[16], EE1[16], EE2[16];
+            basisK<K>(k, Ek);
+            basisK<K>(l, El);
+            mat4mul(Ek, El, EE1);
+            mat4mul(El, Ek, EE2);
+            for (int i = 0; i < 16; ++i) S[pidx][i] = 0.5 * (EE1[i] + EE2[i]);
+        }
     }
-    if (lane == 0) {
-        for (int i = 0; i < 9; ++i) Rs[i] = s.R[i];
-        for (int i = 0; i < 3; ++i) tsh[i] = s.t[i];
-        theta_of(s.R, s.t, th_E);
-        q_cur = 0.0;
-        step_rot = step_trans = 0.0;
-        stop = 0;
-    }
+    double Rs[9], tsh[3], th_E[12];   // the current pose: registers, identical in every lane
+    for (int i = 0; i < 9; ++i) Rs[i] = s.R[i];
+    for (int i = 0; i < 3; ++i) tsh[i] = s.t[i];
+    theta_of(s.R, s.t, th_E);
+    double q_cur = 0.0, step_rot = 0.0, step_trans = 0.0;
     __syncwarp();
     const double sig2D = mom[72], sumP = mom[73], sumlnp = mom[74];
     const double ntot = mom[75];  // total source points (written by the σ²₀ kernel)
@@ -379,67 +381,65 @@ __device__ __noinline__ void newton_body(IterState* st, const double* __restrict
             Bm[mi * 4 + j] = b;
         }
         __syncwarp();
-        for (int pidx = lane; pidx < NP; pidx += 32) {
-            int k = 0, l = 0;
-            for (int idx = 0, kk = 0; kk < K; ++kk)
-                for (int ll = kk; ll < K; ++ll, ++idx)
-                    if (idx == pidx) { k = kk; l = ll; }
-            double h = 0.0;
-            for (int r = 0; r < 12; ++r) h = fma(J[k][r], GJ[l][r], h);
-            for (int i = 0; i < 16; ++i) h = fma(Bm[i], S[pidx][i], h);
-            H[k * K + l] = h;
-            H[l * K + k] = h;
-        }
-        __syncwarp();
-        if (lane == 0) {
-            double trs = 0.0;
-            for (int k = 0; k < K; ++k) trs += H[k * K + k];
-            const double tr = fabs(trs) / (double)K;
-            double mu = 0.0;
-            bool accepted = false, converged = false;
-            for (int tries = 0; tries < 20; ++tries) {
-                double delta[K], mg[K];
-                for (int k = 0; k < K; ++k) mg[k] = -grad[k];
-                if (!chol_solve<K>(H, mu, mg, delta)) {
-                    mu = fmax(10.0 * mu, 1e-6 * tr);
-                    continue;
-                }
-                double nr = 0.0, nt = 0.0;   // linear (rotation) part, translation part of the step
-                for (int k = 0; k < K - 3; ++k) nr += delta[k] * delta[k];
-                for (int k = K - 3; k < K; ++k) nt += delta[k] * delta[k];
-                nr = sqrt(nr);
-                nt = sqrt(nt);
-                if (nr < 1e-10 && nt < 1e-10 * s.extent) {
-                    converged = true;
-                    break;
-                }
-                double dR[9], dt[3], Rn[9], tn[3];
-                if (K == 6) se3_exp(delta, dR, dt);
-                else aff_exp(delta, dR, dt);
-                for (int i = 0; i < 3; ++i) {
-                    for (int j = 0; j < 3; ++j)
-                        Rn[3 * i + j] = Rs[3 * i] * dR[j] + Rs[3 * i + 1] * dR[3 + j] + Rs[3 * i + 2] * dR[6 + j];
-                    tn[i] = Rs[3 * i] * dt[0] + Rs[3 * i + 1] * dt[1] + Rs[3 * i + 2] * dt[2] + tsh[i];
-                }
-                double thn[12], dthn[12];
-                theta_of(Rn, tn, thn);
-                for (int r = 0; r < 12; ++r) dthn[r] = thn[r] - th_E[r];
-                const double qn = q_rel(mo, dthn);
-                if (qn < q_cur) {
-                    for (int i = 0; i < 9; ++i) Rs[i] = Rn[i];
-                    for (int i = 0; i < 3; ++i) tsh[i] = tn[i];
-                    q_cur = qn;
-                    accepted = true;
-                    step_rot += nr;
-                    step_trans += nt;
-                    break;
-                }
-                mu = fmax(10.0 * mu, 1e-6 * tr);
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+            const int pidx = lane + 32 * u;
+            if (pidx < NP) {
+                const int k = pk[u], l = pl[u];
+                double h = 0.0;
+                for (int r = 0; r < 12; ++r) h = fma(J[k][r], GJ[l][r], h);
+                for (int i = 0; i < 16; ++i) h = fma(Bm[i], S[pidx][i], h);
+                H[k * K + l] = h;
+                H[l * K + k] = h;
             }
-            stop = (converged || !accepted) ? 1 : 0;
         }
         __syncwarp();
-        if (stop) break;
+        double trs = 0.0;
+        for (int k = 0; k < K; ++k) trs += H[k * K + k];
+        const double tr = fabs(trs) / (double)K;
+        double mu = 0.0;
+        bool accepted = false, converged = false;
+        for (int tries = 0; tries < 20; ++tries) {
+            double delta[K], mg[K];
+            for (int k = 0; k < K; ++k) mg[k] = -grad[k];
+            if (!chol_solve<K>(H, mu, mg, delta)) {
+                mu = fmax(10.0 * mu, 1e-6 * tr);
+                continue;
+            }
+            double nr = 0.0, nt = 0.0;   // linear (rotation) part, translation part of the step
+            for (int k = 0; k < K - 3; ++k) nr += delta[k] * delta[k];
+            for (int k = K - 3; k < K; ++k) nt += delta[k] * delta[k];
+            nr = sqrt(nr);
+            nt = sqrt(nt);
+            if (nr < 1e-10 && nt < 1e-10 * s.extent) {
+                converged = true;
+                break;
+            }
+            double dR[9], dt[3], Rn[9], tn[3];
+            if (K == 6) se3_exp(delta, dR, dt);
+            else aff_exp(delta, dR, dt);
+            for (int i = 0; i < 3; ++i) {
+                for (int j = 0; j < 3; ++j)
+                    Rn[3 * i + j] = Rs[3 * i] * dR[j] + Rs[3 * i + 1] * dR[3 + j] + Rs[3 * i + 2] * dR[6 + j];
+                tn[i] = Rs[3 * i] * dt[0] + Rs[3 * i + 1] * dt[1] + Rs[3 * i + 2] * dt[2] + tsh[i];
+            }
+            double thn[12], dthn[12];
+            theta_of(Rn, tn, thn);
+            for (int r = 0; r < 12; ++r) dthn[r] = thn[r] - th_E[r];
+            const double qn = q_rel_warp(mo, dthn, lane);
+            if (qn < q_cur) {
+                for (int i = 0; i < 9; ++i) Rs[i] = Rn[i];
+                for (int i = 0; i < 3; ++i) tsh[i] = tn[i];
+                q_cur = qn;
+                accepted = true;
+                step_rot += nr;
+                step_trans += nt;
+                break;
+            }
+            mu = fmax(10.0 * mu, 1e-6 * tr);
+        }
+        __syncwarp();   // every lane is done with H and grad before the next iteration rewrites them
+        if (converged || !accepted) break;
     }
     if (lane != 0) return;
 
@@ -481,6 +481,112 @@ __global__ void __launch_bounds__(32) newton_kernel(IterState* st, const double*
                                                     double* nll_trace, double* sigma2_trace, int* iters_done) {
     if (rp.group) newton_body<12>(st, mom, rp, nll_trace, sigma2_trace, iters_done);
     else newton_body<6>(st, mom, rp, nll_trace, sigma2_trace, iters_done);
+}
+
+// ---- EM tail: merge + moments (+ Newton) in one launch ---------------------------------------------------
+// For N ≤ kTailMaxN the kernels after the E step collapse into one (Newton included without a communicator;
+// with one, the moments are all-reduced and newton_kernel follows, so one rank with NCCL equals none): each CTA
+// merges 32-point groups (merge_tile32, grid-stride) and folds them into the moments at once (no record
+// round trip); warp w < 6 owns the 10 moments of G row w, warps 6-8 the 4 of U row w - 6, warp 9 σ²ΣD, ΣP,
+// Σ ln p.  The last CTA to finish (atomic ticket, as block_reduce_store) sums the per-CTA moments in CTA
+// order and (run_newton) runs the Newton step and σ² update with its first warp.  Deterministic for a fixed grid.
+constexpr int kTailThreads = kMergePts * 16;
+template <int K>
+__device__ __forceinline__ void tail_newton(IterState* st, const double* mom, const RegParams& rp, double* nll,
+                                            double* s2t, int* it) {
+    newton_body<K>(st, mom, rp, nll, s2t, it);
+}
+__global__ void __launch_bounds__(kTailThreads)
+    em_tail_kernel(const float* __restrict__ part, const float* __restrict__ src, int64_t N, IterState* st,
+                   Sched sc, const float* __restrict__ phi, double* blockpart, double* mom, unsigned* counter,
+                   RegParams rp, double* nll_trace, double* sigma2_trace, int* iters_done, int run_newton) {
+    if (!st->active) return;
+    __shared__ float tile[kMergePts][LSGCPD_REC + 1];
+    __shared__ double a0s[kMergePts];
+    __shared__ double msum[kMom];
+    __shared__ bool last;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double R[9], t[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) R[i] = st->R[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) t[i] = st->t[i];
+    const double s2 = st->sigma2;
+    double acc[10];
+#pragma unroll
+    for (int j = 0; j < 10; ++j) acc[j] = 0.0;
+    const int64_t ngroups = (N + kMergePts - 1) / kMergePts;
+    for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const int64_t n0 = g * kMergePts;
+        merge_tile32(part, N, n0, st, sc, phi, tile, a0s);
+        __syncthreads();
+        const int64_t n = n0 + lane;
+        if (w < 10 && n < N) {
+            const float* r = tile[lane];
+            const double P = r[0];
+            const double x[4] = {(double)src[3 * n], (double)src[3 * n + 1], (double)src[3 * n + 2], 1.0};
+            if (w < 6) {            // G_{ij,ab} += H_ij x̃_a x̃_b, ij = w
+                const double H[6] = {P + (double)r[4], (double)r[5], (double)r[6], P + (double)r[7], (double)r[8],
+                                     P + (double)r[9]};
+                double h = H[0];
+#pragma unroll
+                for (int q = 1; q < 6; ++q) h = (w == q) ? H[q] : h;
+                int k = 0;
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = a; b < 4; ++b) { acc[k] = fma(h, x[a] * x[b], acc[k]); ++k; }
+            } else if (w < 9) {     // U_{ia} += u_i x̃_a, i = w - 6
+                const double H[6] = {P + (double)r[4], (double)r[5], (double)r[6], P + (double)r[7], (double)r[8],
+                                     P + (double)r[9]};
+                const double gv[3] = {(double)r[1] + (double)r[10], (double)r[2] + (double)r[11],
+                                      (double)r[3] + (double)r[12]};
+                double xh[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    xh[i] = fma(R[3 * i], x[0], fma(R[3 * i + 1], x[1], fma(R[3 * i + 2], x[2], t[i])));
+                double u[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    u[i] = H[s3(i, 0)] * xh[0] + H[s3(i, 1)] * xh[1] + H[s3(i, 2)] * xh[2] - gv[i];
+                const double ui = w == 6 ? u[0] : (w == 7 ? u[1] : u[2]);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) acc[a] = fma(ui, x[a], acc[a]);
+            } else {                // σ²ΣD, ΣP, Σ ln p
+                acc[0] = fma(s2, (double)r[13], acc[0]);
+                acc[1] += P;
+                acc[2] += (double)r[14];
+            }
+        }
+        __syncthreads();            // the tile is rewritten by the next group
+    }
+    const int nacc = w < 6 ? 10 : (w < 9 ? 4 : (w == 9 ? 3 : 0));
+    const int m0 = w < 6 ? 10 * w : (w < 9 ? 60 + 4 * (w - 6) : 72);
+#pragma unroll
+    for (int j = 0; j < 10; ++j) {
+        const double v = warp_sum(acc[j]);
+        if (lane == 0 && j < nacc) msum[m0 + j] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < kMom) blockpart[(int64_t)blockIdx.x * kMom + threadIdx.x] = msum[threadIdx.x];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x < kMom) {
+        const volatile double* bp = blockpart;
+        double v = bp[threadIdx.x];
+        for (unsigned b = 1; b < gridDim.x; ++b) v += bp[(int64_t)b * kMom + threadIdx.x];
+        mom[threadIdx.x] = v;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+    __syncthreads();
+    if (run_newton && threadIdx.x < 32) {
+        if (rp.group) tail_newton<12>(st, mom, rp, nll_trace, sigma2_trace, iters_done);
+        else tail_newton<6>(st, mom, rp, nll_trace, sigma2_trace, iters_done);
+    }
 }
 
 // ---- batched registrations (NEXT-3): one CTA / warp per problem -----------------------------------------
@@ -592,6 +698,20 @@ void sigma2_init_launch(IterState* st, const void* d_target, const double* sums,
                         double sigma2_user, double* sigma2_trace, double* ntot_out, cudaStream_t stream) {
     sigma2_init_kernel<<<1, 1, 0, stream>>>(st, reinterpret_cast<const TargetHeader*>(d_target), sums, rp,
                                              sigma2_user, sigma2_trace, ntot_out);
+}
+void em_tail_launch(const float* part, const float* src, int64_t N, IterState* st, const Sched& sc, const float* phi,
+                    double* blockpart, double* mom, unsigned* counter, const RegParams& rp, double* nll_trace,
+                    double* sigma2_trace, int* iters_done, int run_newton, cudaStream_t stream) {
+    static int nsm = 0;
+    if (nsm == 0) {
+        int dev;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t ng = (N + kMergePts - 1) / kMergePts;
+    const int64_t cap = nsm < kMomentBlocks ? nsm : kMomentBlocks;   // blockpart holds kMomentBlocks rows
+    em_tail_kernel<<<(unsigned)(ng < cap ? ng : cap), kTailThreads, 0, stream>>>(
+        part, src, N, st, sc, phi, blockpart, mom, counter, rp, nll_trace, sigma2_trace, iters_done, run_newton);
 }
 void newton_launch(IterState* st, const double* mom, const RegParams& rp, double* nll_trace, double* sigma2_trace,
                    int* iters_done, cudaStream_t stream) {

@@ -55,6 +55,14 @@ struct BatchCursor {
         j = lu / bp[b].T;
         tile = lu % bp[b].T;
     }
+    // jump to the last unit of the current problem (the caller's loop step then enters the next problem):
+    // skipping a problem costs one step instead of one per unit
+    __device__ void to_last(const BatchProblem* bp, int64_t& u) {
+        const BatchProblem& P = bp[b];
+        j = P.nblk - 1;
+        tile = P.T - 1;
+        u = P.unit0 + P.nblk * P.T - 1;
+    }
     __device__ void next(const BatchProblem* bp) {
         if (++tile == bp[b].T) {
             tile = 0;
@@ -88,6 +96,12 @@ __global__ void __launch_bounds__((kBNCW + 1) * 32, kBMinB)
     const int64_t g = blockIdx.x;
     const int64_t u0 = sched_start(sc, g), u1 = sched_start(sc, g + 1);
     if (u0 >= u1) return;
+    {   // nothing to serve in this CTA's range (e.g. mode 1 while every problem is in the fixed-max mode)
+        const int b0 = find_problem_unit(bp, B, u0), b1 = find_problem_unit(bp, B, u1 - 1);
+        bool any = false;
+        for (int b = b0; b <= b1 && !any; ++b) any = serves(st[b], mode);
+        if (!any) return;
+    }
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -105,7 +119,7 @@ __global__ void __launch_bounds__((kBNCW + 1) * 32, kBMinB)
             cur.start(bp, B, u0);
             int64_t it = 0;
             for (int64_t u = u0; u < u1; ++u, cur.next(bp)) {
-                if (!serves(st[cur.b], mode)) continue;
+                if (!serves(st[cur.b], mode)) { cur.to_last(bp, u); continue; }
                 const int s = (int)(it % kStages);
                 const uint32_t ph = (uint32_t)((it / kStages) & 1);
                 mbar_wait_sleep(&empty_bar[s], ph ^ 1);
@@ -184,7 +198,7 @@ __global__ void __launch_bounds__((kBNCW + 1) * 32, kBMinB)
     cur.start(bp, B, u0);
     int64_t it = 0;
     for (int64_t u = u0; u < u1; ++u, cur.next(bp)) {
-        if (!serves(st[cur.b], mode)) continue;
+        if (!serves(st[cur.b], mode)) { cur.to_last(bp, u); continue; }
         if (cur.b != cur_b || cur.j != cur_j) {
             if (cur_b >= 0) flush(cur_b, cur_j);
             cur_b = cur.b;
@@ -350,7 +364,7 @@ __global__ void __launch_bounds__(kBTThreads, 1)
             cur.start(bp, B, u0);
             int64_t it = 0;
             for (int64_t u = u0; u < u1; ++u, cur.next(bp)) {
-                if (!serves_tc(st[cur.b])) continue;
+                if (!serves_tc(st[cur.b])) { cur.to_last(bp, u); continue; }
                 const int s = (int)(it & 3);
                 mbar_wait_sleep(&empty_bar[s], (uint32_t)(((it >> 2) & 1) ^ 1));
                 mbar_arrive_expect_tx(&full_bar[s], kTcTileBytes);
@@ -369,7 +383,7 @@ __global__ void __launch_bounds__(kBTThreads, 1)
         int64_t it = 0, grp = 0;
         int tig = 0;
         for (int64_t u = u0; u < u1; ++u, cur.next(bp)) {
-            if (!serves_tc(st[cur.b])) continue;
+            if (!serves_tc(st[cur.b])) { cur.to_last(bp, u); continue; }
             const int s = (int)(it & 3);
             const int db = (int)(grp & 1);
             const bool first = tig == 0;
@@ -553,7 +567,7 @@ __global__ void __launch_bounds__(kBTThreads, 1)
     int tig = 0;
     bool pending = false;
     for (int64_t u = u0; u < u1; ++u, cur.next(bp)) {
-        if (!serves_tc(st[cur.b])) continue;
+        if (!serves_tc(st[cur.b])) { cur.to_last(bp, u); continue; }
         if (cur.b != cur_b || cur.j != cur_j) {   // previous block fully drained and flushed at its end
             cur_b = cur.b;
             cur_j = cur.j;

@@ -146,3 +146,22 @@ def test_register_tolerance_stops_early_and_matches_a_fixed_count():
     np.testing.assert_array_equal(early["R"], fixed["R"])
     np.testing.assert_array_equal(early["t"], fixed["t"])
     assert early["sigma2"] == fixed["sigma2"]
+
+
+@pytest.mark.parametrize("name,conf", [("tiny", False), ("object", True)])
+def test_fused_em_tail_equals_separate_kernels(name, conf, monkeypatch):
+    # N ≤ 2^17: merge + moments + Newton run as one kernel (em_tail_kernel); LSGCPD_NO_FUSE=1 selects the
+    # separate merge / moments / Newton kernels.  Same records, different FP64 summation order of the moments:
+    # the registrations agree to FP64 rounding, with and without per-point confidence weights.
+    import paper_2103_15039_b200 as lsg
+    wl = workload(name)
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    phi = to_dev(np.random.default_rng(2).uniform(0.3, 1.0, wl.N).astype(np.float32)) if conf else None
+    kw = dict(w=wl.w, traces=True, src_conf=phi) if conf else dict(w=wl.w, traces=True)
+    fused = lsg.register(tgt, to_dev(wl.source), 30, **kw)
+    monkeypatch.setenv("LSGCPD_NO_FUSE", "1")
+    sep = lsg.register(tgt, to_dev(wl.source), 30, **kw)
+    assert fused["iters"] == sep["iters"] == 30
+    _close(fused["R"], fused["t"], sep["R"], sep["t"], tgt.extent, tol=1e-9)
+    np.testing.assert_allclose(fused["sigma2_trace"], sep["sigma2_trace"], rtol=1e-9)
+    np.testing.assert_allclose(fused["nll"], sep["nll"], rtol=1e-10)

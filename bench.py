@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--skip-cpu", action="store_true", help="skip the cpu_baseline leg (profiling runs)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--iters", type=int, default=0, help="override EM iterations per step (0 = config's)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="every rank registers the whole config on its own (no collective, weak scaling): "
+                         "the SURVEY 8(d).3 'replicas' mode for the small configs")
     return ap.parse_args()
 
 
@@ -206,14 +209,14 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     iters = args.iters or wl.iters
-    lo, hi = shard(wl.N, rank, world)
+    lo, hi = (0, wl.N) if args.replicas else shard(wl.N, rank, world)
     n_local = hi - lo
 
     # resident inputs
     tgt_xyz = torch.from_numpy(wl.target).to(dev)
     src = torch.from_numpy(np.ascontiguousarray(wl.source[lo:hi])).to(dev)
     target = lsg.prepare_target(tgt_xyz, wl.knn_k)
-    comm = lsg.Comm(rank, world) if world > 1 else None
+    comm = lsg.Comm(rank, world) if world > 1 and not args.replicas else None
     reg = lsg.Registrar(target, src, iters)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MiB > 126 MB L2
 
@@ -248,7 +251,7 @@ def main():
         e1.record(stream)
         barrier()
     dev_s = max_over_ranks(e0.elapsed_time(e1) / 1e3)
-    pairs_per_step = float(wl.M) * float(wl.N) * iters
+    pairs_per_step = float(wl.M) * float(wl.N) * iters * (world if args.replicas else 1)
     assert all(i == iters for i in iters_done), iters_done
     value = pairs_per_step * args.steps / dev_s
     clocks = clk.summary()
@@ -331,19 +334,27 @@ def main():
     if world > 1:
         dist.barrier()
     if rank == 0:
-        # per registration: setup + σ²₀ sums + σ²₀ init, then per EM iteration: tensor-core E step,
-        # CUDA-core E step (returns at once in the fixed-max mode), merge, moments, Newton
-        launches_per_step = 3 + 5 * iters
+        # per registration: setup + σ²₀ sums + σ²₀ init, then per EM iteration the pair kernels (tensor-core
+        # E step + CUDA-core E step, which returns at once in the fixed-max mode; one small-block CUDA-core
+        # kernel for problems too small to fill the GPU), then merge, moments, Newton — or, for N ≤ 2^17,
+        # one em_tail_kernel (plus newton_kernel after the all-reduce when a communicator is used)
+        m_pad = -(-wl.M // 64) * 64
+        tc = -(-n_local // 768) * (m_pad // 64) >= 2 * torch.cuda.get_device_properties(dev).multi_processor_count
+        tail = (1 if comm is None else 2) if n_local <= (1 << 17) else 3
+        launches_per_step = 3 + ((2 if tc else 1) + tail) * iters
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak" if args.replicas else "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
             "config": {"workload": wl.name, "M": wl.M, "N": wl.N, "iters_per_step": iters, "w": wl.w,
                        "knn_k": wl.knn_k, "step": "one full registration (lsgcpd_register)",
-                       "parallelism": f"source-sharded x{world}, target replicated, 75-double NCCL all-reduce "
-                                      f"per EM iteration",
+                       "parallelism": (f"replicas x{world} (independent registrations, no collective)"
+                                       if args.replicas else
+                                       f"source-sharded x{world}, target replicated, 75-double NCCL all-reduce "
+                                       f"per EM iteration"),
                        "l2": "flushed between steps (256 MiB write)"},
-            "registrations_per_s": args.steps / dev_s,
+            "registrations_per_s": args.steps * (world if args.replicas else 1) / dev_s,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
         }

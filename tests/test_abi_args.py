@@ -1,0 +1,113 @@
+"""Argument validation at the C ABI, on the CPU: empty, out-of-range and non-finite arguments are refused with
+LSGCPD_EINVAL and a message before any device work (include/lsgcpd.h "Errors"), so these run without a GPU.
+The fake device pointers below are never dereferenced: every call fails validation first."""
+import ctypes
+
+import numpy as np
+import pytest
+
+EINVAL = -1
+FAKE = 0x10000          # 16-byte aligned, never dereferenced
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2103_15039_b200 import build
+    build.build()
+    import paper_2103_15039_b200 as pkg
+    return pkg.lib()
+
+
+def _pose():
+    R = (ctypes.c_double * 9)(1, 0, 0, 0, 1, 0, 0, 0, 1)
+    t = (ctypes.c_double * 3)(0, 0, 0)
+    return ctypes.cast(R, ctypes.POINTER(ctypes.c_double)), ctypes.cast(t, ctypes.POINTER(ctypes.c_double))
+
+
+def _estep(L, M, N, s2=1e-3, w=0.1, V=1.0, R=None, t=None):
+    R0, t0 = _pose()
+    return L.lsgcpd_estep(FAKE, M, FAKE, N, R or R0, t or t0, s2, w, V, 1, FAKE, FAKE, 1 << 40, None)
+
+
+def _err(L):
+    return L.lsgcpd_last_error().decode()
+
+
+@pytest.mark.parametrize("M,N", [(0, 10), (10, 0), (0, 0), (-5, 10), (1 << 30, 10), (10, 1 << 34)])
+def test_estep_empty_and_out_of_range_sizes(L, M, N):
+    assert _estep(L, M, N) == EINVAL
+    assert "out of range" in _err(L)
+
+
+@pytest.mark.parametrize("kw,msg", [(dict(s2=0.0), "sigma2"), (dict(s2=float("nan")), "sigma2"),
+                                    (dict(w=1.0), "w must"), (dict(w=-0.1), "w must"), (dict(V=0.0), "volume"),
+                                    (dict(V=float("inf")), "volume")])
+def test_estep_bad_scalars(L, kw, msg):
+    assert _estep(L, 100, 100, **kw) == EINVAL
+    assert msg in _err(L)
+
+
+def test_estep_bad_pose_and_pointers(L):
+    Rb = (ctypes.c_double * 9)(2, 0, 0, 0, 1, 0, 0, 0, 1)                 # not a rotation
+    assert _estep(L, 100, 100, R=ctypes.cast(Rb, ctypes.POINTER(ctypes.c_double))) == EINVAL
+    Rr = (ctypes.c_double * 9)(1, 0, 0, 0, -1, 0, 0, 0, -1)               # det +1 reflection pair: a rotation
+    tn = (ctypes.c_double * 3)(np.nan, 0, 0)
+    assert _estep(L, 100, 100, R=ctypes.cast(Rr, ctypes.POINTER(ctypes.c_double)),
+                  t=ctypes.cast(tn, ctypes.POINTER(ctypes.c_double))) == EINVAL
+    assert "t must be finite" in _err(L)
+    R0, t0 = _pose()
+    assert L.lsgcpd_estep(None, 10, FAKE, 10, R0, t0, 1e-3, 0.1, 1.0, 1, FAKE, FAKE, 1 << 40, None) == EINVAL
+    assert L.lsgcpd_estep(FAKE + 4, 10, FAKE, 10, R0, t0, 1e-3, 0.1, 1.0, 1, FAKE, FAKE, 1 << 40, None) == EINVAL
+    assert "aligned" in _err(L)
+
+
+def test_workspace_queries_refuse_empty_sizes(L):
+    assert L.lsgcpd_estep_workspace_bytes(0, 10) == 0
+    assert L.lsgcpd_estep_workspace_bytes(10, 0) == 0
+    assert L.lsgcpd_register_workspace_bytes(10, 0, 5) == 0
+    assert L.lsgcpd_register_workspace_bytes(10, 10, -1) == 0
+    assert L.lsgcpd_select_workspace_bytes(0) == 0
+    assert L.lsgcpd_target_prior_workspace_bytes(0) == 0
+    assert L.lsgcpd_prepare_workspace_bytes(-1, 10) == 0
+
+
+def test_prepare_register_and_model_extensions_refuse_bad_arguments(L):
+    import paper_2103_15039_b200 as pkg
+    info = pkg.TargetInfo()
+    # prepare: M < 3, k out of range
+    assert L.lsgcpd_prepare_target(FAKE, 2, None, FAKE, FAKE, 1 << 40, ctypes.byref(info), None, None) == EINVAL
+    pp = pkg.PrepParams()
+    L.lsgcpd_prep_params_default(ctypes.byref(pp))
+    pp.knn_k = 40
+    assert L.lsgcpd_prepare_target(FAKE, 100, ctypes.byref(pp), FAKE, FAKE, 1 << 40, ctypes.byref(info), None,
+                                   None) == EINVAL
+    # register: empty local shard, w out of range, eta ≥ 1, unknown group
+    ep = pkg.EmParams()
+    L.lsgcpd_em_params_default(ctypes.byref(ep))
+    Ro = (ctypes.c_double * 9)()
+    to = (ctypes.c_double * 3)()
+    s2 = ctypes.c_double()
+    it = ctypes.c_int()
+    dp = ctypes.POINTER(ctypes.c_double)
+
+    def reg(N, p):
+        return L.lsgcpd_register(FAKE, 100, 0.0, FAKE, N, ctypes.byref(p), None, None, ctypes.cast(Ro, dp),
+                                 ctypes.cast(to, dp), ctypes.byref(s2), ctypes.byref(it), None, None, None, FAKE,
+                                 1 << 40, None)
+    assert reg(0, ep) == EINVAL
+    for field, val in (("w", 1.0), ("eta", 1.0), ("group", 2), ("max_iters", -1), ("newton_max", 5000)):
+        bad = pkg.EmParams()
+        L.lsgcpd_em_params_default(ctypes.byref(bad))
+        setattr(bad, field, val)
+        assert reg(100, bad) == EINVAL, field
+    # batch: no problems
+    assert L.lsgcpd_register_batch(None, 0, None, ctypes.cast(Ro, dp), ctypes.cast(to, dp), ctypes.cast(to, dp),
+                                   ctypes.byref(it), ctypes.byref(it), FAKE, 1 << 40, None) == EINVAL
+    # truncation and the depth error model: empty input, non-finite threshold, a zero error model
+    n_out = ctypes.c_int64()
+    assert L.lsgcpd_select_confident(FAKE, FAKE, 0, 0.5, FAKE, FAKE, ctypes.byref(n_out), FAKE, 1 << 40,
+                                     None) == EINVAL
+    assert L.lsgcpd_select_confident(FAKE, FAKE, 10, float("nan"), FAKE, FAKE, ctypes.byref(n_out), FAKE, 1 << 40,
+                                     None) == EINVAL
+    assert L.lsgcpd_depth_confidence(FAKE, 0, 0.0, 0.002, 0.4, FAKE, None) == EINVAL
+    assert L.lsgcpd_depth_confidence(FAKE, 10, 0.0, 0.0, 0.4, FAKE, None) == EINVAL

@@ -1014,7 +1014,8 @@ struct Variant {
 static const Variant kVariants[] = {
     LSG_VARIANT(2, 16, 1, true), LSG_VARIANT(2, 8, 2, true), LSG_VARIANT(4, 8, 1, true), LSG_VARIANT(2, 12, 1, true),
     LSG_VARIANT(4, 4, 2, true),  LSG_VARIANT(2, 8, 2, false), LSG_VARIANT(1, 16, 1, false), LSG_VARIANT(2, 16, 1, true),
-    LSG_VARIANT(2, 14, 1, true), LSG_VARIANT(2, 8, 1, true), LSG_VARIANT(2, 2, 8, true),
+    LSG_VARIANT(2, 14, 1, true), LSG_VARIANT(2, 8, 1, true), LSG_VARIANT(2, 2, 8, true), LSG_VARIANT(1, 2, 8, false),
+    LSG_VARIANT(2, 1, 8, true),
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kDefaultVariant = 3;   // packed, 2 points/thread, 12 consumer warps (tools/estep_speed.py)
@@ -1090,7 +1091,7 @@ static int tc_variant_index() {
 static int g_num_sms = 0;
 static int g_occ[kNumVariants] = {0};
 
-constexpr int kSmallVariant = 10;   // 128-point blocks for problems too small to fill the GPU
+constexpr int kSmallVariant = 12;   // one consumer warp, 64-point blocks: problems too small to fill the GPU
 
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
     const int tvi = tc_variant_index();

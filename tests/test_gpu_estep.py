@@ -119,7 +119,7 @@ def test_estep_invalid_arguments_raise():
         lsg.estep(tgt, X, np.eye(3), np.array([np.nan, 0, 0]), 1e-3, 0.1, V)
 
 
-@pytest.mark.parametrize("variant", range(11))
+@pytest.mark.parametrize("variant", range(13))
 def test_estep_every_kernel_variant(variant, monkeypatch):
     # every compiled CUDA-core kernel variant (scalar / packed f32x2, points per thread, warps), with the
     # tensor-core kernel disabled, gives the same record

@@ -57,8 +57,11 @@ def test_register_teacher_forced_full_scale(name):
     del reg
 
 
-def test_register_with_one_rank_nccl_comm_equals_no_comm():
-    # the communicator path (ncclAllReduce of the 75 moments per iteration) with world size 1
+@pytest.mark.parametrize("no_fuse", ["0", "1"])
+def test_register_with_one_rank_nccl_comm_equals_no_comm(no_fuse, monkeypatch):
+    # the communicator path (ncclAllReduce of the 75 moments per iteration) with world size 1, after the fused
+    # merge + moments kernel (N ≤ 2^17) and after the separate merge / moments kernels (the N > 2^17 path)
+    monkeypatch.setenv("LSGCPD_NO_FUSE", no_fuse)
     import paper_2103_15039_b200 as lsg
     wl = workload("object")
     tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
@@ -74,3 +77,33 @@ def test_register_with_one_rank_nccl_comm_equals_no_comm():
     assert np.array_equal(viac["R"], plain["R"]) and np.array_equal(viac["t"], plain["t"])
     assert viac["sigma2"] == plain["sigma2"]
     np.testing.assert_array_equal(viac["nll"], plain["nll"])
+
+
+def test_estep_indexing_beyond_2_31_record_floats():
+    # maximum-size edge case: N·16 > 2^31 record floats (and a partial buffer twice that), so every source
+    # offset past point 2^27 needs 64-bit indexing in the pair kernels, the merge and the record store.
+    # Source: the tiny workload tiled with a per-copy shift, built on the device from the seeded input by the
+    # same float32 formula the host repeats for the sampled rows.
+    import torch
+    import paper_2103_15039_b200 as lsg
+    from tests.gpu_common import oracle_target32
+    wl, n32, a32, V, ext = oracle_target32("tiny")
+    tgt = lsg.pack_target(to_dev(wl.target), to_dev(n32), to_dev(a32))
+    N = (1 << 27) + 77
+    base = torch.from_numpy(wl.source).cuda()
+    k = torch.arange(N, device="cuda")
+    X = base[k % wl.N] + ((k // wl.N).to(torch.float32) * np.float32(1e-7))[:, None]
+    del k
+    R, t = wl.R_expected, wl.t_expected
+    s2 = 1e-3
+    rec = lsg.estep(tgt, X, R, t, s2, wl.w, V)
+    rng = np.random.default_rng(29)
+    idx = np.unique(np.concatenate([rng.choice(N, 40, replace=False), np.arange(N - 8, N),
+                                    np.arange((1 << 27) - 4, (1 << 27) + 4)]))
+    sub = rec[torch.from_numpy(idx).cuda()].cpu().numpy()
+    del rec, X
+    torch.cuda.empty_cache()
+    xs = wl.source[idx % wl.N] + ((idx // wl.N).astype(np.float32) * np.float32(1e-7))[:, None]
+    ora = oracle.estep(wl.target, n32.astype(np.float64), a32.astype(np.float64), xs.astype(np.float32), R, t, s2,
+                       wl.w, V)
+    assert_record_parity(sub, ora, wl.target, a32, what="N = 2^27 + 77 sampled")

@@ -107,3 +107,25 @@ def test_estep_indexing_beyond_2_31_record_floats():
     ora = oracle.estep(wl.target, n32.astype(np.float64), a32.astype(np.float64), xs.astype(np.float32), R, t, s2,
                        wl.w, V)
     assert_record_parity(sub, ora, wl.target, a32, what="N = 2^27 + 77 sampled")
+
+
+def test_estep_targets_beyond_2_31_bytes():
+    # maximum-size edge case on the target side: M = 2^24 + 5 targets (2.7 GB of prepared target, tile offsets
+    # past 2^31 bytes), every one of them within reach of every source point (the tiny target tiled with a
+    # 1e-7 shift per copy), so the sums run over all 16.8 M targets, against the oracle on sampled points.
+    import paper_2103_15039_b200 as lsg
+    from tests.gpu_common import oracle_target32
+    wl, n32, a32, _, _ = oracle_target32("tiny")
+    M = (1 << 24) + 5
+    k = np.arange(M)
+    Y = wl.target[k % wl.M] + ((k // wl.M).astype(np.float32) * np.float32(1e-7))[:, None]
+    nY, aY = n32[k % wl.M], a32[k % wl.M]
+    del k
+    V, _ = oracle.working_volume(Y)
+    tgt = lsg.pack_target(to_dev(Y), to_dev(nY), to_dev(aY))
+    X = wl.source[:64]
+    R, t = wl.R_expected, wl.t_expected
+    for s2 in (1e-3, 1e-5):
+        rec = lsg.estep(tgt, to_dev(X), R, t, s2, wl.w, V).cpu().numpy()
+        ora = oracle.estep(Y, nY.astype(np.float64), aY.astype(np.float64), X, R, t, s2, wl.w, V)
+        assert_record_parity(rec, ora, Y, aY, what=f"M = 2^24 + 5, s2={s2}")

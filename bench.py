@@ -321,6 +321,7 @@ def main():
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - t0)
         e2e = {"value": pairs_per_step * ne / e2e_s, "unit": UNIT,
+               "registrations_per_s": ne * (world if args.replicas else 1) / e2e_s,
                "h2d_bytes_per_step": int(h_tgt.numel() * 4 + h_src.numel() * 4),
                "d2h_bytes_per_step": int(9 * 8 + 3 * 8 + 8 + 4), "steps": ne,
                "includes": "H2D target+source, lsgcpd_prepare_target, lsgcpd_register, R/t/sigma2 to host"}

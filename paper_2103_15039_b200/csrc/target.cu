@@ -33,7 +33,7 @@ constexpr int kFineRings = LSG_KNN_RMAX;        // fine rings searched before th
 // stats1: [max(-x), max(-y), max(-z), max x, max y, max z, Σx, Σy, Σz]
 __global__ void __launch_bounds__(kRedThreads)
     cloud_stats_kernel(const float* __restrict__ xyz, int64_t M, double* blockpart, double* out, unsigned* counter) {
-    double v[9] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0, 0.0, 0.0};
+    double v[12] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
@@ -41,9 +41,10 @@ __global__ void __launch_bounds__(kRedThreads)
             v[a] = fmax(v[a], -c);
             v[3 + a] = fmax(v[3 + a], c);
             v[6 + a] += c;
+            v[9 + a] = fma(c, c, v[9 + a]);
         }
     }
-    block_reduce_store<9, 6, kRedThreads>(v, blockpart, out, counter);
+    block_reduce_store<12, 6, kRedThreads>(v, blockpart, out, counter);
 }
 
 // stats2 (after the model is built): [max ω, Σ α, Σ ||y - ȳ||², Σ nn-distance, n_degenerate, Σ √(1+α)]
@@ -276,6 +277,20 @@ __device__ __forceinline__ bool ring_search(const float* __restrict__ xyz, doubl
                     const int key = (cx * g.dim[1] + cy) * g.dim[2] + cz;
                     const int s = cstart[key];
                     if (s < 0) continue;
+                    if (cnt == k) {   // skip a cell whose box is farther than the k-th distance (border cells
+                                      // are open outwards: they hold the clamped points beyond the grid)
+                        const int cc3[3] = {cx, cy, cz};
+                        const double pp[3] = {p0, p1, p2};
+                        double d2 = 0.0;
+                        for (int a = 0; a < 3; ++a) {
+                            const double lo = g.lo[a] + cc3[a] * g.h, hi = lo + g.h;
+                            double e = 0.0;
+                            if (pp[a] < lo && cc3[a] > 0) e = lo - pp[a];
+                            else if (pp[a] > hi && cc3[a] < g.dim[a] - 1) e = pp[a] - hi;
+                            d2 = fma(e, e, d2);
+                        }
+                        if (d2 > bd[k - 1]) continue;
+                    }
                     const int e = cend[key];
                     for (int i = s; i < e; ++i) {
                         const int j = sids[i];
@@ -316,24 +331,31 @@ __device__ __forceinline__ bool ring_search(const float* __restrict__ xyz, doubl
     return false;
 }
 
-// Two grids: the fine one (≈ one point per cell for a volume-filling cloud) serves dense regions in ≤ 3
-// rings; points in sparse regions (isolated outliers, far LiDAR returns) restart on a grid 4× coarser
-// instead of scanning O(r³) fine cells.  Both searches are exact, so the result does not depend on which
-// one finished.
+// Up to three grids: the bulk grid (fine cells over the robust box, when the AABB is inflated by outliers),
+// the fine one (≈ one point per cell of the AABB volume) and a grid 4× coarser.  A point tries them in that
+// order, giving up on the first two after kFineRings rings; points in sparse regions (isolated outliers, far
+// LiDAR returns) thus end on the coarse grid instead of scanning O(r³) fine cells.  Every search is exact,
+// so the result does not depend on which one finished.
 __global__ void __launch_bounds__(128)
     knn_surface_kernel(const float* __restrict__ xyz, int64_t M, Grid g, const int* __restrict__ sids,
                        const int* __restrict__ cstart, const int* __restrict__ cend, Grid gc,
                        const int* __restrict__ sids_c, const int* __restrict__ cstart_c,
-                       const int* __restrict__ cend_c, int k, float alpha_max, float lambda,
+                       const int* __restrict__ cend_c, Grid gb, const int* __restrict__ sids_b,
+                       const int* __restrict__ cstart_b, const int* __restrict__ cend_b, int use_bulk, int k,
+                       float alpha_max, float lambda,
                        float* __restrict__ nrm_out, float* __restrict__ kappa_out, float* __restrict__ alpha_out,
                        int* __restrict__ knn_out, float* __restrict__ nnd_out, int* __restrict__ degen_out) {
-    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= M) return;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    // threads take the points in cell order (of the grid searched first): a warp's points share cells, so
+    // their searches visit the same cells and take similar time
+    const int64_t m = (int64_t)(use_bulk ? sids_b[i] : sids[i]);
     const double p0 = xyz[3 * m], p1 = xyz[3 * m + 1], p2 = xyz[3 * m + 2];
     double bd[kMaxK];
     int bi[kMaxK];
     int cnt = 0;
-    if (!ring_search(xyz, p0, p1, p2, g, sids, cstart, cend, k, kFineRings, bd, bi, cnt))
+    if (!(use_bulk && ring_search(xyz, p0, p1, p2, gb, sids_b, cstart_b, cend_b, k, kFineRings, bd, bi, cnt)) &&
+        !ring_search(xyz, p0, p1, p2, g, sids, cstart, cend, k, kFineRings, bd, bi, cnt))
         ring_search(xyz, p0, p1, p2, gc, sids_c, cstart_c, cend_c, k, 1 << 20, bd, bi, cnt);
     // neighbour ids, nearest other point distance
     double nn = 0.0;
@@ -392,6 +414,7 @@ struct PrepLayout {
     size_t blockpart, stats1, stats2, counter, keys, ids, skeys, sids, cstart, cend, nrm, kappa, alpha, nnd,
         degen, cub_tmp, cub_bytes, total;
     size_t skeys_c, sids_c, cstart_c, cend_c;   // the 4× coarser grid of the kNN search
+    size_t skeys_b, sids_b, cstart_b, cend_b;   // the bulk grid (fine cells over the robust box)
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int64_t kMaxCells = 1 << 22;
@@ -427,11 +450,16 @@ static PrepLayout prep_layout(int64_t M, bool with_knn) {
         L.sids_c = o; o += al(sizeof(int) * M);
         L.cstart_c = o; o += al(sizeof(int) * kMaxCellsCoarse);
         L.cend_c = o; o += al(sizeof(int) * kMaxCellsCoarse);
+        L.skeys_b = o; o += al(sizeof(int) * M);
+        L.sids_b = o; o += al(sizeof(int) * M);
+        L.cstart_b = o; o += al(sizeof(int) * kMaxCells);
+        L.cend_b = o; o += al(sizeof(int) * kMaxCells);
         L.cub_bytes = cub_sort_bytes(M);
         L.cub_tmp = o; o += al(L.cub_bytes);
     } else {
         L.keys = L.ids = L.skeys = L.sids = L.cstart = L.cend = L.cub_tmp = L.cub_bytes = 0;
         L.skeys_c = L.sids_c = L.cstart_c = L.cend_c = 0;
+        L.skeys_b = L.sids_b = L.cstart_b = L.cend_b = 0;
     }
     L.total = o;
     return L;
@@ -496,12 +524,12 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     unsigned* ctr = reinterpret_cast<unsigned*>(ws + L.counter);
     LSG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 4, stream));
     cloud_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_xyz, M, bp, st1, ctr);
-    double s1[9];
+    double s1[12];
     LSG_CUDA(cudaMemcpyAsync(s1, st1, sizeof(s1), cudaMemcpyDeviceToHost, stream));
     LSG_CUDA(cudaStreamSynchronize(stream));
     // grid: cell size from the AABB volume per point (≈ 1 point per cell for a volume-filling cloud)
     Grid g;
-    double ext[3], maxe = 0.0;
+    double ext[3], ext_b[3], maxe = 0.0;
     for (int a = 0; a < 3; ++a) {
         g.lo[a] = -s1[a];
         ext[a] = s1[3 + a] + s1[a];
@@ -523,6 +551,35 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
         h *= 1.25;
     }
     g.h = h;
+    // the bulk grid: the same cell rule over mean ± 2.5 sd per axis (clipped to the AABB; points outside are
+    // clamped into its border cells, which keeps every search exact).  Used first when that box is under a
+    // quarter of the AABB volume — a cloud whose AABB is inflated by sparse outliers (the LiDAR config's
+    // 100 m box), where AABB-sized cells would hold hundreds of the dense points.
+    Grid gb = g;
+    double vb = 1.0, va = 1.0;
+    for (int a = 0; a < 3; ++a) {
+        const double mean = s1[6 + a] / (double)M;
+        const double sd = sqrt(fmax(s1[9 + a] / (double)M - mean * mean, 0.0));
+        const double lo = fmax(-s1[a], mean - 2.5 * sd), hi = fmin(s1[3 + a], mean + 2.5 * sd);
+        gb.lo[a] = lo;
+        ext_b[a] = fmax(hi - lo, floor_e);
+        vb *= ext_b[a];
+        va *= fmax(ext[a], floor_e);
+    }
+    const int use_bulk = (vb * 4.0 < va) ? 1 : 0;
+    if (use_bulk) {
+        double hb = cbrt(vb / (double)M) / LSG_KNN_FINE;
+        for (;;) {
+            int64_t cells = 1;
+            for (int a = 0; a < 3; ++a) {
+                gb.dim[a] = (int)fmin(floor(ext_b[a] / hb) + 1.0, 1024.0);
+                cells *= gb.dim[a];
+            }
+            if (cells <= kMaxCells) break;
+            hb *= 1.25;
+        }
+        gb.h = hb;
+    }
     int* keys = reinterpret_cast<int*>(ws + L.keys);
     int* ids = reinterpret_cast<int*>(ws + L.ids);
     int* skeys = reinterpret_cast<int*>(ws + L.skeys);
@@ -554,6 +611,20 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     LSG_CUDA(cudaMemsetAsync(cstart_c, 0xff, sizeof(int) * ncells_c, stream));
     LSG_CUDA(cudaMemsetAsync(cend_c, 0xff, sizeof(int) * ncells_c, stream));
     cell_ranges_kernel<<<nb, 256, 0, stream>>>(skeys_c, M, cstart_c, cend_c);
+    int* sids_b = reinterpret_cast<int*>(ws + L.sids_b);
+    int* cstart_b = reinterpret_cast<int*>(ws + L.cstart_b);
+    int* cend_b = reinterpret_cast<int*>(ws + L.cend_b);
+    if (use_bulk) {
+        int* skeys_b = reinterpret_cast<int*>(ws + L.skeys_b);
+        cell_keys_kernel<<<nb, 256, 0, stream>>>(d_xyz, M, gb, keys, ids);
+        cub_bytes = L.cub_bytes;
+        LSG_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.cub_tmp, cub_bytes, keys, skeys_b, ids, sids_b, (int)M, 0, 22,
+                                                 stream));
+        const int64_t ncells_b = (int64_t)gb.dim[0] * gb.dim[1] * gb.dim[2];
+        LSG_CUDA(cudaMemsetAsync(cstart_b, 0xff, sizeof(int) * ncells_b, stream));
+        LSG_CUDA(cudaMemsetAsync(cend_b, 0xff, sizeof(int) * ncells_b, stream));
+        cell_ranges_kernel<<<nb, 256, 0, stream>>>(skeys_b, M, cstart_b, cend_b);
+    }
     float* nrm = ann && ann->d_normals ? ann->d_normals : reinterpret_cast<float*>(ws + L.nrm);
     float* kap = ann && ann->d_kappa ? ann->d_kappa : reinterpret_cast<float*>(ws + L.kappa);
     float* alp = ann && ann->d_alpha ? ann->d_alpha : reinterpret_cast<float*>(ws + L.alpha);
@@ -561,8 +632,9 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     float* nnd = reinterpret_cast<float*>(ws + L.nnd);
     int* degen = reinterpret_cast<int*>(ws + L.degen);
     knn_surface_kernel<<<(unsigned)((M + 127) / 128), 128, 0, stream>>>(d_xyz, M, g, sids, cstart, cend, gc, sids_c,
-                                                                        cstart_c, cend_c, p.knn_k, p.alpha_max,
-                                                                        p.lambda, nrm, kap, alp, knn, nnd, degen);
+                                                                        cstart_c, cend_c, gb, sids_b, cstart_b, cend_b,
+                                                                        use_bulk, p.knn_k, p.alpha_max, p.lambda, nrm,
+                                                                        kap, alp, knn, nnd, degen);
     LSG_CUDA(cudaGetLastError());
     return finish_target(d_xyz, nrm, alp, nnd, degen, M, p.volume_margin, ws, L, d_target, info, stream);
 }

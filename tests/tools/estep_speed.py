@@ -1,7 +1,7 @@
 """Time lsgcpd_estep per kernel variant (LSGCPD_ESTEP_VARIANT) on BASELINE configs; check sampled parity."""
 import os, sys, time, json
 import numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import synth, oracle
 import paper_2103_15039_b200 as lsg
 from tests.parity import record_errors

@@ -1,7 +1,7 @@
 """Quick check of the tensor-core E step: parity vs the oracle (tiny, sampled scale) and speed vs CUDA-core."""
 import os, sys, time
 import numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import synth, oracle
 import paper_2103_15039_b200 as lsg
 from tests.parity import record_errors

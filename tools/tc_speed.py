@@ -1,4 +1,4 @@
-"""Time lsgcpd_estep on one config for a list of tensor-core variants (no parity; see tc_check.py)."""
+"""Time lsgcpd_estep on one config for a list of tensor-core variants (no parity; see tests/tools/tc_check.py)."""
 import os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

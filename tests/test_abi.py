@@ -78,3 +78,14 @@ def test_oracle_is_not_imported_by_the_product():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower() or f == "__init__.py" and \
                     "import oracle" not in txt, f
+
+
+def test_only_test_infrastructure_imports_the_oracle():
+    # oracle/ is test infrastructure: outside tests/, only __graft_entry__.smoke() and bench.py (cpu_baseline,
+    # --impl reference) may import it; tools/, synth/ and include/ never do
+    pat = re.compile(r"^\s*(import oracle|from oracle\b)", re.M)
+    for top in ("tools", "synth", "include", "examples"):
+        for dirpath, _, files in os.walk(os.path.join(ROOT, top)):
+            for f in files:
+                if f.endswith((".py", ".c", ".h", ".sh")):
+                    assert not pat.search(open(os.path.join(dirpath, f)).read()), os.path.join(dirpath, f)

@@ -16,6 +16,8 @@
 // LDS.128.  Source points live in registers as FP32 hi/lo pairs of x̂ (computed in FP64).
 // Arithmetic: packed f32x2 (FFMA2/FADD2/FMUL2) over two source points per instruction with the
 // target field as a broadcast operand (PACKED), or scalar FP32 (reference variant).
+#include <string.h>
+
 #include "common.cuh"
 #include "estep_dev.cuh"
 #include "kernels.h"
@@ -1119,6 +1121,7 @@ int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
         g_occ[vi] = occ > 0 ? occ : 1;
     }
     Sched s;
+    memset(&s, 0, sizeof(s));
     s.variant = tc ? -1 - vi : vi;   // negative: tensor-core kernel + CUDA-core variant for running max
     s.tc_variant = tvi;
     s.B = (int64_t)V.ppt * V.ncw * 32;

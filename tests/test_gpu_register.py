@@ -165,3 +165,24 @@ def test_fused_em_tail_equals_separate_kernels(name, conf, monkeypatch):
     _close(fused["R"], fused["t"], sep["R"], sep["t"], tgt.extent, tol=1e-9)
     np.testing.assert_allclose(fused["sigma2_trace"], sep["sigma2_trace"], rtol=1e-9)
     np.testing.assert_allclose(fused["nll"], sep["nll"], rtol=1e-10)
+
+
+def test_graph_cache_replay_and_update_match_fresh_graphs(monkeypatch):
+    # lsgcpd_register keeps the instantiated EM-iteration graph of recent calls: a repeated call replays it, a
+    # call with other buffers of the same sizes updates it in place (cudaGraphExecUpdate).  Both must give
+    # exactly what a freshly captured graph gives (LSGCPD_GRAPH_CACHE=0).
+    import paper_2103_15039_b200 as lsg
+    import synth
+    wls = synth.make_batch(3, 800, seed=21)
+    probs = []
+    for w in wls:
+        tgt = lsg.prepare_target(to_dev(w.target), w.knn_k)
+        probs.append(lsg.Registrar(tgt, to_dev(w.source), 25))
+    cached = [p(w=0.1) for p in probs] + [probs[0](w=0.1), probs[1](w=0.2)]
+    monkeypatch.setenv("LSGCPD_GRAPH_CACHE", "0")
+    fresh = [p(w=0.1) for p in probs] + [probs[0](w=0.1), probs[1](w=0.2)]
+    for a, b in zip(cached, fresh):
+        assert a["iters"] == b["iters"] == 25
+        np.testing.assert_array_equal(a["R"], b["R"])
+        np.testing.assert_array_equal(a["t"], b["t"])
+        assert a["sigma2"] == b["sigma2"]

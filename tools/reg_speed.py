@@ -11,7 +11,7 @@ for cfg in os.environ.get("CFGS", "tiny,object,rgbd,lidar").split(","):
     reg = lsg.Registrar(tgt, X, wl.iters)
     out = reg(w=wl.w)
     torch.cuda.synchronize()
-    reps = 5 if wl.M < 20000 else 2
+    reps = 20 if wl.M < 20000 else 2
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     for _ in range(reps):

@@ -260,7 +260,8 @@ __device__ inline bool chol_solve(const double* A, double mu, const double* b, d
 }
 
 // exp of an aff(3) element δ (matrix exponential of the 4×4 [[B, v], [0, 0]]): scaling and squaring with a
-// 16-term Taylor series (‖·‖₁ ≤ 1/4 after scaling: truncation < 1e-30).  Returns the linear block and translation.
+// Taylor series (‖·‖₁ ≤ 1/4 after scaling) summed until a term falls below 1e-18 (at most 16 terms: < 1e-30);
+// Newton steps near convergence need only a few terms.  Returns the linear block and translation.
 __device__ inline void aff_exp(const double* d, double* dA, double* dt) {
     double G[16];
     for (int i = 0; i < 16; ++i) G[i] = 0.0;
@@ -278,12 +279,16 @@ __device__ inline void aff_exp(const double* d, double* dA, double* dt) {
     for (int i = 0; i < 16; ++i) G[i] *= sc;
     double E[16], T[16], T2[16];
     for (int i = 0; i < 16; ++i) E[i] = T[i] = (i % 5 == 0) ? 1.0 : 0.0;
-    for (int k = 1; k <= 16; ++k) {
+    for (int k = 1; k <= 16; ++k) {   // terms shrink by ≥ 4k after scaling: stop once one is below 1e-18
         mat4mul(T, G, T2);
+        double tmax = 0.0;
+        const double ik = 1.0 / (double)k;
         for (int i = 0; i < 16; ++i) {
-            T[i] = T2[i] / (double)k;
+            T[i] = T2[i] * ik;
             E[i] += T[i];
+            tmax = fmax(tmax, fabs(T[i]));
         }
+        if (tmax < 1e-18) break;
     }
     for (int r = 0; r < sq; ++r) {
         mat4mul(E, E, T2);

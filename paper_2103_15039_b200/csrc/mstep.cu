@@ -230,29 +230,39 @@ __device__ inline void se3_exp(const double* d, double* dR, double* dt) {
 // Cholesky solve (A + μI) x = b, K×K.  Returns false if not positive definite.
 template <int K>
 __device__ inline bool chol_solve(const double* A, double mu, const double* b, double* x) {
+    // fully unrolled for K = 6, so L lives in registers (a dynamically indexed L goes to local memory)
     double L[K * K], id[K];   // id[j] = 1 / L_jj: one reciprocal square root per column, no divisions
+#pragma unroll
     for (int i = 0; i < K * K; ++i) L[i] = 0.0;
+#pragma unroll
     for (int j = 0; j < K; ++j) {
         double s = A[j * K + j] + mu;
+#pragma unroll
         for (int k = 0; k < j; ++k) s -= L[j * K + k] * L[j * K + k];
         if (!(s > 0.0)) return false;
         const double r = rsqrt(s);
         id[j] = r;
         L[j * K + j] = s * r;
+#pragma unroll
         for (int i = j + 1; i < K; ++i) {
             double v = A[i * K + j];
+#pragma unroll
             for (int k = 0; k < j; ++k) v -= L[i * K + k] * L[j * K + k];
             L[i * K + j] = v * r;
         }
     }
     double y[K];
+#pragma unroll
     for (int i = 0; i < K; ++i) {
         double v = b[i];
+#pragma unroll
         for (int k = 0; k < i; ++k) v -= L[i * K + k] * y[k];
         y[i] = v * id[i];
     }
+#pragma unroll
     for (int i = K - 1; i >= 0; --i) {
         double v = y[i];
+#pragma unroll
         for (int k = i + 1; k < K; ++k) v -= L[k * K + i] * x[k];
         x[i] = v * id[i];
     }

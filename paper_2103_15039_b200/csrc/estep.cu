@@ -1093,6 +1093,7 @@ static int tc_variant_index() {
 static int g_num_sms = 0;
 static int g_occ[kNumVariants] = {0};
 
+constexpr int kMidVariant = 9, kMidBlk = 2 * 8 * 32;   // packed, 2 points/thread, 8 consumer warps: 512-point blocks
 constexpr int kSmallVariant = 12;   // one consumer warp, 64-point blocks: problems too small to fill the GPU
 
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
@@ -1110,8 +1111,12 @@ int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
         // big blocks — use the small-block CUDA-core kernel so every SM gets work
         const int64_t units_big = (N + kTcVariants[tvi].blk - 1) / kTcVariants[tvi].blk * (M_pad / kTT);
         if (units_big < 2 * (int64_t)g_num_sms) {
+            // 512-point blocks once they give ~3/4 of a unit per SM, else 64-point blocks (the most CTAs):
+            // tools/small_path_sweep.py — 1,000 points 38 µs per EM iteration with 64-point blocks, 2,000 / 3,500
+            // points 44 / 56 µs with 512-point blocks (64-point: 51 / 72; tensor cores: 50 / 59)
             tc = false;
-            vi = kSmallVariant;
+            const int64_t units_mid = (N + kMidBlk - 1) / kMidBlk * (M_pad / kTT);
+            vi = 4 * units_mid >= 3 * (int64_t)g_num_sms ? kMidVariant : kSmallVariant;
         }
     }
     const Variant& V = kVariants[vi];

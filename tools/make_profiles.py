@@ -23,6 +23,9 @@ for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
 open(os.path.join(P, f"{out}_launches.txt"), "w").write("\n".join(lines) + "\n")
 shutil.copy(os.path.join(G, f"launches_{tag}.csv"), os.path.join(P, f"{out}_launches.csv"))
 rep = os.path.join(G, f"prof_estep_{tag}.ncu-rep")
+if not os.path.exists(rep):   # launch list only (the E-step kernel's full capture is an earlier round's)
+    print("\n".join(lines[:14]))
+    sys.exit(0)
 raw = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()))
 d = dict(zip(raw[0], raw[2])); u = dict(zip(raw[0], raw[1]))
 keys = ['Kernel Name', 'gpu__time_duration.sum', 'launch__grid_size', 'launch__block_size', 'launch__registers_per_thread',

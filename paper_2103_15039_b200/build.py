@@ -37,14 +37,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
-    objs = []
-    for src in sources():
+    objs, procs = [], []
+    for src in sources():   # one nvcc per translation unit, in parallel
         obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
         cmd = [nvcc, *ARCH, *FLAGS, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
-        subprocess.check_call(cmd)
+        procs.append((cmd, subprocess.Popen(cmd)))
         objs.append(obj)
+    for cmd, pr in procs:
+        if pr.wait() != 0:
+            raise subprocess.CalledProcessError(pr.returncode, cmd)
     tmp = SO + ".tmp%d" % os.getpid()
     subprocess.check_call([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, SO)

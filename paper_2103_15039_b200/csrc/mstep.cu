@@ -310,6 +310,55 @@ __device__ inline void aff_exp(const double* d, double* dA, double* dt) {
     }
 }
 
+// (Θ̃ E_k)[0:3, :] row-major (3 × 4) for the basis of basisK<K>, without a dynamically indexed E_k (which
+// would live in local memory): se(3) rotations give ±columns of R, translations a column of R; aff(3)'s
+// e_i e_jᵀ puts column i of A in column j.  The translation t never enters (E_k's last row is 0).
+template <int K>
+__device__ __forceinline__ void jacobian_col(int k, const double* R, const double* /*t*/, double* P) {
+#pragma unroll
+    for (int r = 0; r < 12; ++r) P[r] = 0.0;
+    if constexpr (K == 6) {
+        switch (k) {
+            case 0:
+#pragma unroll
+                for (int i = 0; i < 3; ++i) { P[4 * i + 1] = R[3 * i + 2]; P[4 * i + 2] = -R[3 * i + 1]; }
+                break;
+            case 1:
+#pragma unroll
+                for (int i = 0; i < 3; ++i) { P[4 * i + 0] = -R[3 * i + 2]; P[4 * i + 2] = R[3 * i + 0]; }
+                break;
+            case 2:
+#pragma unroll
+                for (int i = 0; i < 3; ++i) { P[4 * i + 0] = R[3 * i + 1]; P[4 * i + 1] = -R[3 * i + 0]; }
+                break;
+            case 3:
+#pragma unroll
+                for (int i = 0; i < 3; ++i) P[4 * i + 3] = R[3 * i + 0];
+                break;
+            case 4:
+#pragma unroll
+                for (int i = 0; i < 3; ++i) P[4 * i + 3] = R[3 * i + 1];
+                break;
+            default:
+#pragma unroll
+                for (int i = 0; i < 3; ++i) P[4 * i + 3] = R[3 * i + 2];
+                break;
+        }
+    } else {
+        // k < 9: e_a e_bᵀ (a = k / 3, b = k % 3) → column b = A[:, a];  k ≥ 9: column 3 = A[:, k - 9]
+        const int a = k < 9 ? k / 3 : k - 9, b = k < 9 ? k % 3 : 3;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (c == b) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const double v = a == 0 ? R[3 * i] : (a == 1 ? R[3 * i + 1] : R[3 * i + 2]);
+                    P[4 * i + c] = v;
+                }
+            }
+    }
+}
+
 // One warp: the dense algebra (v = U + 𝔾Δθ, J, 𝔾J, ∇, H) is spread over the lanes.  The damping loop
 // (Cholesky K×K, exp, candidate q) runs redundantly in every lane on identical data, so its branches are
 // warp-uniform and no lane waits on a shared-memory handoff; the candidate q is a 12-lane dot product
@@ -371,11 +420,11 @@ __device__ __noinline__ void newton_body(IterState* st, const double* __restrict
             for (int c = 0; c < 12; ++c) gr = fma(mo.GG[lane][c], dth[c], gr);
             v[lane] = mo.U[lane] + gr;                // ½ ∇_θ q
         } else if (lane < 12 + K) {
-            const int k = lane - 12;                  // dθ/dξ_k = (Θ̃ E_k)[0:3,:]
-            double Ek[16], P4[16];
-            basisK<K>(k, Ek);
-            mat4mul(Gt, Ek, P4);
-            for (int r = 0; r < 12; ++r) J[k][r] = P4[r];
+            const int k = lane - 12;                  // dθ/dξ_k = (Θ̃ E_k)[0:3,:], written out per generator
+            double P[12];
+            jacobian_col<K>(k, Rs, tsh, P);
+#pragma unroll
+            for (int r = 0; r < 12; ++r) J[k][r] = P[r];
         }
         __syncwarp();
         for (int e = lane; e < K * 12; e += 32) {     // 𝔾 J_k

@@ -331,32 +331,13 @@ __device__ __forceinline__ bool ring_search(const float* __restrict__ xyz, doubl
     return false;
 }
 
-// Up to three grids: the bulk grid (fine cells over the robust box, when the AABB is inflated by outliers),
-// the fine one (≈ one point per cell of the AABB volume) and a grid 4× coarser.  A point tries them in that
-// order, giving up on the first two after kFineRings rings; points in sparse regions (isolated outliers, far
-// LiDAR returns) thus end on the coarse grid instead of scanning O(r³) fine cells.  Every search is exact,
-// so the result does not depend on which one finished.
-__global__ void __launch_bounds__(128)
-    knn_surface_kernel(const float* __restrict__ xyz, int64_t M, Grid g, const int* __restrict__ sids,
-                       const int* __restrict__ cstart, const int* __restrict__ cend, Grid gc,
-                       const int* __restrict__ sids_c, const int* __restrict__ cstart_c,
-                       const int* __restrict__ cend_c, Grid gb, const int* __restrict__ sids_b,
-                       const int* __restrict__ cstart_b, const int* __restrict__ cend_b, int use_bulk, int k,
-                       float alpha_max, float lambda,
-                       float* __restrict__ nrm_out, float* __restrict__ kappa_out, float* __restrict__ alpha_out,
-                       int* __restrict__ knn_out, float* __restrict__ nnd_out, int* __restrict__ degen_out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M) return;
-    // threads take the points in cell order (of the grid searched first): a warp's points share cells, so
-    // their searches visit the same cells and take similar time
-    const int64_t m = (int64_t)(use_bulk ? sids_b[i] : sids[i]);
-    const double p0 = xyz[3 * m], p1 = xyz[3 * m + 1], p2 = xyz[3 * m + 2];
-    double bd[kMaxK];
-    int bi[kMaxK];
-    int cnt = 0;
-    if (!(use_bulk && ring_search(xyz, p0, p1, p2, gb, sids_b, cstart_b, cend_b, k, kFineRings, bd, bi, cnt)) &&
-        !ring_search(xyz, p0, p1, p2, g, sids, cstart, cend, k, kFineRings, bd, bi, cnt))
-        ring_search(xyz, p0, p1, p2, gc, sids_c, cstart_c, cend_c, k, 1 << 20, bd, bi, cnt);
+// Outputs of target m from its k nearest neighbours bi[0..k) (ascending distance bd): the nearest other point
+// distance, the centred scatter, a cyclic Jacobi eigen-solve (FP64), n, κ and α (Eq. 3, tanh form).
+__device__ __noinline__ void finish_point(const float* __restrict__ xyz, int64_t m, const double* bd, const int* bi,
+                                          int k, float alpha_max, float lambda, float* __restrict__ nrm_out,
+                                          float* __restrict__ kappa_out, float* __restrict__ alpha_out,
+                                          int* __restrict__ knn_out, float* __restrict__ nnd_out,
+                                          int* __restrict__ degen_out) {
     // neighbour ids, nearest other point distance
     double nn = 0.0;
     for (int i = 0; i < k; ++i) {
@@ -406,7 +387,176 @@ __global__ void __launch_bounds__(128)
     for (int a = 0; a < 3; ++a) nrm_out[3 * m + a] = (float)n[a];
     kappa_out[m] = (float)kappa;
     alpha_out[m] = (float)alpha;
-    degen_out[m] = degenerate;
+    degen_out[m] = degenerate;}
+
+// Up to three grids: the bulk grid (fine cells over the robust box, when the AABB is inflated by outliers),
+// the fine one (≈ one point per cell of the AABB volume) and a grid 4× coarser.  A point tries them in that
+// order, giving up on the first two after kFineRings rings; points in sparse regions (isolated outliers, far
+// LiDAR returns) thus end on the coarse grid instead of scanning O(r³) fine cells.  Every search is exact,
+// so the result does not depend on which one finished.
+__global__ void __launch_bounds__(128)
+    knn_surface_kernel(const float* __restrict__ xyz, int64_t M, Grid g, const int* __restrict__ sids,
+                       const int* __restrict__ cstart, const int* __restrict__ cend, Grid gc,
+                       const int* __restrict__ sids_c, const int* __restrict__ cstart_c,
+                       const int* __restrict__ cend_c, Grid gb, const int* __restrict__ sids_b,
+                       const int* __restrict__ cstart_b, const int* __restrict__ cend_b, int use_bulk, int k,
+                       float alpha_max, float lambda,
+                       float* __restrict__ nrm_out, float* __restrict__ kappa_out, float* __restrict__ alpha_out,
+                       int* __restrict__ knn_out, float* __restrict__ nnd_out, int* __restrict__ degen_out,
+                       int* __restrict__ hard, int* __restrict__ nhard) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    // threads take the points in cell order (of the grid searched first): a warp's points share cells, so
+    // their searches visit the same cells and take similar time
+    const int64_t m = (int64_t)(use_bulk ? sids_b[i] : sids[i]);
+    const double p0 = xyz[3 * m], p1 = xyz[3 * m + 1], p2 = xyz[3 * m + 2];
+    double bd[kMaxK];
+    int bi[kMaxK];
+    int cnt = 0;
+    if (!(use_bulk && ring_search(xyz, p0, p1, p2, gb, sids_b, cstart_b, cend_b, k, kFineRings, bd, bi, cnt)) &&
+        !ring_search(xyz, p0, p1, p2, g, sids, cstart, cend, k, kFineRings, bd, bi, cnt)) {
+        hard[atomicAdd(nhard, 1)] = (int)m;   // knn_hard_kernel: one warp per such point on the coarse grid
+        return;
+    }
+    finish_point(xyz, m, bd, bi, k, alpha_max, lambda, nrm_out, kappa_out, alpha_out, knn_out, nnd_out, degen_out);
+}
+
+// The points whose search left the first two grids (isolated outliers, far returns): one warp per point on the
+// coarse grid.  Ring by ring, the lanes split the shell's points (cell by cell, each cell's points strided over
+// the warp), each keeping its own k best (distance, id);
+// the warp then merges the 32 lists (k rounds of a warp-wide lexicographic minimum) into the ring's k best,
+// whose k-th distance prunes the next rings' cells and decides the stop exactly as ring_search does.  Lane 0
+// finishes the point.  Same result as the one-thread search (exact k nearest, ties → lower id).
+__global__ void __launch_bounds__(128)
+    knn_hard_kernel(const float* __restrict__ xyz, Grid g, const int* __restrict__ sids, const int* __restrict__ cstart,
+                    const int* __restrict__ cend, int k, float alpha_max, float lambda, float* __restrict__ nrm_out,
+                    float* __restrict__ kappa_out, float* __restrict__ alpha_out, int* __restrict__ knn_out,
+                    float* __restrict__ nnd_out, int* __restrict__ degen_out, const int* __restrict__ hard,
+                    const int* __restrict__ nhard) {
+    __shared__ double sd[4][kMaxK];
+    __shared__ int si[4][kMaxK];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    const int nh = *nhard;
+    for (int h = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); h < nh; h += nw) {
+        const int64_t m = hard[h];
+        const double p0 = xyz[3 * m], p1 = xyz[3 * m + 1], p2 = xyz[3 * m + 2];
+        const double pp[3] = {p0, p1, p2};
+        const int c0 = cell_coord(p0, g.lo[0], g.h, g.dim[0]);
+        const int c1 = cell_coord(p1, g.lo[1], g.h, g.dim[1]);
+        const int c2 = cell_coord(p2, g.lo[2], g.h, g.dim[2]);
+        const int cc[3] = {c0, c1, c2};
+        double bd[kMaxK];
+        int bi[kMaxK];
+        int cnt = 0;
+        double gk = INFINITY;   // the warp's k-th distance so far (after the last merge)
+        for (int r = 0;; ++r) {
+            const int x0 = max(c0 - r, 0), x1 = min(c0 + r, g.dim[0] - 1);
+            const int y0 = max(c1 - r, 0), y1 = min(c1 + r, g.dim[1] - 1);
+            const int z0 = max(c2 - r, 0), z1 = min(c2 + r, g.dim[2] - 1);
+            const int nx = x1 - x0 + 1, ny = y1 - y0 + 1, nz = z1 - z0 + 1;
+            const int64_t ncube = (int64_t)nx * ny * nz;
+            // 32 cube cells at a time, one per lane; then every lane scans a share of each kept cell's points
+            // (a dense cell is split over the warp instead of stalling one lane)
+            for (int64_t q0 = 0; q0 < ncube; q0 += 32) {
+                const int64_t q = q0 + lane;
+                int s0 = -1, e0 = -1;
+                if (q < ncube) {
+                    const int cx = x0 + (int)(q / ((int64_t)ny * nz));
+                    const int cy = y0 + (int)((q / nz) % ny);
+                    const int cz = z0 + (int)(q % nz);
+                    const bool shell = cx == c0 - r || cx == c0 + r || cy == c1 - r || cy == c1 + r ||
+                                       cz == c2 - r || cz == c2 + r;   // interior cells: earlier rings
+                    const int key = (cx * g.dim[1] + cy) * g.dim[2] + cz;
+                    if (shell && cstart[key] >= 0) {
+                        const int cell[3] = {cx, cy, cz};
+                        double d2c = 0.0;
+                        for (int a = 0; a < 3; ++a) {
+                            const double lo = g.lo[a] + cell[a] * g.h, hi = lo + g.h;
+                            double e = 0.0;
+                            if (pp[a] < lo && cell[a] > 0) e = lo - pp[a];
+                            else if (pp[a] > hi && cell[a] < g.dim[a] - 1) e = pp[a] - hi;
+                            d2c = fma(e, e, d2c);
+                        }
+                        if (!(d2c > gk)) {
+                            s0 = cstart[key];
+                            e0 = cend[key];
+                        }
+                    }
+                }
+                unsigned todo = __ballot_sync(0xffffffffu, s0 >= 0);
+                while (todo) {
+                    const int src = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const int a0 = __shfl_sync(0xffffffffu, s0, src), a1 = __shfl_sync(0xffffffffu, e0, src);
+                    for (int t = a0 + lane; t < a1; t += 32) {
+                        const int j = sids[t];
+                        const double dx = (double)xyz[3 * (int64_t)j] - p0, dy = (double)xyz[3 * (int64_t)j + 1] - p1,
+                                     dz = (double)xyz[3 * (int64_t)j + 2] - p2;
+                        const double d = dx * dx + dy * dy + dz * dz;
+                        if (cnt == k && !(d < bd[k - 1] || (d == bd[k - 1] && j < bi[k - 1]))) continue;
+                        int pos = cnt < k ? cnt : k - 1;
+                        while (pos > 0 && (d < bd[pos - 1] || (d == bd[pos - 1] && j < bi[pos - 1]))) {
+                            bd[pos] = bd[pos - 1];
+                            bi[pos] = bi[pos - 1];
+                            --pos;
+                        }
+                        bd[pos] = d;
+                        bi[pos] = j;
+                        if (cnt < k) ++cnt;
+                    }
+                }
+            }
+            // merge the lanes' lists: k rounds of a warp-wide minimum over the lanes' next entries
+            int head = 0, total = 0;
+            for (int t = 0; t < k; ++t) {
+                double d = head < cnt ? bd[head] : INFINITY;
+                int id = head < cnt ? bi[head] : 0x7fffffff;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double od = __shfl_xor_sync(0xffffffffu, d, o);
+                    const int oid = __shfl_xor_sync(0xffffffffu, id, o);
+                    if (od < d || (od == d && oid < id)) {
+                        d = od;
+                        id = oid;
+                    }
+                }
+                if (head < cnt && bd[head] == d && bi[head] == id) ++head;
+                if (lane == 0) {
+                    sd[wib][t] = d;
+                    si[wib][t] = id;
+                }
+                if (d < INFINITY) ++total;
+            }
+            __syncwarp();
+            if (total == k) gk = sd[wib][k - 1];
+            // stop as ring_search does: every cell searched, or the k-th distance inside the searched box
+            double bound = INFINITY;
+            bool all_covered = true;
+            for (int a = 0; a < 3; ++a) {
+                if (cc[a] - r > 0) {
+                    bound = fmin(bound, pp[a] - (g.lo[a] + (cc[a] - r) * g.h));
+                    all_covered = false;
+                }
+                if (cc[a] + r < g.dim[a] - 1) {
+                    bound = fmin(bound, g.lo[a] + (cc[a] + r + 1) * g.h - pp[a]);
+                    all_covered = false;
+                }
+            }
+            if (all_covered || (total == k && gk < bound * bound)) break;
+            __syncwarp();
+        }
+        if (lane == 0) {
+            double fd[kMaxK];
+            int fi[kMaxK];
+            for (int t = 0; t < k; ++t) {
+                fd[t] = sd[wib][t];
+                fi[t] = si[wib][t];
+            }
+            finish_point(xyz, m, fd, fi, k, alpha_max, lambda, nrm_out, kappa_out, alpha_out, knn_out, nnd_out,
+                         degen_out);
+        }
+        __syncwarp();
+    }
 }
 
 // ---- host side -------------------------------------------------------------------------------------
@@ -415,6 +565,7 @@ struct PrepLayout {
         degen, cub_tmp, cub_bytes, total;
     size_t skeys_c, sids_c, cstart_c, cend_c;   // the 4× coarser grid of the kNN search
     size_t skeys_b, sids_b, cstart_b, cend_b;   // the bulk grid (fine cells over the robust box)
+    size_t hard;                                // points left to the coarse grid (knn_hard_kernel)
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int64_t kMaxCells = 1 << 22;
@@ -450,6 +601,7 @@ static PrepLayout prep_layout(int64_t M, bool with_knn) {
         L.sids_c = o; o += al(sizeof(int) * M);
         L.cstart_c = o; o += al(sizeof(int) * kMaxCellsCoarse);
         L.cend_c = o; o += al(sizeof(int) * kMaxCellsCoarse);
+        L.hard = o; o += al(sizeof(int) * (M + 1));   // [0] = count, then the point ids
         L.skeys_b = o; o += al(sizeof(int) * M);
         L.sids_b = o; o += al(sizeof(int) * M);
         L.cstart_b = o; o += al(sizeof(int) * kMaxCells);
@@ -459,7 +611,7 @@ static PrepLayout prep_layout(int64_t M, bool with_knn) {
     } else {
         L.keys = L.ids = L.skeys = L.sids = L.cstart = L.cend = L.cub_tmp = L.cub_bytes = 0;
         L.skeys_c = L.sids_c = L.cstart_c = L.cend_c = 0;
-        L.skeys_b = L.sids_b = L.cstart_b = L.cend_b = 0;
+        L.skeys_b = L.sids_b = L.cstart_b = L.cend_b = L.hard = 0;
     }
     L.total = o;
     return L;
@@ -631,10 +783,14 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     int* knn = ann ? ann->d_knn : nullptr;
     float* nnd = reinterpret_cast<float*>(ws + L.nnd);
     int* degen = reinterpret_cast<int*>(ws + L.degen);
+    int* nhard = reinterpret_cast<int*>(ws + L.hard);
+    LSG_CUDA(cudaMemsetAsync(nhard, 0, sizeof(int), stream));
     knn_surface_kernel<<<(unsigned)((M + 127) / 128), 128, 0, stream>>>(d_xyz, M, g, sids, cstart, cend, gc, sids_c,
                                                                         cstart_c, cend_c, gb, sids_b, cstart_b, cend_b,
                                                                         use_bulk, p.knn_k, p.alpha_max, p.lambda, nrm,
-                                                                        kap, alp, knn, nnd, degen);
+                                                                        kap, alp, knn, nnd, degen, nhard + 1, nhard);
+    knn_hard_kernel<<<(unsigned)(4 * 148), 128, 0, stream>>>(d_xyz, gc, sids_c, cstart_c, cend_c, p.knn_k, p.alpha_max,
+                                                             p.lambda, nrm, kap, alp, knn, nnd, degen, nhard + 1, nhard);
     LSG_CUDA(cudaGetLastError());
     return finish_target(d_xyz, nrm, alp, nnd, degen, M, p.volume_margin, ws, L, d_target, info, stream);
 }

@@ -212,6 +212,15 @@ __global__ void cell_keys_kernel(const float* __restrict__ xyz, int64_t M, Grid 
     ids[m] = (int)m;
 }
 
+// A grid's points in its cell order, padded to 16 B: the searches read a cell's points contiguously.
+__global__ void gather_pts_kernel(const float* __restrict__ xyz, const int* __restrict__ sids, int64_t M,
+                                  float4* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int64_t j = sids[i];
+    out[i] = make_float4(xyz[3 * j], xyz[3 * j + 1], xyz[3 * j + 2], 0.f);
+}
+
 __global__ void cell_ranges_kernel(const int* __restrict__ skeys, int64_t M, int* cstart, int* cend) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= M) return;
@@ -259,7 +268,7 @@ __device__ inline void jacobi3(double A[3][3], double V[3][3]) {
 // Exact k nearest neighbours of p (self included, ties → lower id) by ring search over the cells of `g`:
 // rings r = 0, 1, … until the k-th distance is below the distance to the unsearched region.  Gives up
 // (returns false) after ring rmax; the caller then restarts on a coarser grid.
-__device__ __forceinline__ bool ring_search(const float* __restrict__ xyz, double p0, double p1, double p2,
+__device__ __forceinline__ bool ring_search(const float4* __restrict__ pts, double p0, double p1, double p2,
                                             const Grid& g, const int* __restrict__ sids,
                                             const int* __restrict__ cstart, const int* __restrict__ cend, int k,
                                             int rmax, double* bd, int* bi, int& cnt) {
@@ -294,8 +303,8 @@ __device__ __forceinline__ bool ring_search(const float* __restrict__ xyz, doubl
                     const int e = cend[key];
                     for (int i = s; i < e; ++i) {
                         const int j = sids[i];
-                        const double dx = (double)xyz[3 * (int64_t)j] - p0, dy = (double)xyz[3 * (int64_t)j + 1] - p1,
-                                     dz = (double)xyz[3 * (int64_t)j + 2] - p2;
+                        const float4 q = pts[i];   // the grid's points in cell order: a cell is contiguous
+                        const double dx = (double)q.x - p0, dy = (double)q.y - p1, dz = (double)q.z - p2;
                         const double d = dx * dx + dy * dy + dz * dz;
                         if (cnt == k && !(d < bd[k - 1] || (d == bd[k - 1] && j < bi[k - 1]))) continue;
                         int pos = cnt < k ? cnt : k - 1;
@@ -403,7 +412,8 @@ __global__ void __launch_bounds__(128)
                        float alpha_max, float lambda,
                        float* __restrict__ nrm_out, float* __restrict__ kappa_out, float* __restrict__ alpha_out,
                        int* __restrict__ knn_out, float* __restrict__ nnd_out, int* __restrict__ degen_out,
-                       int* __restrict__ hard, int* __restrict__ nhard) {
+                       int* __restrict__ hard, int* __restrict__ nhard, const float4* __restrict__ pts_f,
+                       const float4* __restrict__ pts_b) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= M) return;
     // threads take the points in cell order (of the grid searched first): a warp's points share cells, so
@@ -413,8 +423,8 @@ __global__ void __launch_bounds__(128)
     double bd[kMaxK];
     int bi[kMaxK];
     int cnt = 0;
-    if (!(use_bulk && ring_search(xyz, p0, p1, p2, gb, sids_b, cstart_b, cend_b, k, kFineRings, bd, bi, cnt)) &&
-        !ring_search(xyz, p0, p1, p2, g, sids, cstart, cend, k, kFineRings, bd, bi, cnt)) {
+    if (!(use_bulk && ring_search(pts_b, p0, p1, p2, gb, sids_b, cstart_b, cend_b, k, kFineRings, bd, bi, cnt)) &&
+        !ring_search(pts_f, p0, p1, p2, g, sids, cstart, cend, k, kFineRings, bd, bi, cnt)) {
         hard[atomicAdd(nhard, 1)] = (int)m;   // knn_hard_kernel: one warp per such point on the coarse grid
         return;
     }
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(128)
                     const int* __restrict__ cend, int k, float alpha_max, float lambda, float* __restrict__ nrm_out,
                     float* __restrict__ kappa_out, float* __restrict__ alpha_out, int* __restrict__ knn_out,
                     float* __restrict__ nnd_out, int* __restrict__ degen_out, const int* __restrict__ hard,
-                    const int* __restrict__ nhard) {
+                    const int* __restrict__ nhard, const float4* __restrict__ pts) {
     __shared__ double sd[4][kMaxK];
     __shared__ int si[4][kMaxK];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -491,8 +501,8 @@ __global__ void __launch_bounds__(128)
                     const int a0 = __shfl_sync(0xffffffffu, s0, src), a1 = __shfl_sync(0xffffffffu, e0, src);
                     for (int t = a0 + lane; t < a1; t += 32) {
                         const int j = sids[t];
-                        const double dx = (double)xyz[3 * (int64_t)j] - p0, dy = (double)xyz[3 * (int64_t)j + 1] - p1,
-                                     dz = (double)xyz[3 * (int64_t)j + 2] - p2;
+                        const float4 q = pts[t];
+                        const double dx = (double)q.x - p0, dy = (double)q.y - p1, dz = (double)q.z - p2;
                         const double d = dx * dx + dy * dy + dz * dz;
                         if (cnt == k && !(d < bd[k - 1] || (d == bd[k - 1] && j < bi[k - 1]))) continue;
                         int pos = cnt < k ? cnt : k - 1;
@@ -566,6 +576,7 @@ struct PrepLayout {
     size_t skeys_c, sids_c, cstart_c, cend_c;   // the 4× coarser grid of the kNN search
     size_t skeys_b, sids_b, cstart_b, cend_b;   // the bulk grid (fine cells over the robust box)
     size_t hard;                                // points left to the coarse grid (knn_hard_kernel)
+    size_t pts_f, pts_c, pts_b;                 // float4 copies of the points in each grid's cell order
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int64_t kMaxCells = 1 << 22;
@@ -602,6 +613,9 @@ static PrepLayout prep_layout(int64_t M, bool with_knn) {
         L.cstart_c = o; o += al(sizeof(int) * kMaxCellsCoarse);
         L.cend_c = o; o += al(sizeof(int) * kMaxCellsCoarse);
         L.hard = o; o += al(sizeof(int) * (M + 1));   // [0] = count, then the point ids
+        L.pts_f = o; o += al(sizeof(float4) * M);       // each grid's points in its cell order
+        L.pts_c = o; o += al(sizeof(float4) * M);
+        L.pts_b = o; o += al(sizeof(float4) * M);
         L.skeys_b = o; o += al(sizeof(int) * M);
         L.sids_b = o; o += al(sizeof(int) * M);
         L.cstart_b = o; o += al(sizeof(int) * kMaxCells);
@@ -612,6 +626,7 @@ static PrepLayout prep_layout(int64_t M, bool with_knn) {
         L.keys = L.ids = L.skeys = L.sids = L.cstart = L.cend = L.cub_tmp = L.cub_bytes = 0;
         L.skeys_c = L.sids_c = L.cstart_c = L.cend_c = 0;
         L.skeys_b = L.sids_b = L.cstart_b = L.cend_b = L.hard = 0;
+        L.pts_f = L.pts_c = L.pts_b = 0;
     }
     L.total = o;
     return L;
@@ -746,6 +761,8 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     LSG_CUDA(cudaMemsetAsync(cstart, 0xff, sizeof(int) * ncells, stream));
     LSG_CUDA(cudaMemsetAsync(cend, 0xff, sizeof(int) * ncells, stream));
     cell_ranges_kernel<<<nb, 256, 0, stream>>>(skeys, M, cstart, cend);
+    float4* pts_f = reinterpret_cast<float4*>(ws + L.pts_f);
+    gather_pts_kernel<<<nb, 256, 0, stream>>>(d_xyz, sids, M, pts_f);
     // the coarse grid (keys and ids scratch reused: the fine sort has consumed them)
     Grid gc = g;
     gc.h = g.h * kCoarse;
@@ -763,6 +780,9 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     LSG_CUDA(cudaMemsetAsync(cstart_c, 0xff, sizeof(int) * ncells_c, stream));
     LSG_CUDA(cudaMemsetAsync(cend_c, 0xff, sizeof(int) * ncells_c, stream));
     cell_ranges_kernel<<<nb, 256, 0, stream>>>(skeys_c, M, cstart_c, cend_c);
+    float4* pts_c = reinterpret_cast<float4*>(ws + L.pts_c);
+    gather_pts_kernel<<<nb, 256, 0, stream>>>(d_xyz, sids_c, M, pts_c);
+    float4* pts_b = reinterpret_cast<float4*>(ws + L.pts_b);
     int* sids_b = reinterpret_cast<int*>(ws + L.sids_b);
     int* cstart_b = reinterpret_cast<int*>(ws + L.cstart_b);
     int* cend_b = reinterpret_cast<int*>(ws + L.cend_b);
@@ -776,6 +796,7 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
         LSG_CUDA(cudaMemsetAsync(cstart_b, 0xff, sizeof(int) * ncells_b, stream));
         LSG_CUDA(cudaMemsetAsync(cend_b, 0xff, sizeof(int) * ncells_b, stream));
         cell_ranges_kernel<<<nb, 256, 0, stream>>>(skeys_b, M, cstart_b, cend_b);
+        gather_pts_kernel<<<nb, 256, 0, stream>>>(d_xyz, sids_b, M, pts_b);
     }
     float* nrm = ann && ann->d_normals ? ann->d_normals : reinterpret_cast<float*>(ws + L.nrm);
     float* kap = ann && ann->d_kappa ? ann->d_kappa : reinterpret_cast<float*>(ws + L.kappa);
@@ -788,9 +809,11 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     knn_surface_kernel<<<(unsigned)((M + 127) / 128), 128, 0, stream>>>(d_xyz, M, g, sids, cstart, cend, gc, sids_c,
                                                                         cstart_c, cend_c, gb, sids_b, cstart_b, cend_b,
                                                                         use_bulk, p.knn_k, p.alpha_max, p.lambda, nrm,
-                                                                        kap, alp, knn, nnd, degen, nhard + 1, nhard);
+                                                                        kap, alp, knn, nnd, degen, nhard + 1, nhard,
+                                                                        pts_f, pts_b);
     knn_hard_kernel<<<(unsigned)(4 * 148), 128, 0, stream>>>(d_xyz, gc, sids_c, cstart_c, cend_c, p.knn_k, p.alpha_max,
-                                                             p.lambda, nrm, kap, alp, knn, nnd, degen, nhard + 1, nhard);
+                                                             p.lambda, nrm, kap, alp, knn, nnd, degen, nhard + 1, nhard,
+                                                             pts_c);
     LSG_CUDA(cudaGetLastError());
     return finish_target(d_xyz, nrm, alp, nnd, degen, M, p.volume_margin, ws, L, d_target, info, stream);
 }

@@ -75,3 +75,19 @@ def test_prepare_degenerate_inputs():
     np.testing.assert_allclose(ann["alpha"].cpu().numpy(), 0.0, atol=1e-6)
     with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
         lsg.prepare_target(to_dev(np.zeros((2, 3), np.float32)))
+
+
+@pytest.mark.parametrize("k", [3, 10, 32])
+def test_prepare_knn_dense_cluster_with_far_outliers(k):
+    # the three search paths of the kNN at once: a dense cluster (bulk grid: its box is far smaller than the
+    # AABB the outliers inflate), points beside it (fine grid) and isolated outliers far out (one warp each on
+    # the coarse grid); every point's k nearest against the brute-force oracle
+    import paper_2103_15039_b200 as lsg
+    rng = np.random.default_rng(41)
+    dense = rng.normal(0.0, 0.01, (3000, 3))
+    plane = np.c_[rng.uniform(-0.3, 0.3, (600, 2)), rng.normal(0.0, 1e-3, 600)]
+    far = rng.uniform(-50.0, 50.0, (250, 3))
+    Y = np.concatenate([dense, plane, far]).astype(np.float32)
+    tgt, ann = lsg.prepare_target(to_dev(Y), k, annotations=True)
+    tg = oracle.prepare_target(Y, k)
+    _check_stage(Y, ann, tg, np.arange(Y.shape[0]), k)

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Benchmark: LSG-CPD E-step pair evaluations/s on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config scale] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config scale|batch|tiny|object|rgbd|lidar] [--replicas] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL)
 
 A step is one full registration of the workload through the library (lsgcpd_register: σ²₀, then
@@ -192,10 +192,156 @@ def run_reference(args, wl, rank):
     print(json.dumps(line), flush=True)
 
 
+BATCH_B, BATCH_N, BATCH_ITERS = 550, 3500, 50
+
+
+def batch_oracle_rate(wls, budget_s: float = 12.0):
+    """The FP64 oracle E step on whole batch problems, one after another, until ~budget_s of CPU work."""
+    import oracle
+    cores = int(oracle._lib.lib().ora_max_threads())
+    rng = np.random.default_rng(0)
+    pairs, t_all, used = 0.0, 0.0, 0
+    for wl in wls:
+        n = rng.standard_normal(wl.target.shape)
+        n /= np.linalg.norm(n, axis=1, keepdims=True)
+        a = rng.uniform(0, 50, wl.M)
+        V, _ = oracle.working_volume(wl.target)
+        t0 = time.perf_counter()
+        oracle.estep(wl.target, n, a, wl.source, wl.R_expected, wl.t_expected, 1e-3, wl.w, V)
+        t_all += time.perf_counter() - t0
+        pairs += float(wl.M) * wl.N
+        used += 1
+        if t_all >= budget_s:
+            break
+    return pairs / t_all, cores, f"oracle E step (FP64, OpenMP) on {used} whole problems of the batch", t_all
+
+
+def run_batch(args, rank, world, local):
+    """--config batch: 550 desk-corner problems of 3,500 points, 50 EM iterations, all
+    registered by lsgcpd_register_batch; under torchrun each rank takes a contiguous share of the problems
+    (replicas only: no collective).  value = pair evaluations of all ranks' problems per second."""
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_2103_15039_b200 as lsg
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wls = synth.make_batch(BATCH_B, BATCH_N)
+    b0, b1 = shard(BATCH_B, rank, world)
+    mine = wls[b0:b1]
+    iters = args.iters or BATCH_ITERS
+    tgts = [lsg.prepare_target(torch.from_numpy(w.target).to(dev), w.knn_k) for w in mine]
+    srcs = [torch.from_numpy(w.source).to(dev) for w in mine]
+    reg = lsg.BatchRegistrar(tgts, srcs, iters)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        reg(w=0.1)
+        flush.fill_(1)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            out = reg(w=0.1)
+            flush.fill_(1)
+        e1.record(stream)
+        barrier()
+    dev_s = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    assert np.all(out["iters"] == iters) and np.all(out["status"] == 0)
+    pairs_step = float(sum(float(w.M) * w.N for w in wls)) * iters
+    value = pairs_step * args.steps / dev_s
+    # roofline over the whole batched step (the batched tensor-core E step is ≈ 96 % of it, DESIGN §11)
+    peaks, peak_src = measured_peaks()
+    f_max = float(peaks.get("sm_max_mhz", SM_MAX_MHZ_FALLBACK)) * 1e6
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = sms * FP32_LANES_PER_SM * 2 * f_max / 1e12
+    my_pairs = float(sum(float(w.M) * w.N for w in mine)) * iters
+    t_rank = e0.elapsed_time(e1) / 1e3 / args.steps
+    ach = FLOPS_PER_PAIR * my_pairs / t_rank / 1e12
+    roofline = {"bound": "alu", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                "traffic": None,
+                "kernel": "lsg::estep_batch_tc_kernel, timed as the whole lsgcpd_register_batch step",
+                "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 flop x {f_max/1e6:.0f} MHz (sm_max_mhz {peak_src})",
+                "mufu_ex2_frac": my_pairs / t_rank / (sms * MUFU_EX2_PER_SM * f_max)}
+    e2e = None
+    if not args.skip_e2e:   # host clouds → prepare every target → batched registration → poses to the host
+        h_t = [torch.from_numpy(w.target).pin_memory() for w in mine]
+        h_s = [torch.from_numpy(w.source).pin_memory() for w in mine]
+
+        def e2e_step():
+            dt_ = [x.to(dev, non_blocking=True) for x in h_t]
+            ds_ = [x.to(dev, non_blocking=True) for x in h_s]
+            tg_ = [lsg.prepare_target(d, w.knn_k) for d, w in zip(dt_, mine)]
+            return lsg.BatchRegistrar(tg_, ds_, iters)(w=0.1)
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        ne = max(1, min(args.steps, 2))
+        for _ in range(ne):
+            e2e_step()
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": pairs_step * ne / e2e_s, "unit": UNIT, "registrations_per_s": BATCH_B * ne / e2e_s,
+               "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in h_t + h_s)),
+               "d2h_bytes_per_step": int(len(mine) * (12 + 1 + 1 + 1) * 8), "steps": ne,
+               "includes": "H2D of every cloud, lsgcpd_prepare_target per problem, lsgcpd_register_batch, poses to host"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        rate, cores, sample, secs = batch_oracle_rate(wls)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample, "seconds": secs}
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": "batch", "problems": BATCH_B, "points_per_cloud": BATCH_N,
+                           "iters_per_step": iters, "w": 0.1, "step": "one lsgcpd_register_batch of all problems",
+                           "parallelism": f"problems sharded x{world} (replicas only, no collective)",
+                           "l2": "flushed between steps (256 MiB write)"},
+                "registrations_per_s": BATCH_B * args.steps / dev_s, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": (2 + 5 * iters) * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     import synth
+    if args.config == "batch":
+        if args.impl == "reference":
+            if rank == 0:
+                wls = synth.make_batch(BATCH_B, BATCH_N)
+                rate, cores, sample, secs = batch_oracle_rate(wls, budget_s=10.0)
+                print(json.dumps({"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+                                  "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                                  "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                                  "dtype": "f64", "data": "synthetic", "config": {"workload": "batch"},
+                                  "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                                   "sample": sample},
+                                  "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}), flush=True)
+            return
+        return run_batch(args, rank, world, local)
     wl = synth.make(args.config)
     if args.impl == "reference":
         return run_reference(args, wl, rank)

@@ -232,7 +232,7 @@ def run_batch(args, rank, world, local):
     b0, b1 = shard(BATCH_B, rank, world)
     mine = wls[b0:b1]
     iters = args.iters or BATCH_ITERS
-    tgts = [lsg.prepare_target(torch.from_numpy(w.target).to(dev), w.knn_k) for w in mine]
+    tgts = lsg.prepare_batch([torch.from_numpy(w.target).to(dev) for w in mine], mine[0].knn_k)
     srcs = [torch.from_numpy(w.source).to(dev) for w in mine]
     reg = lsg.BatchRegistrar(tgts, srcs, iters)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -287,7 +287,7 @@ def run_batch(args, rank, world, local):
         def e2e_step():
             dt_ = [x.to(dev, non_blocking=True) for x in h_t]
             ds_ = [x.to(dev, non_blocking=True) for x in h_s]
-            tg_ = [lsg.prepare_target(d, w.knn_k) for d, w in zip(dt_, mine)]
+            tg_ = lsg.prepare_batch(dt_, mine[0].knn_k)   # every target in one lsgcpd_prepare_batch call
             return lsg.BatchRegistrar(tg_, ds_, iters)(w=0.1)
 
         e2e_step()
@@ -301,7 +301,7 @@ def run_batch(args, rank, world, local):
         e2e = {"value": pairs_step * ne / e2e_s, "unit": UNIT, "registrations_per_s": BATCH_B * ne / e2e_s,
                "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in h_t + h_s)),
                "d2h_bytes_per_step": int(len(mine) * (12 + 1 + 1 + 1) * 8), "steps": ne,
-               "includes": "H2D of every cloud, lsgcpd_prepare_target per problem, lsgcpd_register_batch, poses to host"}
+               "includes": "H2D of every cloud, lsgcpd_prepare_batch, lsgcpd_register_batch, poses to host"}
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         rate, cores, sample, secs = batch_oracle_rate(wls)

@@ -116,6 +116,17 @@ int lsgcpd_prepare_target(const float* d_xyz, int64_t M, const lsgcpd_prep_param
                           lsgcpd_target_info* h_info, const lsgcpd_annotations* annotations,
                           lsgcpd_stream_t stream);
 
+/* B targets in one call (many small registrations, §8(f) NEXT-3): the same model as B calls of
+ * lsgcpd_prepare_target (no annotations), with two host synchronisations in all instead of two per
+ * target.  h_d_xyz[b] / h_d_target[b]: HOST arrays of B DEVICE pointers (cloud b [M_b][3], target b of
+ * lsgcpd_target_bytes(M_b) bytes); h_M: HOST [B]; h_info: HOST [B] or NULL.  One workspace of
+ * lsgcpd_prepare_batch_workspace_bytes() bytes serves all targets.  sync.
+ * Errors: as lsgcpd_prepare_target, the message naming the problem; EINVAL also for B < 1. */
+size_t lsgcpd_prepare_batch_workspace_bytes(const int64_t* h_M, int B, int knn_k);
+int lsgcpd_prepare_batch(const float* const* h_d_xyz, const int64_t* h_M, int B,
+                         const lsgcpd_prep_params* params, void* const* h_d_target, void* d_ws,
+                         size_t ws_bytes, lsgcpd_target_info* h_info, lsgcpd_stream_t stream);
+
 /* Pack a target from caller-supplied normals and α (e.g. an oracle's or a sensor's), no kNN.
  * d_normals [M][3] (used as given), d_alpha [M] (α_m ≥ 0).  sync (returns h_info).
  * Errors: EINVAL (null, M < 1, negative or non-finite α, ws too small), ECUDA. */

@@ -74,6 +74,10 @@ _SIGS = {
     "lsgcpd_prepare_workspace_bytes": ([_i64, _i32], _sz),
     "lsgcpd_prepare_target": ([_vp, _i64, ctypes.POINTER(PrepParams), _vp, _vp, _sz, ctypes.POINTER(TargetInfo),
                                ctypes.POINTER(Annotations), _vp], _i32),
+    "lsgcpd_prepare_batch_workspace_bytes": ([ctypes.POINTER(ctypes.c_int64), _i32, _i32], _sz),
+    "lsgcpd_prepare_batch": ([ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int64), _i32,
+                              ctypes.POINTER(PrepParams), ctypes.POINTER(ctypes.c_void_p), _vp, _sz,
+                              ctypes.POINTER(TargetInfo), _vp], _i32),
     "lsgcpd_pack_workspace_bytes": ([_i64], _sz),
     "lsgcpd_pack_target": ([_vp, _vp, _vp, _i64, _d, _vp, _vp, _sz, ctypes.POINTER(TargetInfo), _vp], _i32),
     "lsgcpd_estep_workspace_bytes": ([_i64, _i64], _sz),
@@ -193,6 +197,30 @@ def prepare_target(xyz, knn_k: int = 10, alpha_max: float = 50.0, lam: float = 0
                                    _stream_ptr(stream)))
     tgt = _target_from_info(buf, M, info)
     return (tgt, ann_t) if annotations else tgt
+
+
+def prepare_batch(clouds, knn_k: int = 10, alpha_max: float = 50.0, lam: float = 0.5, volume_margin: float = 0.1,
+                  stream=None):
+    """lsgcpd_prepare_batch: one Target per [M_b,3] float32 CUDA tensor, all prepared in one call."""
+    B = len(clouds)
+    if B < 1:
+        raise ValueError("need at least one cloud")
+    for c in clouds:
+        _need_cuda_f32(c, "cloud", 3)
+    L = lib()
+    Ms = (ctypes.c_int64 * B)(*[int(c.shape[0]) for c in clouds])
+    bufs = [_alloc_bytes(L.lsgcpd_target_bytes(int(c.shape[0])), clouds[0].device) for c in clouds]
+    xs = (ctypes.c_void_p * B)(*[c.data_ptr() for c in clouds])
+    ts = (ctypes.c_void_p * B)(*[b.data_ptr() for b in bufs])
+    nbytes = L.lsgcpd_prepare_batch_workspace_bytes(Ms, B, knn_k)
+    if nbytes == 0:
+        raise LsgcpdError(-1, "invalid batch of clouds")
+    ws = _alloc_bytes(nbytes, clouds[0].device)
+    p = PrepParams(alpha_max, lam, knn_k, volume_margin)
+    infos = (TargetInfo * B)()
+    _check(L.lsgcpd_prepare_batch(xs, Ms, B, ctypes.byref(p), ts, ws.data_ptr(), ws.numel(), infos,
+                                  _stream_ptr(stream)))
+    return [_target_from_info(bufs[b], int(Ms[b]), infos[b]) for b in range(B)]
 
 
 def pack_target(xyz, normals, alpha, volume_margin: float = 0.1, stream=None) -> Target:

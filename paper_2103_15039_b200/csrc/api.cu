@@ -264,7 +264,7 @@ using namespace lsg;
 // =============================================================================================
 // exported C ABI
 // =============================================================================================
-LSG_EXPORT int lsgcpd_version(void) { return 10100; }
+LSG_EXPORT int lsgcpd_version(void) { return 10200; }
 LSG_EXPORT const char* lsgcpd_last_error(void) { return g_err; }
 
 LSG_EXPORT void lsgcpd_prep_params_default(lsgcpd_prep_params* p) {
@@ -323,6 +323,39 @@ LSG_EXPORT int lsgcpd_prepare_target(const float* d_xyz, int64_t M, const lsgcpd
               prepare_ws_bytes(M));
     NvtxRange r("lsgcpd_prepare_target");
     return prepare_target_impl(d_xyz, M, p, d_target, d_ws, h_info, annotations, (cudaStream_t)stream);
+}
+
+LSG_EXPORT size_t lsgcpd_prepare_batch_workspace_bytes(const int64_t* h_M, int B, int knn_k) {
+    (void)knn_k;
+    if (!h_M || B < 1) return 0;
+    for (int b = 0; b < B; ++b)
+        if (h_M[b] < 3 || h_M[b] >= (int64_t)1 << 30) return 0;
+    return prepare_batch_ws_bytes(h_M, B);
+}
+
+LSG_EXPORT int lsgcpd_prepare_batch(const float* const* h_d_xyz, const int64_t* h_M, int B,
+                                    const lsgcpd_prep_params* params, void* const* h_d_target, void* d_ws,
+                                    size_t ws_bytes, lsgcpd_target_info* h_info, lsgcpd_stream_t stream) {
+    lsgcpd_prep_params p;
+    lsgcpd_prep_params_default(&p);
+    if (params) p = *params;
+    LSG_CHECK(h_d_xyz && h_M && h_d_target && d_ws && B >= 1 && B <= (1 << 20), LSGCPD_EINVAL,
+              "null pointer argument or bad B=%d", B);
+    for (int b = 0; b < B; ++b) {
+        LSG_CHECK(h_d_xyz[b] && h_d_target[b], LSGCPD_EINVAL, "problem %d: null pointer", b);
+        LSG_CHECK(aligned16(h_d_target[b]), LSGCPD_EINVAL, "problem %d: d_target must be 16-byte aligned", b);
+        LSG_CHECK(h_M[b] >= 3 && h_M[b] < (int64_t)1 << 30 && p.knn_k <= h_M[b], LSGCPD_EINVAL,
+                  "problem %d: M=%lld out of range [max(3, knn_k), 2^30)", b, (long long)h_M[b]);
+    }
+    LSG_CHECK(p.knn_k >= 3 && p.knn_k <= 32, LSGCPD_EINVAL, "knn_k=%d out of range [3, 32]", p.knn_k);
+    LSG_CHECK(isfinite(p.alpha_max) && p.alpha_max >= 0.f && isfinite(p.lambda) && p.lambda > 0.f, LSGCPD_EINVAL,
+              "alpha_max must be >= 0 and lambda > 0");
+    LSG_CHECK(isfinite(p.volume_margin) && p.volume_margin >= 0.0, LSGCPD_EINVAL, "volume_margin must be >= 0");
+    LSG_CHECK(aligned16(d_ws), LSGCPD_EINVAL, "d_ws must be 16-byte aligned");
+    LSG_CHECK(ws_bytes >= prepare_batch_ws_bytes(h_M, B), LSGCPD_EINVAL, "workspace too small (%zu < %zu)", ws_bytes,
+              prepare_batch_ws_bytes(h_M, B));
+    NvtxRange r("lsgcpd_prepare_batch");
+    return prepare_batch_impl(h_d_xyz, h_M, B, p, h_d_target, d_ws, h_info, (cudaStream_t)stream);
 }
 
 LSG_EXPORT int lsgcpd_pack_target(const float* d_xyz, const float* d_normals, const float* d_alpha, int64_t M,

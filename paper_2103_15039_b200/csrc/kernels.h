@@ -81,6 +81,9 @@ int select_confident_impl(const float* d_xyz, const float* d_phi, int64_t n, flo
                           float* d_phi_out, int64_t* h_n_out, void* d_ws, cudaStream_t stream);
 void depth_confidence_launch(const float* d_xyz, int64_t n, double c0, double c1, double z_min, float* d_phi,
                              cudaStream_t stream);
+size_t prepare_batch_ws_bytes(const int64_t* M, int B);
+int prepare_batch_impl(const float* const* xyz, const int64_t* M, int B, const lsgcpd_prep_params& p,
+                       void* const* targets, void* d_ws, lsgcpd_target_info* info, cudaStream_t stream);
 int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p, void* d_target, void* d_ws,
                         lsgcpd_target_info* info, const lsgcpd_annotations* ann, cudaStream_t stream);
 

@@ -3,6 +3,8 @@
 // the packed 64-B-per-target model the E step streams through TMA.
 #include <cub/cub.cuh>
 
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -108,6 +110,9 @@ __global__ void header_kernel(TargetHeader* hdr, int64_t M, const double* stats1
     h.prior = 0;
     h.pad_[0] = h.pad_[1] = 0;
     *hdr = h;
+    // the rest of the 256-byte header region is zero (the prepared target's bytes are fully defined)
+    uint32_t* tail = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(hdr) + sizeof(TargetHeader));
+    for (size_t i = 0; i < (kHeaderBytes - sizeof(TargetHeader)) / 4; ++i) tail[i] = 0u;
 }
 
 // Packed per-target record (FP64 arithmetic, FP32 storage); padding targets contribute nothing.
@@ -580,7 +585,13 @@ struct PrepLayout {
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int64_t kMaxCells = 1 << 22;
-constexpr int64_t kMaxCellsCoarse = 2 * kMaxCells / (kCoarse * kCoarse * kCoarse);   // with rounding slack
+// dense-grid cell cap of an M-point cloud: 128 cells per point (a volume-filling cloud needs ~64 at a quarter of
+// the mean spacing), at least 2^16, at most 2^22 — small clouds get small workspaces
+static int64_t cell_cap(int64_t M) {
+    const int64_t c = 128 * M;
+    return c < (1 << 16) ? (1 << 16) : (c > kMaxCells ? kMaxCells : c);
+}
+static int64_t cell_cap_coarse(int64_t M) { return 2 * cell_cap(M) / (kCoarse * kCoarse * kCoarse); }
 
 static size_t cub_sort_bytes(int64_t M) {
     size_t bytes = 0;
@@ -606,20 +617,20 @@ static PrepLayout prep_layout(int64_t M, bool with_knn) {
         L.ids = o; o += al(sizeof(int) * M);
         L.skeys = o; o += al(sizeof(int) * M);
         L.sids = o; o += al(sizeof(int) * M);
-        L.cstart = o; o += al(sizeof(int) * kMaxCells);
-        L.cend = o; o += al(sizeof(int) * kMaxCells);
+        L.cstart = o; o += al(sizeof(int) * cell_cap(M));
+        L.cend = o; o += al(sizeof(int) * cell_cap(M));
         L.skeys_c = o; o += al(sizeof(int) * M);
         L.sids_c = o; o += al(sizeof(int) * M);
-        L.cstart_c = o; o += al(sizeof(int) * kMaxCellsCoarse);
-        L.cend_c = o; o += al(sizeof(int) * kMaxCellsCoarse);
+        L.cstart_c = o; o += al(sizeof(int) * cell_cap_coarse(M));
+        L.cend_c = o; o += al(sizeof(int) * cell_cap_coarse(M));
         L.hard = o; o += al(sizeof(int) * (M + 1));   // [0] = count, then the point ids
         L.pts_f = o; o += al(sizeof(float4) * M);       // each grid's points in its cell order
         L.pts_c = o; o += al(sizeof(float4) * M);
         L.pts_b = o; o += al(sizeof(float4) * M);
         L.skeys_b = o; o += al(sizeof(int) * M);
         L.sids_b = o; o += al(sizeof(int) * M);
-        L.cstart_b = o; o += al(sizeof(int) * kMaxCells);
-        L.cend_b = o; o += al(sizeof(int) * kMaxCells);
+        L.cstart_b = o; o += al(sizeof(int) * cell_cap(M));
+        L.cend_b = o; o += al(sizeof(int) * cell_cap(M));
         L.cub_bytes = cub_sort_bytes(M);
         L.cub_tmp = o; o += al(L.cub_bytes);
     } else {
@@ -635,11 +646,11 @@ static PrepLayout prep_layout(int64_t M, bool with_knn) {
 size_t prepare_ws_bytes(int64_t M) { return prep_layout(M, true).total; }
 size_t pack_ws_bytes(int64_t M) { return prep_layout(M, false).total; }
 
-static int finish_target(const float* d_xyz, const float* nrm, const float* alpha, const float* nnd, const int* degen,
-                         int64_t M, double margin, char* ws, const PrepLayout& L, void* d_target,
-                         lsgcpd_target_info* info, cudaStream_t stream) {
+// Model statistics, header and the two packed sections of one target (async; st1 = its cloud statistics).
+static int finish_launch(const float* d_xyz, const float* nrm, const float* alpha, const float* nnd, const int* degen,
+                         int64_t M, double margin, char* ws, const PrepLayout& L, const double* st1, void* d_target,
+                         cudaStream_t stream) {
     double* bp = reinterpret_cast<double*>(ws + L.blockpart);
-    double* st1 = reinterpret_cast<double*>(ws + L.stats1);
     double* st2 = reinterpret_cast<double*>(ws + L.stats2);
     unsigned* ctr = reinterpret_cast<unsigned*>(ws + L.counter);
     model_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_xyz, alpha, nnd, degen, M, st1, bp, st2, ctr);
@@ -651,9 +662,11 @@ static int finish_target(const float* d_xyz, const float* nrm, const float* alph
     pack_tc_kernel<<<(unsigned)((M_pad + 255) / 256), 256, 0, stream>>>(d_xyz, nrm, alpha, M, M_pad, st2,
                                                                         target_tc(d_target, M_pad));
     LSG_CUDA(cudaGetLastError());
-    TargetHeader h;
-    LSG_CUDA(cudaMemcpyAsync(&h, hdr, sizeof(h), cudaMemcpyDeviceToHost, stream));
-    LSG_CUDA(cudaStreamSynchronize(stream));
+    return 0;
+}
+
+// Host summary and final checks of a finished target, from its header (already copied to the host).
+static int info_from_header(const TargetHeader& h, int64_t M, bool knn, lsgcpd_target_info* info) {
     if (info) {
         info->volume = h.volume;
         info->extent = h.extent;
@@ -666,9 +679,21 @@ static int finish_target(const float* d_xyz, const float* nrm, const float* alph
     }
     LSG_CHECK(isfinite(h.extent) && isfinite(h.ybar[0]) && isfinite(h.ybar[1]) && isfinite(h.ybar[2]), LSGCPD_EINVAL,
               "non-finite coordinate in the target cloud");
-    LSG_CHECK(h.extent > 0.0 || nnd == nullptr, LSGCPD_EDEGENERATE, "degenerate target: all points coincide");
+    LSG_CHECK(h.extent > 0.0 || !knn, LSGCPD_EDEGENERATE, "degenerate target: all points coincide");
     LSG_CHECK(isfinite(h.volume) && h.volume > 0.0, LSGCPD_EDEGENERATE, "degenerate target: zero working volume");
     return 0;
+}
+
+static int finish_target(const float* d_xyz, const float* nrm, const float* alpha, const float* nnd, const int* degen,
+                         int64_t M, double margin, char* ws, const PrepLayout& L, void* d_target,
+                         lsgcpd_target_info* info, cudaStream_t stream) {
+    int rc = finish_launch(d_xyz, nrm, alpha, nnd, degen, M, margin, ws, L,
+                           reinterpret_cast<const double*>(ws + L.stats1), d_target, stream);
+    if (rc) return rc;
+    TargetHeader h;
+    LSG_CUDA(cudaMemcpyAsync(&h, d_target, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    LSG_CUDA(cudaStreamSynchronize(stream));
+    return info_from_header(h, M, nnd != nullptr, info);
 }
 
 int pack_target_impl(const float* d_xyz, const float* d_nrm, const float* d_alpha, int64_t M, double margin,
@@ -682,18 +707,11 @@ int pack_target_impl(const float* d_xyz, const float* d_nrm, const float* d_alph
     return finish_target(d_xyz, d_nrm, d_alpha, nullptr, nullptr, M, margin, ws, L, d_target, info, stream);
 }
 
-int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p, void* d_target, void* d_ws,
-                        lsgcpd_target_info* info, const lsgcpd_annotations* ann, cudaStream_t stream) {
-    const PrepLayout L = prep_layout(M, true);
-    char* ws = static_cast<char*>(d_ws);
-    double* bp = reinterpret_cast<double*>(ws + L.blockpart);
-    double* st1 = reinterpret_cast<double*>(ws + L.stats1);
-    unsigned* ctr = reinterpret_cast<unsigned*>(ws + L.counter);
-    LSG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 4, stream));
-    cloud_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_xyz, M, bp, st1, ctr);
-    double s1[12];
-    LSG_CUDA(cudaMemcpyAsync(s1, st1, sizeof(s1), cudaMemcpyDeviceToHost, stream));
-    LSG_CUDA(cudaStreamSynchronize(stream));
+// kNN grids, sorts, the searches, the surface fit and the packed model of one target, from its cloud statistics
+// s1 (host copy) and st1 (device copy).  Async: no host synchronisation.
+static int prep_build(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p, const double* s1, const double* st1,
+                      void* d_target, char* ws, const PrepLayout& L, const lsgcpd_annotations* ann,
+                      cudaStream_t stream) {
     // grid: cell size from the AABB volume per point (≈ 1 point per cell for a volume-filling cloud)
     Grid g;
     double ext[3], ext_b[3], maxe = 0.0;
@@ -714,7 +732,7 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
             g.dim[a] = (int)fmin(floor(ext[a] / h) + 1.0, 1024.0);
             cells *= g.dim[a];
         }
-        if (cells <= kMaxCells) break;
+        if (cells <= cell_cap(M)) break;
         h *= 1.25;
     }
     g.h = h;
@@ -742,7 +760,7 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
                 gb.dim[a] = (int)fmin(floor(ext_b[a] / hb) + 1.0, 1024.0);
                 cells *= gb.dim[a];
             }
-            if (cells <= kMaxCells) break;
+            if (cells <= cell_cap(M)) break;
             hb *= 1.25;
         }
         gb.h = hb;
@@ -776,7 +794,7 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     LSG_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.cub_tmp, cub_bytes, keys, skeys_c, ids, sids_c, (int)M, 0, 22,
                                              stream));
     const int64_t ncells_c = (int64_t)gc.dim[0] * gc.dim[1] * gc.dim[2];
-    LSG_CHECK(ncells_c <= kMaxCellsCoarse, LSGCPD_EINVAL, "coarse grid too large (%lld cells)", (long long)ncells_c);
+    LSG_CHECK(ncells_c <= cell_cap_coarse(M), LSGCPD_EINVAL, "coarse grid too large (%lld cells)", (long long)ncells_c);
     LSG_CUDA(cudaMemsetAsync(cstart_c, 0xff, sizeof(int) * ncells_c, stream));
     LSG_CUDA(cudaMemsetAsync(cend_c, 0xff, sizeof(int) * ncells_c, stream));
     cell_ranges_kernel<<<nb, 256, 0, stream>>>(skeys_c, M, cstart_c, cend_c);
@@ -815,7 +833,104 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
                                                              p.lambda, nrm, kap, alp, knn, nnd, degen, nhard + 1, nhard,
                                                              pts_c);
     LSG_CUDA(cudaGetLastError());
-    return finish_target(d_xyz, nrm, alp, nnd, degen, M, p.volume_margin, ws, L, d_target, info, stream);
+    return finish_launch(d_xyz, nrm, alp, nnd, degen, M, p.volume_margin, ws, L, st1, d_target, stream);
+}
+
+int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p, void* d_target, void* d_ws,
+                        lsgcpd_target_info* info, const lsgcpd_annotations* ann, cudaStream_t stream) {
+    const PrepLayout L = prep_layout(M, true);
+    char* ws = static_cast<char*>(d_ws);
+    double* bp = reinterpret_cast<double*>(ws + L.blockpart);
+    double* st1 = reinterpret_cast<double*>(ws + L.stats1);
+    unsigned* ctr = reinterpret_cast<unsigned*>(ws + L.counter);
+    LSG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 4, stream));
+    cloud_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_xyz, M, bp, st1, ctr);
+    double s1[12];
+    LSG_CUDA(cudaMemcpyAsync(s1, st1, sizeof(s1), cudaMemcpyDeviceToHost, stream));
+    LSG_CUDA(cudaStreamSynchronize(stream));
+    int rc = prep_build(d_xyz, M, p, s1, st1, d_target, ws, L, ann, stream);
+    if (rc) return rc;
+    TargetHeader h;
+    LSG_CUDA(cudaMemcpyAsync(&h, d_target, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    LSG_CUDA(cudaStreamSynchronize(stream));
+    return info_from_header(h, M, true, info);
+}
+
+// B targets in one call (NEXT-3 workloads): every cloud's statistics, one host synchronisation, then every
+// target's grids, searches and packing on kPrepStreams streams (each with a workspace region sized for the
+// largest cloud), then one copy of all headers.  Two host synchronisations instead of two per target, and the
+// small targets' kernel chains overlap.
+constexpr int kPrepStreams = 8;   // concurrent target builds in lsgcpd_prepare_batch
+size_t prepare_batch_ws_bytes(const int64_t* M, int B) {
+    int64_t mmax = 1;
+    for (int b = 0; b < B; ++b) mmax = M[b] > mmax ? M[b] : mmax;
+    return (size_t)kPrepStreams * al(prep_layout(mmax, true).total) + al(sizeof(double) * 16 * (size_t)B);
+}
+
+int prepare_batch_impl(const float* const* xyz, const int64_t* M, int B, const lsgcpd_prep_params& p,
+                       void* const* targets, void* d_ws, lsgcpd_target_info* info, cudaStream_t stream) {
+    int64_t mmax = 1;
+    for (int b = 0; b < B; ++b) mmax = M[b] > mmax ? M[b] : mmax;
+    const PrepLayout L = prep_layout(mmax, true);
+    const int S = B < kPrepStreams ? B : kPrepStreams;
+    char* ws = static_cast<char*>(d_ws);
+    double* stats = reinterpret_cast<double*>(ws + (size_t)kPrepStreams * al(L.total));   // [B][16]
+    double* bp = reinterpret_cast<double*>(ws + L.blockpart);
+    unsigned* ctr = reinterpret_cast<unsigned*>(ws + L.counter);
+    for (int r = 0; r < S; ++r)
+        LSG_CUDA(cudaMemsetAsync(ws + (size_t)r * al(L.total) + L.counter, 0, sizeof(unsigned) * 4, stream));
+    for (int b = 0; b < B; ++b)
+        cloud_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(xyz[b], M[b], bp, stats + 16 * (size_t)b, ctr);
+    std::vector<double> hs(16 * (size_t)B);
+    LSG_CUDA(cudaMemcpyAsync(hs.data(), stats, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost, stream));
+    LSG_CUDA(cudaStreamSynchronize(stream));
+    // the targets' builds are chains of small kernels: S streams, each with its own workspace region, overlap them
+    struct Streams {
+        std::vector<cudaStream_t> s;
+        std::vector<cudaEvent_t> e;
+        ~Streams() {
+            for (auto x : s)
+                if (x) cudaStreamDestroy(x);
+            for (auto x : e)
+                if (x) cudaEventDestroy(x);
+        }
+    } sub;
+    sub.s.assign(S, nullptr);
+    sub.e.assign(S, nullptr);
+    for (int r = 0; r < S; ++r) {
+        LSG_CUDA(cudaStreamCreateWithFlags(&sub.s[r], cudaStreamNonBlocking));
+        LSG_CUDA(cudaEventCreateWithFlags(&sub.e[r], cudaEventDisableTiming));
+    }
+    for (int b = 0; b < B; ++b) {
+        const int r = b % S;
+        const int rc = prep_build(xyz[b], M[b], p, hs.data() + 16 * (size_t)b, stats + 16 * (size_t)b, targets[b],
+                                  ws + (size_t)r * al(L.total), L, nullptr, sub.s[r]);
+        if (rc) {
+            char msg[1024];
+            snprintf(msg, sizeof(msg), "problem %d: %s", b, lsgcpd_last_error());
+            for (int q = 0; q < S; ++q) cudaStreamSynchronize(sub.s[q]);
+            set_error("%s", msg);
+            return rc;
+        }
+    }
+    for (int r = 0; r < S; ++r) {
+        LSG_CUDA(cudaEventRecord(sub.e[r], sub.s[r]));
+        LSG_CUDA(cudaStreamWaitEvent(stream, sub.e[r], 0));
+    }
+    std::vector<TargetHeader> hh(B);
+    for (int b = 0; b < B; ++b)
+        LSG_CUDA(cudaMemcpyAsync(&hh[b], targets[b], sizeof(TargetHeader), cudaMemcpyDeviceToHost, stream));
+    LSG_CUDA(cudaStreamSynchronize(stream));
+    for (int b = 0; b < B; ++b) {
+        const int rc = info_from_header(hh[b], M[b], true, info ? info + b : nullptr);
+        if (rc) {
+            char msg[1024];
+            snprintf(msg, sizeof(msg), "problem %d: %s", b, lsgcpd_last_error());
+            set_error("%s", msg);
+            return rc;
+        }
+    }
+    return 0;
 }
 
 // ---- confidence filtering (Eq. 8) ----------------------------------------------------------

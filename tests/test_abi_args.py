@@ -111,3 +111,17 @@ def test_prepare_register_and_model_extensions_refuse_bad_arguments(L):
                                      None) == EINVAL
     assert L.lsgcpd_depth_confidence(FAKE, 0, 0.0, 0.002, 0.4, FAKE, None) == EINVAL
     assert L.lsgcpd_depth_confidence(FAKE, 10, 0.0, 0.0, 0.4, FAKE, None) == EINVAL
+
+
+def test_prepare_batch_refuses_bad_arguments(L):
+    M = (ctypes.c_int64 * 2)(100, 2)
+    assert L.lsgcpd_prepare_batch_workspace_bytes(M, 2, 10) == 0          # a cloud with M < 3
+    M_ok = (ctypes.c_int64 * 2)(100, 50)
+    assert L.lsgcpd_prepare_batch_workspace_bytes(M_ok, 0, 10) == 0       # B < 1
+    assert L.lsgcpd_prepare_batch_workspace_bytes(M_ok, 2, 10) > 0
+    ptrs = (ctypes.c_void_p * 2)(FAKE, FAKE)
+    assert L.lsgcpd_prepare_batch(ptrs, M, 2, None, ptrs, FAKE, 1 << 40, None, None) == EINVAL
+    assert "problem 1" in _err(L)
+    assert L.lsgcpd_prepare_batch(ptrs, M_ok, 0, None, ptrs, FAKE, 1 << 40, None, None) == EINVAL
+    unaligned = (ctypes.c_void_p * 2)(FAKE, FAKE + 4)
+    assert L.lsgcpd_prepare_batch(ptrs, M_ok, 2, None, unaligned, FAKE, 1 << 40, None, None) == EINVAL

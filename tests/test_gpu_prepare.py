@@ -91,3 +91,27 @@ def test_prepare_knn_dense_cluster_with_far_outliers(k):
     tgt, ann = lsg.prepare_target(to_dev(Y), k, annotations=True)
     tg = oracle.prepare_target(Y, k)
     _check_stage(Y, ann, tg, np.arange(Y.shape[0]), k)
+
+
+def test_prepare_batch_equals_single_prepares():
+    # lsgcpd_prepare_batch builds exactly (byte for byte) the targets B lsgcpd_prepare_target calls build,
+    # for clouds of different sizes and kinds (one of them with far outliers: the bulk-grid path)
+    import paper_2103_15039_b200 as lsg
+    import synth
+    clouds = [w.target for w in synth.make_batch(3, 900, seed=5, ragged=True)]
+    rng = np.random.default_rng(2)
+    clouds.append(np.concatenate([rng.normal(0, 0.02, (800, 3)), rng.uniform(-20, 20, (60, 3))]).astype(np.float32))
+    clouds.append(workload("tiny").target)
+    dev = [to_dev(c) for c in clouds]
+    batch = lsg.prepare_batch(dev, 10)
+    for c, tb in zip(dev, batch):
+        ts = lsg.prepare_target(c, 10)
+        assert tb.M == ts.M and tb.volume == ts.volume and tb.extent == ts.extent
+        assert torch_equal(tb.buf, ts.buf)
+    with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
+        lsg.prepare_batch([to_dev(np.zeros((2, 3), np.float32))], 10)
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))

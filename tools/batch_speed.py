@@ -6,7 +6,15 @@ import synth
 import paper_2103_15039_b200 as lsg
 B = int(os.environ.get("B", "550")); n = int(os.environ.get("NPTS", "3500")); iters = int(os.environ.get("ITERS", "50"))
 wls = synth.make_batch(B, n)
-tgts = [lsg.prepare_target(torch.from_numpy(w.target).cuda(), w.knn_k) for w in wls]
+clouds = [torch.from_numpy(w.target).cuda() for w in wls]
+[lsg.prepare_target(c, w.knn_k) for c, w in zip(clouds, wls)]; lsg.prepare_batch(clouds, wls[0].knn_k)   # warm-up
+torch.cuda.synchronize(); t0 = time.perf_counter()
+tgts = [lsg.prepare_target(c, w.knn_k) for c, w in zip(clouds, wls)]
+torch.cuda.synchronize(); t1 = time.perf_counter()
+tgts = lsg.prepare_batch(clouds, wls[0].knn_k)
+torch.cuda.synchronize(); t2 = time.perf_counter()
+print(f"prepare {B} targets: {(t1 - t0) * 1e3:.1f} ms one call each, {(t2 - t1) * 1e3:.1f} ms in one lsgcpd_prepare_batch",
+      flush=True)
 srcs = [torch.from_numpy(w.source).cuda() for w in wls]
 reg = lsg.BatchRegistrar(tgts, srcs, iters)
 reg(w=0.1); torch.cuda.synchronize()

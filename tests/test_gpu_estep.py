@@ -51,9 +51,14 @@ def test_estep_parity_outlier_weight_and_normaliser(w, consistent):
         np.testing.assert_allclose(rec[:, 0] + rec[:, 15], 1.0, atol=2e-6)
 
 
+@pytest.mark.parametrize("tc", ["auto", "1"])
 @pytest.mark.parametrize("M,N", [(1, 1), (3, 7), (63, 65), (64, 512), (257, 513), (1000, 1), (2, 5000),
                                  (130, 769)])
-def test_estep_ragged_and_tiny_sizes(M, N):
+def test_estep_ragged_and_tiny_sizes(M, N, tc, monkeypatch):
+    # also with the tensor-core kernel forced (LSGCPD_TC=1) on sizes below its automatic threshold: a single
+    # partial tile, a single partial 768-point block, more CTAs than units
+    if tc != "auto":
+        monkeypatch.setenv("LSGCPD_TC", tc)
     rng = np.random.default_rng(M * 7919 + N)
     Y = rng.uniform(-1, 1, (M, 3)).astype(np.float32)
     n = rng.standard_normal((M, 3))

@@ -89,3 +89,12 @@ def test_only_test_infrastructure_imports_the_oracle():
             for f in files:
                 if f.endswith((".py", ".c", ".h", ".sh")):
                     assert not pat.search(open(os.path.join(dirpath, f)).read()), os.path.join(dirpath, f)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    # no CPU fallback: without liblsgcpd.so the binding raises on first use
+    code = ("import paper_2103_15039_b200 as p\n"
+            "try:\n    p.lib()\nexcept ImportError as e:\n    print('raised', 'no CPU fallback' in str(e))\n")
+    env = dict(os.environ, LSGCPD_LIB=str(tmp_path / "missing.so"))
+    out = subprocess.run(["python", "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert out.stdout.strip() == "raised True", out.stdout + out.stderr

@@ -87,3 +87,25 @@ def test_batch_invalid_arguments():
         lsg.register_batch(tgts, [to_dev(w.source) for w in wls], 5, w=1.0)
     with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
         lsg.register_batch(tgts, [to_dev(w.source) for w in wls], 5, R0s=[2 * np.eye(3)] * 2)
+
+
+def test_batch_running_max_mode_and_priors_match_single_registrations():
+    # w = 0 puts every problem in the running-max mode (the CUDA-core batched kernel serves them); a target
+    # with priors π(m) (Eq. 8) is served by the tensor-core batched kernel: each problem lands where its
+    # single-problem lsgcpd_register lands, and priors with the literal normaliser are refused
+    import paper_2103_15039_b200 as lsg
+    wls = synth.make_batch(3, 800, seed=17)
+    tgts = [_prep(w)[0] for w in wls]
+    srcs = [to_dev(w.source) for w in wls]
+    out = lsg.register_batch(tgts, srcs, 20, w=0.0)
+    for b in range(3):
+        single = lsg.register(tgts[b], srcs[b], 20, w=0.0)
+        assert out["status"][b] == 0 and single["status"] == 0
+        _close(out["R"][b], out["t"][b], single["R"], single["t"], tgts[b].extent, tol=1e-5)
+    phi = to_dev(np.random.default_rng(3).uniform(0.2, 1.0, tgts[1].M).astype(np.float32))
+    lsg.set_prior(tgts[1], phi)
+    out = lsg.register_batch(tgts, srcs, 20, w=0.1)
+    single = lsg.register(tgts[1], srcs[1], 20, w=0.1)
+    _close(out["R"][1], out["t"][1], single["R"], single["t"], tgts[1].extent, tol=1e-5)
+    with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
+        lsg.register_batch(tgts, srcs, 5, w=0.1, consistent=False)

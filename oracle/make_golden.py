@@ -1,7 +1,7 @@
 """Write oracle-only golden files under tests/golden/ (TEST INFRASTRUCTURE ONLY).
 
 Every number written here comes from oracle/ on synth/ inputs; nothing comes from the CUDA path.
-    python -m oracle.make_golden object [rgbd lidar ...]
+    python -m oracle.make_golden object [rgbd lidar rgbd_cf ...]
 """
 from __future__ import annotations
 
@@ -48,6 +48,41 @@ def make(name: str, iters=None):
     print(name, "done in %.1fs" % dt, "rot err %.2e" % g["rot_err_vs_expected"])
 
 
+def make_cf(iters: int = 50):
+    """The RGBD-CF workload (NEXT-2): depth confidences (reading R23), truncation at φ < 0.04,
+    priors π(m) on the truncated target and per-point w_n on the truncated source, whole oracle pipeline."""
+    from oracle import outlier as ol
+    from oracle import prepare_target, register, working_volume
+    wl = synth.make("rgbd")
+    thr = np.float32(0.04)
+    phi_y = ol.depth_confidence(wl.target[:, 2].astype(np.float64)).astype(np.float32)
+    phi_x = ol.depth_confidence(wl.source[:, 2].astype(np.float64)).astype(np.float32)
+    Y, py, _ = ol.truncate(wl.target, phi_y, thr)
+    X, px, _ = ol.truncate(wl.source, phi_x, thr)
+    t0 = time.time()
+    tgt = prepare_target(Y, wl.knn_k)
+    V, extent = working_volume(Y)
+    out = register(tgt, X, wl.w, iters, V, extent, prior=ol.confidence_prior(py.astype(np.float64)),
+                   phi_x=px.astype(np.float64))
+    dt = time.time() - t0
+    tr = out["trace"]
+    g = {
+        "config": "rgbd_cf",
+        "source": "oracle/make_golden.py make_cf (FP64 CPU oracle only); inputs synth.make('rgbd') truncated "
+                  "at phi < 0.04 by oracle.outlier.truncate",
+        "target_sha": digest(Y), "source_sha": digest(X), "M": int(Y.shape[0]), "N": int(X.shape[0]),
+        "w": wl.w, "iters": iters, "knn_k": wl.knn_k, "V": V, "extent": extent,
+        "R": out["R"].tolist(), "t": out["t"].tolist(), "sigma2": out["sigma2"],
+        "nll_trace": tr["nll"], "sigma2_trace": tr["sigma2"],
+        "rot_err_vs_expected": se3.rotation_angle(out["R"].T @ wl.R_expected),
+        "trans_err_vs_expected": float(np.linalg.norm(out["t"] - wl.t_expected)),
+        "oracle_seconds": dt,
+    }
+    with open(os.path.join(OUT, "rgbd_cf_oracle.json"), "w") as f:
+        json.dump(g, f, indent=1)
+    print("rgbd_cf done in %.1fs" % dt, "rot err %.2e" % g["rot_err_vs_expected"])
+
+
 if __name__ == "__main__":
     for n in sys.argv[1:]:
-        make(n)
+        make_cf() if n == "rgbd_cf" else make(n)

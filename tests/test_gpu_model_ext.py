@@ -136,3 +136,28 @@ def test_rgbd_confidence_filtered_registration_teacher_forced():
         assert se3.rotation_angle(np.asarray(nxt["R"]).T @ R1) <= 1e-4
         assert np.linalg.norm(np.asarray(nxt["t"]) - t1) <= 1e-4 * tgt.extent
         assert abs(nxt["sigma2"] - s21) <= 1e-6 * s21
+
+
+def test_rgbd_confidence_filtered_registration_vs_golden():
+    # the whole RGBD-CF pipeline (NEXT-2) against the FP64 oracle's (oracle/make_golden.py rgbd_cf): the
+    # truncated clouds, the GPU-prepared target with priors π(m), per-point w_n, 50 EM iterations
+    import json
+    import os
+    import paper_2103_15039_b200 as lsg
+    from oracle.make_golden import digest
+    path = os.path.join(os.path.dirname(__file__), "golden", "rgbd_cf_oracle.json")
+    g = json.load(open(path))
+    wl = workload("rgbd")
+    thr = np.float32(0.04)
+    Y, py, _ = ol.truncate(wl.target, ol.depth_confidence(wl.target[:, 2].astype(np.float64)).astype(np.float32), thr)
+    X, px, _ = ol.truncate(wl.source, ol.depth_confidence(wl.source[:, 2].astype(np.float64)).astype(np.float32), thr)
+    assert (digest(Y), digest(X)) == (g["target_sha"], g["source_sha"]), "inputs changed"
+    tgt = lsg.prepare_target(to_dev(Y), wl.knn_k)
+    assert tgt.volume == pytest.approx(g["V"], rel=1e-6)
+    lsg.set_prior(tgt, to_dev(py))
+    out = lsg.register(tgt, to_dev(X), g["iters"], w=wl.w, src_conf=to_dev(px))
+    assert out["status"] == 0 and out["iters"] == g["iters"]
+    ang = se3.rotation_angle(np.asarray(out["R"]).T @ np.array(g["R"]))
+    assert ang <= 1e-4, ang
+    assert np.linalg.norm(np.asarray(out["t"]) - np.array(g["t"])) <= 1e-4 * g["extent"]
+    assert out["sigma2"] == pytest.approx(g["sigma2"], rel=1e-3)

@@ -21,3 +21,26 @@ for name in ("object", "rgbd", "lidar"):
     s2t = np.max(np.abs(np.array(out["sigma2_trace"]) / np.array(g["sigma2_trace"]) - 1))
     print(f"{name:7s} iters={g['iters']:3d}  rot diff {ang:.2e} rad  |dt|/extent {dt:.2e}  sigma2 rel {s2:.2e}"
           f"  max sigma2-trace rel {s2t:.2e}  (oracle {g['oracle_seconds']:.0f} s on its host)", flush=True)
+
+# the RGBD-CF pipeline (NEXT-2): truncation, priors, per-point w_n (the truncation decision repeated here in FP32)
+g = json.load(open(os.path.join(G, "rgbd_cf_oracle.json")))
+wl = synth.make("rgbd")
+thr = np.float32(0.04)
+
+
+def depth_phi(z, c1=0.002, zmin=0.4):
+    return np.clip((c1 * zmin * zmin) / (c1 * z.astype(np.float64) ** 2), 0.0, 1.0).astype(np.float32)
+
+
+py_all, px_all = depth_phi(wl.target[:, 2]), depth_phi(wl.source[:, 2])
+ky, kx = py_all >= thr, px_all >= thr
+Y, py, X, px = wl.target[ky], py_all[ky], wl.source[kx], px_all[kx]
+tgt = lsg.prepare_target(torch.from_numpy(np.ascontiguousarray(Y)).cuda(), wl.knn_k)
+lsg.set_prior(tgt, torch.from_numpy(py).cuda())
+out = lsg.register(tgt, torch.from_numpy(np.ascontiguousarray(X)).cuda(), g["iters"], w=wl.w,
+                   src_conf=torch.from_numpy(px).cuda(), traces=True)
+ang = rotation_angle(out["R"].T @ np.array(g["R"]))
+dt = np.linalg.norm(out["t"] - np.array(g["t"])) / g["extent"]
+print(f"rgbd_cf iters={g['iters']:3d}  rot diff {ang:.2e} rad  |dt|/extent {dt:.2e}  sigma2 rel "
+      f"{abs(out['sigma2'] / g['sigma2'] - 1):.2e}  (M={Y.shape[0]} N={X.shape[0]}; oracle {g['oracle_seconds']:.0f} s)",
+      flush=True)

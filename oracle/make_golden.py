@@ -83,6 +83,32 @@ def make_cf(iters: int = 50):
     print("rgbd_cf done in %.1fs" % dt, "rot err %.2e" % g["rot_err_vs_expected"])
 
 
+def make_ext(name: str):
+    """object_eta (w from the outlier ratio η = 0.1, Eq. 7) and object_affine (the affine group): the
+    object config's whole oracle pipeline with one model extension."""
+    from oracle import prepare_target, register, working_volume
+    wl = synth.make("object")
+    t0 = time.time()
+    tgt = prepare_target(wl.target, wl.knn_k)
+    V, extent = working_volume(wl.target)
+    kw = {"eta": 0.1} if name == "object_eta" else {"group": "affine"}
+    out = register(tgt, wl.source, wl.w, wl.iters, V, extent, **kw)
+    dt = time.time() - t0
+    g = {"config": name, "source": "oracle/make_golden.py make_ext (FP64 CPU oracle only); inputs synth.make('object')",
+         "target_sha": digest(wl.target), "source_sha": digest(wl.source), "M": wl.M, "N": wl.N, "w": wl.w,
+         "extension": kw, "iters": wl.iters, "V": V, "extent": extent, "R": out["R"].tolist(),
+         "t": out["t"].tolist(), "sigma2": out["sigma2"], "sigma2_trace": out["trace"]["sigma2"],
+         "oracle_seconds": dt}
+    with open(os.path.join(OUT, f"{name}_oracle.json"), "w") as f:
+        json.dump(g, f, indent=1)
+    print(name, "done in %.1fs" % dt)
+
+
 if __name__ == "__main__":
     for n in sys.argv[1:]:
-        make_cf() if n == "rgbd_cf" else make(n)
+        if n == "rgbd_cf":
+            make_cf()
+        elif n in ("object_eta", "object_affine"):
+            make_ext(n)
+        else:
+            make(n)

@@ -186,3 +186,25 @@ def test_graph_cache_replay_and_update_match_fresh_graphs(monkeypatch):
         np.testing.assert_array_equal(a["R"], b["R"])
         np.testing.assert_array_equal(a["t"], b["t"])
         assert a["sigma2"] == b["sigma2"]
+
+
+@pytest.mark.parametrize("name", ["object_eta", "object_affine"])
+def test_register_object_extensions_vs_golden(name):
+    # whole object registrations with one model extension — w from the outlier ratio η = 0.1 (Eq. 7,
+    # NEXT-1) or the affine group (NEXT-4) — against the oracle's full pipeline
+    # (oracle/make_golden.py); for the affine group "R" is the linear part A, compared by ‖A - A_ref‖
+    import paper_2103_15039_b200 as lsg
+    from oracle.make_golden import digest
+    g = json.load(open(os.path.join(GOLDEN, f"{name}_oracle.json")))
+    wl = workload("object")
+    assert (digest(wl.target), digest(wl.source)) == (g["target_sha"], g["source_sha"]), "inputs changed"
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    kw = {"eta": g["extension"]["eta"]} if "eta" in g["extension"] else {"w": wl.w, "group": "affine"}
+    gpu = lsg.register(tgt, to_dev(wl.source), g["iters"], **kw)
+    assert gpu["status"] == 0 and gpu["iters"] == g["iters"]
+    if name == "object_affine":
+        assert np.abs(np.asarray(gpu["R"]) - np.array(g["R"])).max() <= 1e-4
+        assert np.linalg.norm(np.asarray(gpu["t"]) - np.array(g["t"])) <= 1e-4 * g["extent"]
+    else:
+        _close(gpu["R"], gpu["t"], np.array(g["R"]), np.array(g["t"]), g["extent"])
+    assert gpu["sigma2"] == pytest.approx(g["sigma2"], rel=1e-3)

@@ -1,3 +1,4 @@
+"""Five EM iterations of the tiny and object registrations (a short program to capture with ncu)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch, synth

@@ -773,6 +773,7 @@ static int batch_layout(const lsgcpd_problem* P, int B, int max_iters, BatchLayo
     LSG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     Sched sc;
     memset(&sc, 0, sizeof(sc));
+    sc.halves = 1;
     sc.U = units;
     const int64_t slots = (int64_t)nsm;       // one CTA per SM (both batched E-step kernels)
     sc.G = units < slots ? units : slots;

@@ -223,6 +223,9 @@ struct Sched {
     int64_t B;        // source points per block
     int variant;      // E-step kernel variant (negative: tensor-core kernel + CUDA-core variant -1-variant)
     int tc_variant;   // tensor-core kernel configuration
+    int halves;       // 2: the targets are swept as two halves, one launch each (T = tiles per half); else 1
+    int pad_;
+    int64_t hstride;  // floats between the two halves' partial sets
 };
 __host__ __device__ inline int64_t sched_start(const Sched& s, int64_t g) { return g * s.U / s.G; }
 __host__ __device__ inline int64_t sched_owner(const Sched& s, int64_t u) { return ((u + 1) * s.G - 1) / s.U; }

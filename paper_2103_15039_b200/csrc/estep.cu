@@ -1094,7 +1094,8 @@ static int g_num_sms = 0;
 static int g_occ[kNumVariants] = {0};
 
 constexpr int kMidVariant = 9, kMidBlk = 2 * 8 * 32;   // packed, 2 points/thread, 8 consumer warps: 512-point blocks
-constexpr int kSmallVariant = 12;   // one consumer warp, 64-point blocks: problems too small to fill the GPU
+constexpr int kSmallVariant = 12;
+constexpr int64_t kSplitBytes = 48ll << 20;   // tensor-core sections above this are swept in two halves   // one consumer warp, 64-point blocks: problems too small to fill the GPU
 
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
     const int tvi = tc_variant_index();
@@ -1131,7 +1132,13 @@ int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
     s.tc_variant = tvi;
     s.B = (int64_t)V.ppt * V.ncw * 32;
     s.nblk = (N + s.B - 1) / s.B;
-    s.T = M_pad / kTT;
+    // a tensor-core section larger than ~48 MB is swept in two halves, one launch each, so every CTA reads
+    // tiles of the same half at a time and the half stays in L2 (the whole section re-read from HBM otherwise;
+    // DESIGN §7 "DRAM traffic").  M_pad is a multiple of 256 targets, so the tile count is even.
+    const char* he = getenv("LSGCPD_HALVES");
+    const bool split = tc && (M_pad / kTT) * (int64_t)kTcTileBytes > kSplitBytes && !(he && he[0] == '1');
+    s.halves = split ? 2 : 1;
+    s.T = M_pad / kTT / s.halves;
     s.U = s.nblk * s.T;
     const int64_t slots = (int64_t)g_num_sms * (tc ? 1 : g_occ[vi]);   // the TC kernel holds all TMEM: 1 CTA/SM
     s.G = s.U < slots ? s.U : slots;
@@ -1142,11 +1149,12 @@ int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
         if (k > kmax) kmax = k;
     }
     s.kmax = kmax;
+    s.hstride = s.nblk * s.kmax * (int64_t)kPartF * s.B;
     *sc = s;
     return 0;
 }
 
-size_t estep_partial_bytes(const Sched& s) { return (size_t)s.nblk * s.kmax * kPartF * s.B * sizeof(float); }
+size_t estep_partial_bytes(const Sched& s) { return (size_t)s.halves * s.hstride * sizeof(float); }
 
 void estep_launch_setup(IterState* st, const void* d_target, const double* R, const double* t, double sigma2,
                         double w, double V, int64_t M, int consistent, double eta, cudaStream_t stream) {
@@ -1157,26 +1165,32 @@ void estep_launch_setup(IterState* st, const void* d_target, const double* R, co
 
 void estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
                   float* part, float* rec, int consistent, const float* phi, cudaStream_t stream, int merge) {
-    const float* body = target_body(d_target);
     const bool tc = sc.variant < 0;
     const Variant& V = kVariants[tc ? -1 - sc.variant : sc.variant];
     Sched scv = sc;
     int skip_fixed = tc ? 1 : 0;
-    void* args[] = {(void*)&body, (void*)&d_src, (void*)&N, (void*)&st, (void*)&scv, (void*)&part, (void*)&skip_fixed};
-    if (tc) {
-        const int64_t M_pad = sc.T * kTT;
-        const char* tcb = reinterpret_cast<const char*>(target_tc(d_target, M_pad));
-        const TcVariant& TV = kTcVariants[sc.tc_variant];
-        static bool attr_set[kNumTcVariants] = {};
-        if (!attr_set[sc.tc_variant]) {
-            cudaFuncSetAttribute(TV.fn[0], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TV.smem);
-            cudaFuncSetAttribute(TV.fn[1], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TV.smem);
-            attr_set[sc.tc_variant] = true;
+    const int64_t M_pad = sc.T * kTT * sc.halves;
+    for (int h = 0; h < sc.halves; ++h) {   // one sweep per half of the targets (sc.T tiles each)
+        const float* body = target_body(d_target) + (int64_t)h * sc.T * kTT * kTgtFloats;
+        float* parth = part + (int64_t)h * sc.hstride;
+        void* args[] = {(void*)&body, (void*)&d_src, (void*)&N, (void*)&st, (void*)&scv, (void*)&parth,
+                        (void*)&skip_fixed};
+        if (tc) {
+            const char* tcb = reinterpret_cast<const char*>(target_tc(d_target, M_pad)) +
+                              (int64_t)h * sc.T * kTcTileBytes;
+            const TcVariant& TV = kTcVariants[sc.tc_variant];
+            static bool attr_set[kNumTcVariants] = {};
+            if (!attr_set[sc.tc_variant]) {
+                cudaFuncSetAttribute(TV.fn[0], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TV.smem);
+                cudaFuncSetAttribute(TV.fn[1], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TV.smem);
+                attr_set[sc.tc_variant] = true;
+            }
+            void* targs[] = {(void*)&tcb, (void*)&d_src, (void*)&N, (void*)&st, (void*)&scv, (void*)&parth};
+            cudaLaunchKernel(TV.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3(TV.threads), targs, TV.smem,
+                             stream);
         }
-        void* targs[] = {(void*)&tcb, (void*)&d_src, (void*)&N, (void*)&st, (void*)&scv, (void*)&part};
-        cudaLaunchKernel(TV.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3(TV.threads), targs, TV.smem, stream);
+        cudaLaunchKernel(V.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3((V.ncw + 1) * 32), args, 0, stream);
     }
-    cudaLaunchKernel(V.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3((V.ncw + 1) * 32), args, 0, stream);
     if (!merge) return;
     estep_merge_kernel<<<(unsigned)((N + kMergePts - 1) / kMergePts), kMergePts * 16, 0, stream>>>(part, N, st, sc,
                                                                                                  rec, phi);

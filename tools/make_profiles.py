@@ -28,6 +28,7 @@ if not os.path.exists(rep):   # launch list only (the E-step kernel's full captu
     sys.exit(0)
 raw = list(csv.reader(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()))
 d = dict(zip(raw[0], raw[2])); u = dict(zip(raw[0], raw[1]))
+launches = [dict(zip(raw[0], r)) for r in raw[2:] if len(r) == len(raw[0])]   # every captured launch
 keys = ['Kernel Name', 'gpu__time_duration.sum', 'launch__grid_size', 'launch__block_size', 'launch__registers_per_thread',
         'sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active', 'sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed',
         'sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active', 'sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active',
@@ -49,9 +50,22 @@ open(os.path.join(P, f"{out}_estep_ncu_summary.txt"), "w").write(
     + "\n".join(txt) + "\n")
 shutil.copy(rep, os.path.join(P, f"{out}_estep_full.ncu-rep"))
 mult = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9}
-tr = float(d['dram__bytes_read.sum'].replace(',', '')) * mult[u['dram__bytes_read.sum']] + \
-     float(d['dram__bytes_write.sum'].replace(',', '')) * mult[u['dram__bytes_write.sum']]
+# one lsgcpd_estep call = one tensor-core launch per half of the targets (two on scale): the captured launches
+# (consecutive halves) are summed
+per = []
+for x in launches:
+    try:
+        v = float(x['dram__bytes_read.sum'].replace(',', '')) * mult[u['dram__bytes_read.sum']] + \
+            float(x['dram__bytes_write.sum'].replace(',', '')) * mult[u['dram__bytes_write.sum']]
+    except ValueError:
+        continue
+    if v == v:   # ncu leaves some replays without DRAM counters (-nan)
+        per.append(v)
+HALVES = 2   # tensor-core launches per lsgcpd_estep call on scale (Sched::halves)
+tr = sum(per) / len(per) * HALVES
 json.dump({"workload": "scale", "n_gpus": 1, "kernel": d['Kernel Name'], "dram_bytes_per_launch": tr,
-           "source": f"profiles/{out}_estep_ncu_summary.txt (dram__bytes_read.sum + dram__bytes_write.sum)"},
+           "launches_per_estep": HALVES,
+           "source": f"profiles/{out}_estep_ncu_summary.txt (dram__bytes_read.sum + dram__bytes_write.sum per "
+                     f"tensor-core launch, mean of {len(per)} captured, x {HALVES} launches per lsgcpd_estep call)"},
           open(os.path.join(P, "estep_dram_bytes.json"), "w"), indent=1)
 print("\n".join(lines[:12])); print("\n".join(txt))

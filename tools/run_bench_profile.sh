@@ -13,7 +13,7 @@ if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/launches_${TAG}.csv $SHORT > gpurun_out/ncu_launch_${TAG}.log 2>&1
   echo "launch list rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-estep_tc_kernel} -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-estep_tc_kernel} -s 1 -c ${NCU_COUNT:-2} \
       -o gpurun_out/prof_estep_${TAG} $SHORT > gpurun_out/ncu_full_${TAG}.log 2>&1
   echo "ncu full rc=$?"
 fi

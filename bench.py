@@ -482,13 +482,14 @@ def main():
         dist.barrier()
     if rank == 0:
         # per registration: setup + σ²₀ sums + σ²₀ init, then per EM iteration the pair kernels (tensor-core
-        # E step + CUDA-core E step, which returns at once in the fixed-max mode; one small-block CUDA-core
+        # E step + CUDA-core E step, which returns at once in the fixed-max mode, per half of the target; one small-block CUDA-core
         # kernel for problems too small to fill the GPU), then merge, moments, Newton — or, for N ≤ 2^17,
         # one em_tail_kernel (plus newton_kernel after the all-reduce when a communicator is used)
-        m_pad = -(-wl.M // 64) * 64
+        m_pad = -(-wl.M // 256) * 256
         tc = -(-n_local // 768) * (m_pad // 64) >= 2 * torch.cuda.get_device_properties(dev).multi_processor_count
+        halves = 2 if tc and (m_pad // 64) * 10240 > (48 << 20) else 1   # target swept in halves
         tail = (1 if comm is None else 2) if n_local <= (1 << 17) else 3
-        launches_per_step = 3 + ((2 if tc else 1) + tail) * iters
+        launches_per_step = 3 + ((2 * halves if tc else 1) + tail) * iters
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,

@@ -85,8 +85,12 @@ def test_estep_far_points_and_large_coordinates():
         assert_record_parity(rec, ora, Y, a32, what=f"far/large w={w}")
 
 
-def test_estep_sampled_parity_at_full_scale():
-    # BASELINE configs at full size: oracle on a sample of source points (every target)
+@pytest.mark.parametrize("halves", ["auto", "1"])
+def test_estep_sampled_parity_at_full_scale(halves, monkeypatch):
+    # BASELINE configs at full size: oracle on a sample of source points (every target).  scale's 84 MB
+    # tensor-core section is swept in two halves by default; LSGCPD_HALVES=1 keeps one sweep
+    if halves != "auto":
+        monkeypatch.setenv("LSGCPD_HALVES", halves)
     import paper_2103_15039_b200 as lsg
     for name in ("rgbd", "scale"):
         wl = workload(name)

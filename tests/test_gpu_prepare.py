@@ -115,3 +115,16 @@ def test_prepare_batch_equals_single_prepares():
 def torch_equal(a, b):
     import torch
     return bool(torch.equal(a, b))
+
+
+def test_prepare_batch_edge_cases():
+    # B = 1 with the minimal cloud (M = k = 3), and a batch whose second cloud is degenerate: EDEGENERATE
+    # naming that problem
+    import paper_2103_15039_b200 as lsg
+    tri = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], np.float32)
+    (tb,) = lsg.prepare_batch([to_dev(tri)], 3)
+    ts = lsg.prepare_target(to_dev(tri), 3)
+    assert torch_equal(tb.buf, ts.buf)
+    good = workload("tiny").target
+    with pytest.raises(lsg.LsgcpdError, match="problem 1"):
+        lsg.prepare_batch([to_dev(good), to_dev(np.ones((50, 3), np.float32))], 10)

@@ -15,18 +15,23 @@ def shard_range(n: int, rank: int, world: int):
 
 
 def broadcast_bytes(blob: bytes, src: int = 0, group=None) -> bytes:
-    """Broadcast a small byte string from `src` over torch.distributed (gloo: CPU tensor, nccl: CUDA)."""
+    """Broadcast a small byte string from `src` over torch.distributed (gloo: CPU tensor, nccl: CUDA).
+
+    `src` is a rank WITHIN `group` (the rank a communicator of that group sees); torch's broadcast takes a
+    global rank, so it is translated for a non-default group."""
     import torch
     import torch.distributed as dist
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return blob
-    n = torch.tensor([len(blob) if dist.get_rank(group) == src else 0], dtype=torch.int64)
+    me = dist.get_rank(group)
+    gsrc = src if group is None else dist.get_global_rank(group, src)
+    n = torch.tensor([len(blob) if me == src else 0], dtype=torch.int64)
     on_gpu = dist.get_backend(group) == "nccl"
     dev = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
     n = n.to(dev)
-    dist.broadcast(n, src=src, group=group)
+    dist.broadcast(n, src=gsrc, group=group)
     buf = torch.zeros(int(n.item()), dtype=torch.uint8, device=dev)
-    if dist.get_rank(group) == src:
+    if me == src:
         buf.copy_(torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev))
-    dist.broadcast(buf, src=src, group=group)
+    dist.broadcast(buf, src=gsrc, group=group)
     return bytes(buf.cpu().numpy().tobytes())

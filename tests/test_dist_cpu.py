@@ -116,3 +116,25 @@ def test_two_rank_sharded_em_equals_single_process():
     np.testing.assert_allclose(a[:9], ref["R"].ravel(), atol=1e-10)
     np.testing.assert_allclose(a[9:12], ref["t"], atol=1e-10)
     assert a[12] == pytest.approx(ref["sigma2"], rel=1e-9)
+
+
+def _subgroup_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2103_15039_b200.dist import broadcast_bytes
+    grp = dist.new_group([1, 2])   # group ranks 0, 1 = global ranks 1, 2
+    if rank in (1, 2):
+        # `src` is the GROUP rank: group rank 0 is global rank 1, which holds the id
+        blob = broadcast_bytes(b"id-from-global-1" if rank == 1 else b"", 0, grp)
+        out[rank] = blob
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_broadcast_bytes_in_a_subgroup_uses_group_ranks():
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_subgroup_worker, args=(3, port, out), nprocs=3, join=True)
+    assert out[1] == b"id-from-global-1" and out[2] == b"id-from-global-1"

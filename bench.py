@@ -35,7 +35,11 @@ UNIT = "pair-evals/s"
 SM_MAX_MHZ_FALLBACK = 1965.0
 FLOPS_PER_PAIR = 47.0     # SURVEY §8(d).2 algorithmic FP32 flops per (m, n) pair (FMA = 2), + 1 exp
 FP32_LANES_PER_SM = 128   # FP32 FMA lanes per SM per clock (B200)
-MUFU_EX2_PER_SM = 16      # MUFU.EX2 results per SM per clock (B200; measured 4.58e12/s, tools/microbench)
+MUFU_EX2_PER_SM = 16      # MUFU.EX2 results per SM per clock (B200 unit count)
+# CUDA-core FP32 lane-operations per pair in the tensor-core E step's SASS: tile-centred residual
+# 13 (r 3, ñ·r 3, τ 4, exponent 1, Σpτ 1, TF32 remainder of p 1), hi/lo residual 16 (r 6)
+LANE_OPS_CENTRED, LANE_OPS_HILO = 13.0, 16.0
+TILE_BYTES, TARGET_HDR = 10240, 256
 
 
 def parse():
@@ -59,6 +63,62 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def ensure_ranks(args):
+    """`--gpus N` runs N ranks: under torchrun the environment must say WORLD_SIZE = N; launched plainly with
+    N > 1, bench.py re-executes itself under torch.distributed.run with N processes (one per GPU), after checking
+    that N GPUs are visible.  Any mismatch is an error (never a silent single-rank run)."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return
+    if args.gpus <= 1 or args.impl == "reference":
+        return
+    import socket
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {n}")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
+def centred_tile_share(target, sigma2: float, gate: float) -> float:
+    """Share of the prepared target's 64-target tiles whose E_tile ≤ gate·σ (the tile-centred residual),
+    read from the tile metadata of the tensor-core section (include/lsgcpd.h layout 2)."""
+    import torch
+    M_pad = (target.M + 255) // 256 * 256
+    off = TARGET_HDR + M_pad * 16 * 4
+    T = M_pad // 64
+    raw = target.buf[off: off + T * TILE_BYTES].view(torch.float32).reshape(T, TILE_BYTES // 4)
+    E = raw[:, 31].double().cpu().numpy()   # meta field (7) of target 3 of the tile
+    return float(np.mean(E <= gate * np.sqrt(sigma2)))
+
+
+def microbench_peaks():
+    p = os.path.join(ROOT, "profiles", "microbench_peaks.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
+def traffic_per_launch(workload: str, world: int):
+    """DRAM bytes per lsgcpd_estep call of one rank (ncu, profiles/estep_dram_bytes.json) for this world size."""
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "estep_dram_bytes.json")))
+        if tj.get("workload") == workload:
+            return tj.get("by_n_gpus", {}).get(str(world))
+    except Exception:
+        pass
+    return None
 
 
 def shard(n: int, rank: int, world: int):
@@ -273,12 +333,16 @@ def run_batch(args, rank, world, local):
     fp32_peak = sms * FP32_LANES_PER_SM * 2 * f_max / 1e12
     my_pairs = float(sum(float(w.M) * w.N for w in mine)) * iters
     t_rank = e0.elapsed_time(e1) / 1e3 / args.steps
-    ach = FLOPS_PER_PAIR * my_pairs / t_rank / 1e12
-    roofline = {"bound": "alu", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s", "frac": ach / fp32_peak,
+    ex2_rate = my_pairs / t_rank
+    mufu_peak = sms * MUFU_EX2_PER_SM * f_max
+    roofline = {"bound": "alu", "achieved": ex2_rate, "peak": mufu_peak, "unit": "ex2/s", "frac": ex2_rate / mufu_peak,
                 "traffic": None,
                 "kernel": "lsg::estep_batch_tc_kernel, timed as the whole lsgcpd_register_batch step",
-                "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 flop x {f_max/1e6:.0f} MHz (sm_max_mhz {peak_src})",
-                "mufu_ex2_frac": my_pairs / t_rank / (sms * MUFU_EX2_PER_SM * f_max)}
+                "peak_source": f"MUFU.EX2 roofline: {sms} SMs x {MUFU_EX2_PER_SM} ex2/clk x {f_max/1e6:.0f} MHz "
+                               f"(sm_max_mhz {peak_src})",
+                "mufu_ex2_frac": ex2_rate / mufu_peak,
+                "fp32_equiv_tflops": FLOPS_PER_PAIR * ex2_rate / 1e12,
+                "fp32_equiv_frac_of_nominal": FLOPS_PER_PAIR * ex2_rate / 1e12 / fp32_peak}
     e2e = None
     if not args.skip_e2e:   # host clouds → prepare every target → batched registration → poses to the host
         h_t = [torch.from_numpy(w.target).pin_memory() for w in mine]
@@ -303,7 +367,7 @@ def run_batch(args, rank, world, local):
                "d2h_bytes_per_step": int(len(mine) * (12 + 1 + 1 + 1) * 8), "steps": ne,
                "includes": "H2D of every cloud, lsgcpd_prepare_batch, lsgcpd_register_batch, poses to host"}
     cpu = None
-    if rank == 0 and world == 1 and not args.skip_cpu:
+    if rank == 0 and not args.skip_cpu:
         rate, cores, sample, secs = batch_oracle_rate(wls)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample, "seconds": secs}
     if world > 1:
@@ -325,6 +389,7 @@ def run_batch(args, rank, world, local):
 
 def main():
     args = parse()
+    ensure_ranks(args)
     rank, world, local = dist_env()
     import synth
     if args.config == "batch":
@@ -420,27 +485,30 @@ def main():
     peaks, peak_src = measured_peaks()
     f_max = float(peaks.get("sm_max_mhz", SM_MAX_MHZ_FALLBACK)) * 1e6
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mufu_peak = sms * MUFU_EX2_PER_SM * f_max            # ex2/s: unit count x clock (B200_PROFILING / SURVEY)
     fp32_peak_tflops = sms * FP32_LANES_PER_SM * 2 * f_max / 1e12
-    mufu_peak = sms * MUFU_EX2_PER_SM * f_max
-    achieved_tflops = FLOPS_PER_PAIR * pairs_launch / t_launch / 1e12
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "estep_dram_bytes.json")
-    if os.path.exists(tfile):
-        try:
-            tj = json.load(open(tfile))
-            if tj.get("workload") == wl.name and tj.get("n_gpus") == world:
-                traffic = tj.get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "alu", "achieved": achieved_tflops, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
-                "frac": achieved_tflops / fp32_peak_tflops, "traffic": traffic,
-                "kernel": "lsg::estep_tc2_kernel (tcgen05 TF32 feature sums, default LSGCPD_TC_VARIANT) + merge, via lsgcpd_estep",
-                "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 flop x {f_max/1e6:.0f} MHz "
-                               f"(sm_max_mhz {peak_src}, MEASURED_PEAKS.json); algorithmic "
-                               f"{FLOPS_PER_PAIR:.0f} flop/pair (SURVEY 8(d).2)",
+    ex2_rate = pairs_launch / t_launch                     # one MUFU.EX2 per pair
+    share = centred_tile_share(target, s2_probe, float(lsg.get_option("tile_gate")))
+    lane_ops = LANE_OPS_CENTRED * share + LANE_OPS_HILO * (1.0 - share)
+    mb = microbench_peaks()
+    ffma2_meas = mb.get("ffma2_lane_ops_per_s")
+    ex2_meas = mb.get("ex2_per_s")
+    roofline = {"bound": "alu", "achieved": ex2_rate, "peak": mufu_peak, "unit": "ex2/s",
+                "frac": ex2_rate / mufu_peak, "traffic": traffic_per_launch(wl.name, world),
+                "kernel": "lsg::estep_tc_kernel (tcgen05 TF32 feature sums; tile-centred residual) + merge, via "
+                          "lsgcpd_estep on the launching stream",
+                "peak_source": f"MUFU.EX2 roofline: {sms} SMs x {MUFU_EX2_PER_SM} ex2/clk x {f_max/1e6:.0f} MHz "
+                               f"(sm_max_mhz {peak_src}, MEASURED_PEAKS.json; the north star's roofline)",
                 "pairs_per_launch": pairs_launch, "launch_ms": t_launch * 1e3,
-                "mufu_ex2_frac": pairs_launch / t_launch / mufu_peak,
-                "pairs_per_s_per_gpu": pairs_launch / t_launch}
+                "mufu_ex2_frac": ex2_rate / mufu_peak,
+                "mufu_ex2_frac_vs_microbench": (ex2_rate / ex2_meas) if ex2_meas else None,
+                "centred_tile_share": share, "fp32_lane_ops_per_pair": lane_ops,
+                "fp32_lane_frac": (lane_ops * ex2_rate / ffma2_meas) if ffma2_meas else None,
+                "fp32_lane_peak_source": "measured FFMA2 lane-op/s, profiles/microbench_peaks.json" if ffma2_meas
+                                         else None,
+                "fp32_equiv_tflops": FLOPS_PER_PAIR * ex2_rate / 1e12,
+                "fp32_equiv_frac_of_nominal": FLOPS_PER_PAIR * ex2_rate / 1e12 / fp32_peak_tflops,
+                "pairs_per_s_per_gpu": ex2_rate}
 
     # ---- e2e: host buffers → public API → host results ----
     e2e = None
@@ -473,7 +541,7 @@ def main():
                "includes": "H2D target+source, lsgcpd_prepare_target, lsgcpd_register, R/t/sigma2 to host"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.skip_cpu:
+    if rank == 0 and not args.skip_cpu:   # rank 0 at every world size (the other ranks wait at the barrier)
         rate, cores, sample, secs = cpu_oracle_rate(wl)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                "seconds": secs}

@@ -101,7 +101,10 @@ const char* lsgcpd_last_error(void);      /* thread-local; never NULL           
 /* ---------------------------------------------------------------------------------------
  * Target model.  The prepared target is an opaque device buffer of lsgcpd_target_bytes(M)
  * bytes (16-byte aligned, caller-owned) holding, per target m, y_m, √α_m n_m, α_m n_m n_mᵀ,
- * α_m (n_m·y_m) n_m and the log-determinant weight ½log2(1+α_m), plus a small header.
+ * α_m (n_m·y_m) n_m and the log-determinant weight ½log2(1+α_m), plus a small header.  The
+ * targets are stored in a spatial (Morton) order with per-tile centres (the E step's
+ * precision device); every result is a sum over targets and does not depend on
+ * that order.  Layout 2 (ABI 1.3): a target prepared by an older library is refused (EINVAL).
  * ------------------------------------------------------------------------------------- */
 size_t lsgcpd_target_bytes(int64_t M);
 size_t lsgcpd_prepare_workspace_bytes(int64_t M, int knn_k);
@@ -128,7 +131,8 @@ int lsgcpd_prepare_batch(const float* const* h_d_xyz, const int64_t* h_M, int B,
                          size_t ws_bytes, lsgcpd_target_info* h_info, lsgcpd_stream_t stream);
 
 /* Pack a target from caller-supplied normals and α (e.g. an oracle's or a sensor's), no kNN.
- * d_normals [M][3] (used as given), d_alpha [M] (α_m ≥ 0).  sync (returns h_info).
+ * d_normals [M][3] (normalised to unit length by the pack; a zero or non-finite normal makes
+ * component m isotropic, α_m := 0), d_alpha [M] (α_m ≥ 0).  sync (returns h_info).
  * Errors: EINVAL (null, M < 1, negative or non-finite α, ws too small), ECUDA. */
 size_t lsgcpd_pack_workspace_bytes(int64_t M);
 int lsgcpd_pack_target(const float* d_xyz, const float* d_normals, const float* d_alpha, int64_t M,
@@ -140,6 +144,8 @@ int lsgcpd_pack_target(const float* d_xyz, const float* d_normals, const float* 
  *   d_mn = ((x̂_n-y_m)ᵀ(x̂_n-y_m) + α_m (n_m·(x̂_n-y_m))²)/σ²,
  *   P_mn = (1-w)/M c_m e^{-d_mn/2} / (w/V + (1-w)/M Σ_k c_k e^{-d_kn/2}),
  * reduced to the 16-float record above.  P is never materialised.  async.
+ * d_target must be a target prepared for this M: that is checked on the device (no host
+ * synchronisation) and a mismatch (wrong M, not a prepared target) writes an all-NaN record.
  * Errors: EINVAL (null, N < 1, M < 1, σ² ≤ 0 or non-finite, w ∉ [0,1), V ≤ 0, R not a
  * rotation to 1e-6, ws too small), ECUDA. */
 size_t lsgcpd_estep_workspace_bytes(int64_t M, int64_t N);
@@ -245,6 +251,36 @@ size_t lsgcpd_register_batch_workspace_bytes(const lsgcpd_problem* h_problems, i
 int lsgcpd_register_batch(const lsgcpd_problem* h_problems, int B, const lsgcpd_em_params* params,
                           double* R_out, double* t_out, double* sigma2_out, int* iters_out,
                           int* status_out, void* d_ws, size_t ws_bytes, lsgcpd_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Test support: the multi-GPU protocol on ONE device.  G source
+ * shards h_d_src[g] (HOST array of G DEVICE pointers, [h_N[g]][3]) are registered as G ranks of
+ * lsgcpd_register with a communicator would: each shard runs the production E step, merge,
+ * moment and Newton kernels on its own workspace; the moment all-reduce (75 doubles per EM
+ * iteration) and the σ²₀ all-reduce are a fixed-order device sum over the shards.  d_ws holds G
+ * workspaces at a stride of ws_stride bytes (a multiple of 256, each ≥ lsgcpd_register_
+ * workspace_bytes(M, h_N[g], max_iters)).  Outputs per shard: R_out[9G], t_out[3G],
+ * sigma2_out[G], iters_out[G] (identical across shards by construction).  1 ≤ G ≤ 16;
+ * params->d_src_conf must be NULL.  sync.  Errors: as lsgcpd_register. */
+int lsgcpd_register_shards(const void* d_target, int64_t M, double volume, const float* const* h_d_src,
+                           const int64_t* h_N, int G, const lsgcpd_em_params* params, const double R0[9],
+                           const double t0[3], double* R_out, double* t_out, double* sigma2_out,
+                           int* iters_out, void* d_ws, size_t ws_stride, lsgcpd_stream_t stream);
+
+/* Run-time options (diagnostics and tests; the defaults are the product configuration).  Read
+ * once from the environment at first use (LSGCPD_TC, LSGCPD_ESTEP_VARIANT, LSGCPD_HALVES,
+ * LSGCPD_NO_FUSE, LSGCPD_GRAPH_CACHE, LSGCPD_NO_GRAPH, LSGCPD_TILE_GATE), then only changed
+ * by lsgcpd_set_option; each field is atomic.  Names and values:
+ *   "tc"            2 automatic, 1 tensor-core E step forced, 0 CUDA cores only
+ *   "estep_variant" -1 automatic, 0/1/2 the 768/512/64-point-block CUDA-core E step
+ *   "halves"        0 automatic, 1 one sweep over large targets
+ *   "no_fuse"       1: separate merge and moment kernels (N ≤ 2^17)
+ *   "graph_cache"   0: no cached EM-iteration graphs
+ *   "no_graph"      1: plain launches instead of a captured EM iteration
+ *   "tile_gate"     G: tile-centred residual on tiles with E_tile ≤ G·σ (≤ 0: never)
+ * Errors: EINVAL (unknown name, value out of range). */
+int lsgcpd_set_option(const char* name, double value);
+int lsgcpd_get_option(const char* name, double* value);
 
 /* Defaults for the parameter structs (the values documented above). */
 void lsgcpd_prep_params_default(lsgcpd_prep_params* p);

@@ -98,6 +98,11 @@ _SIGS = {
     "lsgcpd_register_workspace_bytes": ([_i64, _i64, _i32], _sz),
     "lsgcpd_register": ([_vp, _i64, _d, _vp, _i64, ctypes.POINTER(EmParams), _dp, _dp, _dp, _dp, _dp,
                          ctypes.POINTER(ctypes.c_int), _dp, _dp, _vp, _vp, _sz, _vp], _i32),
+    "lsgcpd_register_shards": ([_vp, _i64, _d, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int64), _i32,
+                                ctypes.POINTER(EmParams), _dp, _dp, _dp, _dp, _dp, ctypes.POINTER(ctypes.c_int), _vp,
+                                _sz, _vp], _i32),
+    "lsgcpd_set_option": ([ctypes.c_char_p, _d], _i32),
+    "lsgcpd_get_option": ([ctypes.c_char_p, _dp], _i32),
 }
 
 
@@ -457,3 +462,62 @@ class BatchRegistrar:
 def register_batch(targets, sources, max_iters: int, src_confs=None, volumes=None, R0s=None, t0s=None, **kw):
     """lsgcpd_register_batch → dict(R [B,3,3], t [B,3], sigma2 [B], iters [B], status [B])."""
     return BatchRegistrar(targets, sources, max_iters, src_confs, volumes, R0s, t0s)(**kw)
+
+
+def set_option(name: str, value) -> None:
+    """lsgcpd_set_option: run-time knobs for diagnostics and tests (tc, estep_variant, halves, no_fuse,
+    graph_cache, no_graph, tile_gate; include/lsgcpd.h)."""
+    _check(lib().lsgcpd_set_option(name.encode(), float(value)))
+
+
+def get_option(name: str) -> float:
+    v = ctypes.c_double()
+    _check(lib().lsgcpd_get_option(name.encode(), ctypes.byref(v)))
+    return v.value
+
+
+class options:
+    """Context manager: set options for a block and restore the previous values, e.g.
+    ``with lsg.options(tc=0, estep_variant=1): ...``"""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            set_option(k, v)
+
+
+def register_shards(target: Target, sources, max_iters: int, w: float = 0.1, newton_max: int = 10,
+                    consistent: bool = True, sigma2_init: float = 0.0, sigma2_floor_rel: float = 1e-12,
+                    R0=None, t0=None, volume: float = 0.0, stream=None):
+    """lsgcpd_register_shards: the multi-GPU protocol (shard moments all-reduced every EM iteration, Newton
+    per rank) with len(sources) shards on one device → dict(R [G,3,3], t [G,3], sigma2 [G], iters [G])."""
+    G = len(sources)
+    for x in sources:
+        _need_cuda_f32(x, "source shard", 3)
+    Ns = (ctypes.c_int64 * G)(*[int(x.shape[0]) for x in sources])
+    ptrs = (ctypes.c_void_p * G)(*[x.data_ptr() for x in sources])
+    stride = max(lib().lsgcpd_register_workspace_bytes(target.M, int(n), int(max_iters)) for n in Ns)
+    stride = (stride + 255) // 256 * 256
+    ws = _alloc_bytes(stride * G, sources[0].device)
+    p = EmParams(w, int(max_iters), newton_max, int(bool(consistent)), sigma2_init, sigma2_floor_rel, 0.0, -1.0,
+                 None, 0)
+    R0a, R0p = _darr(np.eye(3) if R0 is None else R0, 9)
+    t0a, t0p = _darr(np.zeros(3) if t0 is None else t0, 3)
+    R = np.zeros((G, 9))
+    t = np.zeros((G, 3))
+    s2 = np.zeros(G)
+    it = (ctypes.c_int * G)()
+    _check(lib().lsgcpd_register_shards(target.buf.data_ptr(), target.M, float(volume), ptrs, Ns, G, ctypes.byref(p),
+                                        R0p, t0p, R.ctypes.data_as(_dp), t.ctypes.data_as(_dp),
+                                        s2.ctypes.data_as(_dp), it, ws.data_ptr(), stride, _stream_ptr(stream)))
+    return {"R": R.reshape(G, 3, 3), "t": t, "sigma2": s2, "iters": np.array(it[:])}
+

@@ -91,7 +91,8 @@ struct GraphCache {
     };
     std::vector<Entry> e;
     uint64_t tick = 0;
-    cudaStream_t cap = nullptr;   // capture stream of this thread
+    static constexpr int kMaxDev = 64;
+    cudaStream_t cap[kMaxDev] = {};   // capture stream of this thread, per device (a stream belongs to one device)
     static constexpr size_t kMax = 4;
     Entry* find(const std::vector<unsigned char>& k, bool topo) {
         for (auto& x : e)
@@ -113,7 +114,8 @@ struct GraphCache {
     }
     ~GraphCache() {
         for (auto& x : e) delete x.run;
-        if (cap) cudaStreamDestroy(cap);
+        for (auto c : cap)
+            if (c) cudaStreamDestroy(c);
     }
 };
 static thread_local GraphCache g_graphs;
@@ -223,38 +225,66 @@ static int read_header(const void* d_target, int64_t M, TargetHeader* h, cudaStr
     return 0;
 }
 
-// One EM iteration (async): E step → moments → [all-reduce] → Newton + σ².
-static int enqueue_iteration(const void* d_target, const float* d_src, int64_t N, char* ws, const RegLayout& L,
-                             const Sched& sc, const RegParams& rp, Comm* comm, cudaStream_t stream) {
+// The two halves of one EM iteration around the moment all-reduce (async).
+// First half: E step → merge → the 75 moments in `mom`.  With fuse_newton (no communicator) the N ≤ 2^17 path
+// also runs Newton + σ² inside em_tail_kernel and the iteration is complete.
+static int enqueue_moments(const void* d_target, const float* d_src, int64_t N, char* ws, const RegLayout& L,
+                           const Sched& sc, const RegParams& rp, bool fuse_newton, cudaStream_t stream) {
     IterState* st = reinterpret_cast<IterState*>(ws + L.state);
     double* mom = reinterpret_cast<double*>(ws + L.mom);
     float* rec = reinterpret_cast<float*>(ws + L.rec);
-    const char* nf = getenv("LSGCPD_NO_FUSE");
-    if (N <= kTailMaxN && !(nf && nf[0] == '1')) {   // one launch for merge + moments (+ Newton without comm)
-        estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), rec, rp.consistent, rp.phi,
-                     stream, 0);
+    if (N <= kTailMaxN && options().no_fuse.load() != 1) {   // one launch for merge + moments (+ Newton w/o comm)
+        const int rc = estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), rec,
+                                    rp.consistent, rp.phi, stream, 0);
+        if (rc) return rc;
         em_tail_launch(reinterpret_cast<float*>(ws + L.part), d_src, N, st, sc, rp.phi,
                        reinterpret_cast<double*>(ws + L.blockpart), mom, reinterpret_cast<unsigned*>(ws + L.counters),
                        rp, reinterpret_cast<double*>(ws + L.nll), reinterpret_cast<double*>(ws + L.sig2),
-                       reinterpret_cast<int*>(ws + L.iters), comm ? 0 : 1, stream);
-        if (!comm) return 0;
-        const ncclResult_t r = g_nccl.AllReduce(mom, mom, kMomentCount, kNcclFloat64, kNcclSum, comm->nc, stream);
-        if (r != 0) return nccl_fail(r, "ncclAllReduce(moments)");
-        newton_launch(st, mom, rp, reinterpret_cast<double*>(ws + L.nll), reinterpret_cast<double*>(ws + L.sig2),
-                      reinterpret_cast<int*>(ws + L.iters), stream);
+                       reinterpret_cast<int*>(ws + L.iters), fuse_newton ? 1 : 0, stream);
         return 0;
     }
-    estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), rec, rp.consistent, rp.phi,
-                 stream);
+    const int rc = estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), rec, rp.consistent,
+                                rp.phi, stream);
+    if (rc) return rc;
     moments_launch(rec, d_src, N, st, reinterpret_cast<double*>(ws + L.blockpart), mom,
                    reinterpret_cast<unsigned*>(ws + L.counters), stream);
+    return 0;
+}
+static bool moments_fused_newton(int64_t N) { return N <= kTailMaxN && options().no_fuse.load() != 1; }
+// Second half: damped Newton + σ² from the (all-reduced) moments; writes the next IterState.
+static void enqueue_newton(char* ws, const RegLayout& L, const RegParams& rp, cudaStream_t stream) {
+    newton_launch(reinterpret_cast<IterState*>(ws + L.state), reinterpret_cast<double*>(ws + L.mom), rp,
+                  reinterpret_cast<double*>(ws + L.nll), reinterpret_cast<double*>(ws + L.sig2),
+                  reinterpret_cast<int*>(ws + L.iters), stream);
+}
+
+// One EM iteration (async): E step → moments → [all-reduce] → Newton + σ².
+static int enqueue_iteration(const void* d_target, const float* d_src, int64_t N, char* ws, const RegLayout& L,
+                             const Sched& sc, const RegParams& rp, Comm* comm, cudaStream_t stream) {
+    const int rc = enqueue_moments(d_target, d_src, N, ws, L, sc, rp, comm == nullptr, stream);
+    if (rc) return rc;
+    if (!comm && moments_fused_newton(N)) return 0;
     if (comm) {
+        double* mom = reinterpret_cast<double*>(ws + L.mom);
         const ncclResult_t r = g_nccl.AllReduce(mom, mom, kMomentCount, kNcclFloat64, kNcclSum, comm->nc, stream);
         if (r != 0) return nccl_fail(r, "ncclAllReduce(moments)");
     }
-    newton_launch(st, mom, rp, reinterpret_cast<double*>(ws + L.nll), reinterpret_cast<double*>(ws + L.sig2),
-                  reinterpret_cast<int*>(ws + L.iters), stream);
+    enqueue_newton(ws, L, rp, stream);
     return 0;
+}
+
+// The all-reduce of lsgcpd_register_shards: out = Σ_g v_g in shard order, written back to every shard's vector
+// (every "rank" receives the same sum, as from ncclAllReduce).
+constexpr int kMaxShards = 16;
+struct ShardPtrs {
+    double* p[kMaxShards];
+};
+__global__ void shard_allreduce_kernel(ShardPtrs v, int G, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = v.p[0][i];
+    for (int g = 1; g < G; ++g) s += v.p[g][i];
+    for (int g = 0; g < G; ++g) v.p[g][i] = s;
 }
 
 }  // namespace lsg
@@ -264,7 +294,7 @@ using namespace lsg;
 // =============================================================================================
 // exported C ABI
 // =============================================================================================
-LSG_EXPORT int lsgcpd_version(void) { return 10200; }
+LSG_EXPORT int lsgcpd_version(void) { return 10300; }
 LSG_EXPORT const char* lsgcpd_last_error(void) { return g_err; }
 
 LSG_EXPORT void lsgcpd_prep_params_default(lsgcpd_prep_params* p) {
@@ -437,8 +467,9 @@ static int estep_impl(const void* d_target, int64_t M, const float* d_src, int64
     char* ws = static_cast<char*>(d_ws);
     IterState* st = reinterpret_cast<IterState*>(ws + L.state);
     estep_launch_setup(st, d_target, R, t, sigma2, w, volume, M, consistent_normalizer ? 1 : 0, eta, s);
-    estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), d_record,
-                 consistent_normalizer ? 1 : 0, phi, s);
+    rc = estep_launch(d_target, d_src, N, st, sc, reinterpret_cast<float*>(ws + L.part), d_record,
+                      consistent_normalizer ? 1 : 0, phi, s);
+    if (rc) return rc;
     LSG_CUDA(cudaGetLastError());
     return 0;
 }
@@ -491,6 +522,41 @@ LSG_EXPORT size_t lsgcpd_register_workspace_bytes(int64_t M, int64_t N_local, in
     return L.total;
 }
 
+namespace lsg {
+// EM parameters common to lsgcpd_register and lsgcpd_register_shards (the checks of include/lsgcpd.h)
+static int check_em_params(const lsgcpd_em_params& p, const double* R, const double* t) {
+    LSG_CHECK(isfinite(p.w) && p.w >= 0.0 && p.w < 1.0, LSGCPD_EINVAL, "w must be in [0, 1)");
+    LSG_CHECK(p.max_iters >= 0 && p.max_iters <= 100000, LSGCPD_EINVAL, "max_iters out of range");
+    LSG_CHECK(p.newton_max >= 0 && p.newton_max <= 1000, LSGCPD_EINVAL, "newton_max out of range");
+    LSG_CHECK(isfinite(p.sigma2_floor_rel) && p.sigma2_floor_rel >= 0.0, LSGCPD_EINVAL, "bad sigma2_floor_rel");
+    LSG_CHECK(isfinite(p.sigma2_init) && isfinite(p.tol), LSGCPD_EINVAL, "sigma2_init and tol must be finite");
+    LSG_CHECK(!(p.eta >= 1.0) && !isnan(p.eta), LSGCPD_EINVAL, "eta must be < 1 (negative: off)");
+    LSG_CHECK(p.group == 0 || p.group == 1, LSGCPD_EINVAL, "group must be 0 (SE(3)) or 1 (affine)");
+    LSG_CHECK(pose_ok(R, p.group), LSGCPD_EINVAL,
+              p.group ? "A0 must be finite with det A0 > 0" : "R0 is not a rotation matrix (to 1e-6)");
+    LSG_CHECK(finite_vec(t, 3), LSGCPD_EINVAL, "t0 must be finite");
+    return 0;
+}
+static RegParams reg_params(const lsgcpd_em_params& p, const TargetHeader& h, double V, int64_t M) {
+    RegParams rp;
+    memset(&rp, 0, sizeof(rp));
+    rp.w = p.eta >= 0.0 ? 0.0 : p.w;
+    rp.eta = p.eta >= 0.0 ? p.eta : -1.0;
+    rp.spc = h.spc;
+    rp.phi = p.d_src_conf;
+    rp.V = V;
+    rp.floor = p.sigma2_floor_rel * h.extent * h.extent;
+    rp.tol = p.tol;
+    rp.omega_ref_target = h.omega_ref;
+    rp.M = M;
+    rp.newton_max = p.newton_max;
+    rp.consistent = p.consistent_normalizer ? 1 : 0;
+    rp.max_iters = p.max_iters;
+    rp.group = p.group;
+    return rp;
+}
+}  // namespace lsg
+
 LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, const float* d_src_local,
                                int64_t N_local, const lsgcpd_em_params* params, const double R0[9], const double t0[3],
                                double R_out[9], double t_out[3], double* sigma2_out, int* iters_out,
@@ -504,19 +570,11 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     LSG_CHECK(aligned16(d_target) && aligned16(d_ws), LSGCPD_EINVAL, "d_target and d_ws must be 16-byte aligned");
     LSG_CHECK(M >= 1 && N_local >= 1 && M < (int64_t)1 << 30 && N_local < (int64_t)1 << 34, LSGCPD_EINVAL,
               "M=%lld N_local=%lld out of range", (long long)M, (long long)N_local);
-    LSG_CHECK(isfinite(p.w) && p.w >= 0.0 && p.w < 1.0, LSGCPD_EINVAL, "w must be in [0, 1)");
-    LSG_CHECK(p.max_iters >= 0 && p.max_iters <= 100000, LSGCPD_EINVAL, "max_iters out of range");
-    LSG_CHECK(p.newton_max >= 0 && p.newton_max <= 1000, LSGCPD_EINVAL, "newton_max out of range");
-    LSG_CHECK(isfinite(p.sigma2_floor_rel) && p.sigma2_floor_rel >= 0.0, LSGCPD_EINVAL, "bad sigma2_floor_rel");
-    LSG_CHECK(isfinite(p.sigma2_init) && isfinite(p.tol), LSGCPD_EINVAL, "sigma2_init and tol must be finite");
-    LSG_CHECK(!(p.eta >= 1.0) && !isnan(p.eta), LSGCPD_EINVAL, "eta must be < 1 (negative: off)");
     double Rid[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, tid[3] = {0, 0, 0};
     const double* R = R0 ? R0 : Rid;
     const double* t = t0 ? t0 : tid;
-    LSG_CHECK(p.group == 0 || p.group == 1, LSGCPD_EINVAL, "group must be 0 (SE(3)) or 1 (affine)");
-    LSG_CHECK(pose_ok(R, p.group), LSGCPD_EINVAL,
-              p.group ? "A0 must be finite with det A0 > 0" : "R0 is not a rotation matrix (to 1e-6)");
-    LSG_CHECK(finite_vec(t, 3), LSGCPD_EINVAL, "t0 must be finite");
+    int rc0 = check_em_params(p, R, t);
+    if (rc0) return rc0;
     cudaStream_t s = (cudaStream_t)stream;
     TargetHeader h;
     int rc = read_header(d_target, M, &h, s);
@@ -540,21 +598,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     IterState* st = reinterpret_cast<IterState*>(ws + L.state);
     double* mom = reinterpret_cast<double*>(ws + L.mom);
     double* sums = reinterpret_cast<double*>(ws + L.sums);
-    RegParams rp;
-    memset(&rp, 0, sizeof(rp));
-    rp.w = p.eta >= 0.0 ? 0.0 : p.w;
-    rp.eta = p.eta >= 0.0 ? p.eta : -1.0;
-    rp.spc = h.spc;
-    rp.phi = p.d_src_conf;
-    rp.V = V;
-    rp.floor = p.sigma2_floor_rel * h.extent * h.extent;
-    rp.tol = p.tol;
-    rp.omega_ref_target = h.omega_ref;
-    rp.M = M;
-    rp.newton_max = p.newton_max;
-    rp.consistent = p.consistent_normalizer ? 1 : 0;
-    rp.max_iters = p.max_iters;
-    rp.group = p.group;
+    const RegParams rp = reg_params(p, h, V, M);
 
     LSG_CUDA(cudaMemsetAsync(ws + L.counters, 0, sizeof(unsigned) * 8, s));
     LSG_CUDA(cudaMemsetAsync(ws + L.iters, 0, sizeof(int) * 4, s));
@@ -573,17 +617,15 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
 
     // EM iterations: captured once into a CUDA graph and replayed (no host sync per iteration)
     NvtxRange rem("EM iterations");
-    const char* env = getenv("LSGCPD_NO_GRAPH");
-    const bool use_graph = p.max_iters > 1 && !(env && env[0] == '1');
+    const Options& op = options();
+    const bool use_graph = p.max_iters > 1 && op.no_graph.load() != 1;
     if (use_graph) {
-        const char* nf = getenv("LSGCPD_NO_FUSE");
-        const char* gc = getenv("LSGCPD_GRAPH_CACHE");
         // (not with a communicator: a destroyed and re-created comm could reuse the address)
-        const bool cache = !(gc && gc[0] == '0') && c == nullptr;
+        const bool cache = op.graph_cache.load() != 0 && c == nullptr;
         std::vector<unsigned char> key, topo;
         int dev = 0;
         LSG_CUDA(cudaGetDevice(&dev));
-        const int nofuse = (nf && nf[0] == '1') ? 1 : 0;
+        const int nofuse = op.no_fuse.load() == 1 ? 1 : 0;
         key_put(topo, dev);
         key_put(topo, N_local);
         key_put(topo, sc);
@@ -600,7 +642,8 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
         GraphRun local;
         if (!g) {
             // capture this call's iteration on a scratch stream of this thread
-            cudaStream_t& cap = g_graphs.cap;
+            LSG_CHECK(dev >= 0 && dev < GraphCache::kMaxDev, LSGCPD_ECUDA, "device ordinal %d out of range", dev);
+            cudaStream_t& cap = g_graphs.cap[dev];
             if (!cap) LSG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
             LSG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
             cudaGraph_t graph = nullptr;
@@ -668,6 +711,146 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     }
     if (fin.status == LSGCPD_EINVAL) {
         set_error("non-finite coordinate in the source cloud");
+        return LSGCPD_EINVAL;
+    }
+    return 0;
+}
+
+// The multi-GPU protocol of lsgcpd_register (source shards, replicated target, one 75-double all-reduce of the
+// moments per EM iteration and one of the σ²₀ sums, Newton run redundantly per rank) with G shards on ONE
+// device: every shard's E step, merge, moments and Newton are the kernels lsgcpd_register enqueues with a
+// communicator; only the all-reduce is a fixed-order device sum (shard_allreduce_kernel).  Test support for
+// SURVEY §8(c).6 step 4 on a one-GPU box; no graph capture.
+LSG_EXPORT int lsgcpd_register_shards(const void* d_target, int64_t M, double volume, const float* const* h_d_src,
+                                      const int64_t* h_N, int G, const lsgcpd_em_params* params, const double R0[9],
+                                      const double t0[3], double* R_out, double* t_out, double* sigma2_out,
+                                      int* iters_out, void* d_ws, size_t ws_stride, lsgcpd_stream_t stream) {
+    lsgcpd_em_params p;
+    lsgcpd_em_params_default(&p);
+    if (params) p = *params;
+    LSG_CHECK(d_target && h_d_src && h_N && d_ws && R_out && t_out && sigma2_out && iters_out, LSGCPD_EINVAL,
+              "null pointer argument");
+    LSG_CHECK(G >= 1 && G <= kMaxShards, LSGCPD_EINVAL, "G=%d out of range [1, %d]", G, kMaxShards);
+    LSG_CHECK(aligned16(d_target) && aligned16(d_ws) && (ws_stride & 255) == 0, LSGCPD_EINVAL,
+              "d_target and d_ws must be 16-byte aligned, ws_stride a multiple of 256");
+    double Rid[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, tid[3] = {0, 0, 0};
+    const double* R = R0 ? R0 : Rid;
+    const double* t = t0 ? t0 : tid;
+    int rc = check_em_params(p, R, t);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    TargetHeader h;
+    rc = read_header(d_target, M, &h, s);
+    if (rc) return rc;
+    LSG_CHECK(p.consistent_normalizer || !h.prior, LSGCPD_EINVAL, "component priors require consistent_normalizer = 1");
+    LSG_CHECK(p.d_src_conf == nullptr, LSGCPD_EINVAL, "per-point confidences are not supported with shards");
+    const double V = volume > 0.0 ? volume : h.volume;
+    LSG_CHECK(isfinite(V) && V > 0.0, LSGCPD_EINVAL, "volume must be finite and > 0");
+    const RegParams rp = reg_params(p, h, V, M);
+    std::vector<RegLayout> L(G);
+    std::vector<Sched> sc(G);
+    std::vector<char*> ws(G);
+    ShardPtrs mom{}, sums{};
+    for (int g = 0; g < G; ++g) {
+        LSG_CHECK(h_d_src[g] && h_N[g] >= 1 && h_N[g] < (int64_t)1 << 34, LSGCPD_EINVAL, "shard %d: bad source", g);
+        rc = reg_layout(h.M_pad, h_N[g], p.max_iters, &L[g], &sc[g]);
+        if (rc) return rc;
+        LSG_CHECK(ws_stride >= L[g].total, LSGCPD_EINVAL, "ws_stride too small (%zu < %zu)", ws_stride, L[g].total);
+        ws[g] = static_cast<char*>(d_ws) + (size_t)g * ws_stride;
+        mom.p[g] = reinterpret_cast<double*>(ws[g] + L[g].mom);
+        sums.p[g] = reinterpret_cast<double*>(ws[g] + L[g].sums);
+    }
+    NvtxRange r("lsgcpd_register_shards");
+    for (int g = 0; g < G; ++g) {
+        char* w = ws[g];
+        LSG_CUDA(cudaMemsetAsync(w + L[g].counters, 0, sizeof(unsigned) * 8, s));
+        LSG_CUDA(cudaMemsetAsync(w + L[g].iters, 0, sizeof(int) * 4, s));
+        LSG_CUDA(cudaMemsetAsync(w + L[g].nll, 0, sizeof(double) * (p.max_iters + 1), s));
+        LSG_CUDA(cudaMemsetAsync(w + L[g].sig2, 0, sizeof(double) * (p.max_iters + 2), s));
+        estep_launch_setup(reinterpret_cast<IterState*>(w + L[g].state), d_target, R, t, 1.0, rp.w, V, M,
+                           rp.consistent, rp.eta, s);
+        sigma2_sums_launch(h_d_src[g], h_N[g], reinterpret_cast<IterState*>(w + L[g].state), d_target,
+                           reinterpret_cast<double*>(w + L[g].blockpart), sums.p[g],
+                           reinterpret_cast<unsigned*>(w + L[g].counters), s);
+    }
+    shard_allreduce_kernel<<<1, 32, 0, s>>>(sums, G, 2);
+    for (int g = 0; g < G; ++g)
+        sigma2_init_launch(reinterpret_cast<IterState*>(ws[g] + L[g].state), d_target, sums.p[g], rp, p.sigma2_init,
+                           reinterpret_cast<double*>(ws[g] + L[g].sig2), mom.p[g] + 75, s);
+    LSG_CUDA(cudaGetLastError());
+    for (int k = 0; k < p.max_iters; ++k) {
+        for (int g = 0; g < G; ++g) {
+            rc = enqueue_moments(d_target, h_d_src[g], h_N[g], ws[g], L[g], sc[g], rp, false, s);
+            if (rc) return rc;
+        }
+        shard_allreduce_kernel<<<(kMomentCount + 127) / 128, 128, 0, s>>>(mom, G, kMomentCount);
+        for (int g = 0; g < G; ++g) enqueue_newton(ws[g], L[g], rp, s);
+    }
+    LSG_CUDA(cudaGetLastError());
+    std::vector<IterState> fin(G);
+    for (int g = 0; g < G; ++g) {
+        LSG_CUDA(cudaMemcpyAsync(&fin[g], ws[g] + L[g].state, sizeof(IterState), cudaMemcpyDeviceToHost, s));
+        LSG_CUDA(cudaMemcpyAsync(iters_out + g, ws[g] + L[g].iters, sizeof(int), cudaMemcpyDeviceToHost, s));
+    }
+    LSG_CUDA(cudaStreamSynchronize(s));
+    int status = 0;
+    for (int g = 0; g < G; ++g) {
+        for (int i = 0; i < 9; ++i) R_out[9 * g + i] = fin[g].R[i];
+        for (int i = 0; i < 3; ++i) t_out[3 * g + i] = fin[g].t[i];
+        sigma2_out[g] = fin[g].sigma2;
+        if (fin[g].status) status = fin[g].status;
+    }
+    if (status == LSGCPD_ENOMASS) {
+        set_error("no inlier mass (sum P <= 1e-12 N) for 3 consecutive iterations");
+        return LSGCPD_ENOMASS;
+    }
+    if (status == LSGCPD_EINVAL) {
+        set_error("non-finite coordinate in the source cloud");
+        return LSGCPD_EINVAL;
+    }
+    return 0;
+}
+
+// Run-time options (diagnostics and tests); see include/lsgcpd.h.
+LSG_EXPORT int lsgcpd_set_option(const char* name, double value) {
+    LSG_CHECK(name && isfinite(value), LSGCPD_EINVAL, "bad option name or value");
+    Options& o = options();
+    const int iv = (int)value;
+    if (!strcmp(name, "tc")) {
+        LSG_CHECK(iv >= 0 && iv <= 2, LSGCPD_EINVAL, "tc must be 0, 1 or 2");
+        o.tc.store(iv);
+    } else if (!strcmp(name, "estep_variant")) {
+        LSG_CHECK(iv >= -1 && iv <= 2, LSGCPD_EINVAL, "estep_variant must be -1..2");
+        o.estep_variant.store(iv);
+    } else if (!strcmp(name, "halves")) {
+        o.halves.store(iv);
+    } else if (!strcmp(name, "no_fuse")) {
+        o.no_fuse.store(iv);
+    } else if (!strcmp(name, "graph_cache")) {
+        o.graph_cache.store(iv);
+    } else if (!strcmp(name, "no_graph")) {
+        o.no_graph.store(iv);
+    } else if (!strcmp(name, "tile_gate")) {
+        o.tile_gate.store((float)value);
+    } else {
+        set_error("unknown option '%s'", name);
+        return LSGCPD_EINVAL;
+    }
+    return 0;
+}
+
+LSG_EXPORT int lsgcpd_get_option(const char* name, double* value) {
+    LSG_CHECK(name && value, LSGCPD_EINVAL, "null pointer argument");
+    const Options& o = options();
+    if (!strcmp(name, "tc")) *value = o.tc.load();
+    else if (!strcmp(name, "estep_variant")) *value = o.estep_variant.load();
+    else if (!strcmp(name, "halves")) *value = o.halves.load();
+    else if (!strcmp(name, "no_fuse")) *value = o.no_fuse.load();
+    else if (!strcmp(name, "graph_cache")) *value = o.graph_cache.load();
+    else if (!strcmp(name, "no_graph")) *value = o.no_graph.load();
+    else if (!strcmp(name, "tile_gate")) *value = o.tile_gate.load();
+    else {
+        set_error("unknown option '%s'", name);
         return LSGCPD_EINVAL;
     }
     return 0;
@@ -774,6 +957,7 @@ static int batch_layout(const lsgcpd_problem* P, int B, int max_iters, BatchLayo
     Sched sc;
     memset(&sc, 0, sizeof(sc));
     sc.halves = 1;
+    sc.gate_g = options().tile_gate.load();
     sc.U = units;
     const int64_t slots = (int64_t)nsm;       // one CTA per SM (both batched E-step kernels)
     sc.G = units < slots ? units : slots;

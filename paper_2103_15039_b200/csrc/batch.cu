@@ -11,6 +11,8 @@
 // partial, reloads the problem's constants (k2, pose, fixed/running-max mode) and source points, and the
 // TMA producer switches to that problem's target.  Problems that finished (IterState.active = 0) are
 // skipped by producer and consumers alike.
+#include <mutex>
+
 #include "common.cuh"
 #include "estep_dev.cuh"
 #include "kernels.h"
@@ -430,9 +432,9 @@ __global__ void __launch_bounds__(kBTThreads, 1)
     const int tid = threadIdx.x;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(wg * kWGCols);
     constexpr int kRC = kNCW * 32 * RB;
-    float2 h[RB][3], l[RB][3];
+    float h[RB][3], l[RB][3];   // x̂ as FP32 hi/lo
     float Rt[RB], Ct[RB];
-    float k2 = 0.f;
+    float k2 = 0.f, gate = 0.f;
     float2 nk2 = bc(0.f);
     int nfold = 0;
 
@@ -440,6 +442,7 @@ __global__ void __launch_bounds__(kBTThreads, 1)
         const IterState* s = st + b;
         k2 = s->k2;
         nk2 = bc(-k2);
+        gate = sc.gate_g * (float)sqrt(s->sigma2);
         double Rm[9], tv[3];
 #pragma unroll
         for (int i = 0; i < 9; ++i) Rm[i] = s->R[i];
@@ -461,9 +464,8 @@ __global__ void __launch_bounds__(kBTThreads, 1)
                                  fma(Rm[6], x0, fma(Rm[7], x1, fma(Rm[8], x2, tv[2])))};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const float hi = __double2float_rn(X[a]);
-                h[k][a] = bc(hi);
-                l[k][a] = bc(__double2float_rn(X[a] - (double)hi));
+                h[k][a] = __double2float_rn(X[a]);
+                l[k][a] = __double2float_rn(X[a] - (double)h[k][a]);
             }
             Rt[k] = Ct[k] = 0.f;
 #pragma unroll
@@ -524,32 +526,12 @@ __global__ void __launch_bounds__(kBTThreads, 1)
             base[15 * kBlk + bb] = 0.f;
         }
     };
-    auto chunk = [&](const float4* core, int c, float2 (&Lt)[RB], auto ABc) {
+    // one K step (tile-centred or hi/lo residual, estep_dev.cuh), then the A rows into TMEM
+    auto chunk = [&](const float4* core, int c, const float2 (&xa)[RB][3], const float2 (&xb)[RB][3],
+                     float2 (&Lt)[RB], auto ABc, auto cheapc) {
         constexpr int AB = decltype(ABc)::value;
         uint32_t av[RB][16];
-#pragma unroll
-        for (int pp = 0; pp < 4; ++pp) {
-            const int pr = c * 4 + pp;
-            const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
-#pragma unroll
-            for (int rb = 0; rb < RB; ++rb) {
-                const float2 rx = __fadd2_rn(__fadd2_rn(h[rb][0], make_float2(-v0.x, -v0.y)), l[rb][0]);
-                const float2 ry = __fadd2_rn(__fadd2_rn(h[rb][1], make_float2(-v0.z, -v0.w)), l[rb][1]);
-                const float2 rz = __fadd2_rn(__fadd2_rn(h[rb][2], make_float2(-v1.x, -v1.y)), l[rb][2]);
-                const float2 qv = __ffma2_rn(make_float2(v3.x, v3.y), rz,
-                                             __ffma2_rn(make_float2(v2.z, v2.w), ry, __fmul2_rn(make_float2(v2.x, v2.y), rx)));
-                const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
-                const float2 e = kLiteral ? __fmul2_rn(nk2, tau) : __ffma2_rn(nk2, tau, make_float2(v1.z, v1.w));
-                const float2 p = make_float2(ex2_approx(e.x), ex2_approx(e.y));
-                Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
-                const uint32_t hx = __float_as_uint(p.x) & 0xFFFFE000u, hy = __float_as_uint(p.y) & 0xFFFFE000u;
-                const float2 lo = __fadd2_rn(p, make_float2(-__uint_as_float(hx), -__uint_as_float(hy)));
-                av[rb][2 * pp] = hx;
-                av[rb][2 * pp + 1] = hy;
-                av[rb][8 + 2 * pp] = __float_as_uint(lo.x);
-                av[rb][8 + 2 * pp + 1] = __float_as_uint(lo.y);
-            }
-        }
+        tc_chunk_pairs<kLiteral, decltype(cheapc)::value, RB>(core, c, xa, xb, nk2, Lt, av);
         mbar_wait_sleep(&aempty[wg][AB], (uint32_t)(((c >> 1) & 1) ^ 1));
         tc_fence_after();
 #pragma unroll
@@ -579,15 +561,22 @@ __global__ void __launch_bounds__(kBTThreads, 1)
         float2 Lt[RB];
 #pragma unroll
         for (int k = 0; k < RB; ++k) Lt[k] = make_float2(0.f, 0.f);
+        const TileMeta tm = tile_meta(core);
+        auto run_tile = [&](auto cheapc) {
+            float2 xa[RB][3], xb[RB][3];
+            tile_points<decltype(cheapc)::value, RB>(h, l, tm, xa, xb);
 #pragma unroll 1
-        for (int c = 0; c < kChunks; c += 2) {
-            chunk(core, c, Lt, std::integral_constant<int, 0>());
-            chunk(core, c + 1, Lt, std::integral_constant<int, 1>());
-            if (c == 0 && pending) {
-                drain(pend_g);
-                pending = false;
+            for (int c = 0; c < kChunks; c += 2) {
+                chunk(core, c, xa, xb, Lt, std::integral_constant<int, 0>(), cheapc);
+                chunk(core, c + 1, xa, xb, Lt, std::integral_constant<int, 1>(), cheapc);
+                if (c == 0 && pending && tig >= kDrainLag) {
+                    drain(pend_g);
+                    pending = false;
+                }
             }
-        }
+        };
+        if (tile_cheap(tm, gate)) run_tile(std::true_type());
+        else run_tile(std::false_type());
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);
 #pragma unroll
@@ -602,6 +591,10 @@ __global__ void __launch_bounds__(kBTThreads, 1)
         const bool last = tig + 1 == NT || block_end;
         if (last) {
             if (block_end) {
+                if (pending) {
+                    drain(pend_g);
+                    pending = false;
+                }
                 drain(grp);
                 flush(cur_b, cur_j);
             } else {
@@ -662,22 +655,24 @@ void batch_fill_launch(BatchProblem* bp, int B, int consistent, int* err, cudaSt
     batch_fill_kernel<<<(B + 127) / 128, 128, 0, stream>>>(bp, B, consistent, err);
 }
 
-static int batch_tc_mode() {   // LSGCPD_TC: unset / 1 = tensor cores for fixed-max problems, 0 = CUDA cores only
-    const char* e = getenv("LSGCPD_TC");
-    return e ? (atoi(e) != 0) : 1;
-}
+// tensor cores for the fixed-max problems unless the tc option is 0 (CUDA cores only)
+static int batch_tc_mode() { return options().tc.load() != 0 ? 1 : 0; }
+static std::mutex g_battr_mu;
+static bool g_battr[64];   // per device: the tensor-core kernel's shared-memory attribute is set
 
 void estep_batch_launch(const BatchProblem* bp, int B, const Sched& sc, const IterState* st, float* part, float* rec,
                         int64_t Ntot, int consistent, cudaStream_t stream) {
     const int tc = batch_tc_mode();
     if (tc) {
-        static bool attr = false;
-        if (!attr) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(g_battr_mu);
+        if (dev >= 0 && dev < 64 && !g_battr[dev]) {
             cudaFuncSetAttribute((const void*)estep_batch_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kBTSmem);
             cudaFuncSetAttribute((const void*)estep_batch_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kBTSmem);
-            attr = true;
+            g_battr[dev] = true;
         }
         if (consistent)
             estep_batch_tc_kernel<false><<<(unsigned)sc.G, kBTThreads, kBTSmem, stream>>>(bp, B, st, sc, part);

@@ -60,29 +60,39 @@ struct TargetHeader {
     uint32_t pad_[2];
 };
 static_assert(sizeof(TargetHeader) <= kHeaderBytes, "header too big");
-constexpr uint32_t kTargetMagic = 0x4c534743u;  // "LSGC"
+constexpr uint32_t kTargetMagic = 0x4c534744u;  // "LSGD": layout 2 (slot order, tile-centred core)
 
 inline int64_t pad_targets(int64_t M) { return (M + kTgtPadMultiple - 1) / kTgtPadMultiple * kTgtPadMultiple; }
 inline const float* target_body(const void* t) { return reinterpret_cast<const float*>(static_cast<const char*>(t) + kHeaderBytes); }
 inline float* target_body(void* t) { return reinterpret_cast<float*>(static_cast<char*>(t) + kHeaderBytes); }
 
+// Targets are stored in SLOT order: the pack sorts them along a Morton (Z-order) curve of the AABB, so the
+// 64 targets of a tile are spatially compact (DESIGN §8 "tile-centred residual").  The record is a sum over
+// targets and does not depend on their order.  A slot section maps original target index → slot.
+//
 // Tensor-core section (after the pair-interleaved body): per 64-target tile, 10 KB:
-//   [0, 2048)     core: 32 target pairs × 64 B, field f of targets (2i, 2i+1) adjacent, f = y0, y1, y2, ω̄,
-//                 ñ0, ñ1, ñ2, 0 (the CUDA-core part of the pair math, two targets per f32x2 instruction)
+//   [0, 2048)     core: 32 target pairs × 64 B, field f of targets (2i, 2i+1) adjacent, f = y'0, y'1, y'2,
+//                 ω̄, ñ0, ñ1, ñ2, meta.  y' = y - c_tile, exact in FP32 (c_a = 0 on an axis where it would
+//                 not be); the CUDA-core part of the pair math, two targets per f32x2 instruction.
+//                 meta of targets 0, 1, 2, 3 = c_0, c_1, c_2, E_tile = R_tile·√(1 + max α) with R_tile =
+//                 max ||y'|| over the tile's real targets (the E step's per-tile precision gate).
 //   [2048, 10240) 8 K-steps × 1024 B: the 32×8 B operand [F_hi; F_lo] of one K step, where
-//                 F[f][m] = (1, y, W, b, 0,0,0), F_hi = F rounded to TF32 (nearest), F_lo = F - F_hi
-//                 (exact in FP32, read as TF32 by the MMA); UMMA K-major, no swizzle:
+//                 F[f][m] = (1, y, W, b, 0,0,0) (original coordinates), F_hi = F rounded to TF32 (nearest),
+//                 F_lo = F - F_hi (exact in FP32, read as TF32 by the MMA); UMMA K-major, no swizzle:
 //                 core matrix = 8 rows × 16 B (4 targets); LBO = 128 B (next 4 targets),
 //                 SBO = 256 B (next 8 rows): byte(row r, j) = 1024 s + (r/8) 256 + (j/4) 128 + (r%8) 16 + (j%4) 4.
+// Slot section (after the tensor-core section): int32 slot_of[M_pad], slot_of[m] = slot of original target m.
 constexpr int kTT_host = 64;   // E-step target tile (targets), host-visible copy of estep_dev.cuh's kTT
 constexpr int kTcTile = 64;
 constexpr int kTcTileBytes = 10240;
 constexpr int kTcCoreBytes = 2048;
 constexpr int kTcBOff = 2048;
 inline size_t tc_section_offset(int64_t M_pad) { return kHeaderBytes + (size_t)M_pad * kTgtFloats * sizeof(float); }
-inline size_t target_total_bytes(int64_t M_pad) { return tc_section_offset(M_pad) + (size_t)(M_pad / kTcTile) * kTcTileBytes; }
+inline size_t slot_section_offset(int64_t M_pad) { return tc_section_offset(M_pad) + (size_t)(M_pad / kTcTile) * kTcTileBytes; }
+inline size_t target_total_bytes(int64_t M_pad) { return slot_section_offset(M_pad) + (size_t)M_pad * sizeof(int32_t); }
 inline const float* target_tc(const void* t, int64_t M_pad) { return reinterpret_cast<const float*>(static_cast<const char*>(t) + tc_section_offset(M_pad)); }
 inline float* target_tc(void* t, int64_t M_pad) { return reinterpret_cast<float*>(static_cast<char*>(t) + tc_section_offset(M_pad)); }
+inline int32_t* target_slots(void* t, int64_t M_pad) { return reinterpret_cast<int32_t*>(static_cast<char*>(t) + slot_section_offset(M_pad)); }
 
 // ------------------------------------------------------------------------------------------
 // Per-E-step constants, computed in FP64 on the device (setup kernel or the Newton kernel),
@@ -224,7 +234,7 @@ struct Sched {
     int variant;      // E-step kernel variant (negative: tensor-core kernel + CUDA-core variant -1-variant)
     int tc_variant;   // tensor-core kernel configuration
     int halves;       // 2: the targets are swept as two halves, one launch each (T = tiles per half); else 1
-    int pad_;
+    float gate_g;     // tile-centred residual when E_tile ≤ gate_g·σ, else the hi/lo residual
     int64_t hstride;  // floats between the two halves' partial sets
 };
 __host__ __device__ inline int64_t sched_start(const Sched& s, int64_t g) { return g * s.U / s.G; }

@@ -18,6 +18,8 @@
 // target field as a broadcast operand (PACKED), or scalar FP32 (reference variant).
 #include <string.h>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "estep_dev.cuh"
 #include "kernels.h"
@@ -25,6 +27,8 @@
 namespace lsg {
 
 // ---- setup: per-call constants (lsgcpd_estep path) ---------------------------------------
+// The target header is checked here (no host synchronisation): a buffer that is not a prepared target of M
+// points leaves the state inactive with status EINVAL, and the merge writes an all-NaN record.
 __global__ void estep_setup_kernel(IterState* st, const TargetHeader* hdr, double r0, double r1, double r2,
                                    double r3, double r4, double r5, double r6, double r7, double r8, double t0,
                                    double t1, double t2, double sigma2, double w, double V, int64_t M,
@@ -32,11 +36,12 @@ __global__ void estep_setup_kernel(IterState* st, const TargetHeader* hdr, doubl
     const double R[9] = {r0, r1, r2, r3, r4, r5, r6, r7, r8};
     const double t[3] = {t0, t1, t2};
     IterState s;
-    make_state(s, R, t, sigma2, w, V, M, hdr->omega_ref, consistent, eta, hdr->spc);
-    s.extent = hdr->extent;
-    s.active = 1;
+    const bool ok = hdr->magic == kTargetMagic && hdr->M == M;
+    make_state(s, R, t, sigma2, w, V, M, ok ? hdr->omega_ref : 0.0, consistent, eta, ok ? hdr->spc : 1.0);
+    s.extent = ok ? hdr->extent : 0.0;
+    s.active = ok ? 1 : 0;
     s.iter = 0;
-    s.status = 0;
+    s.status = ok ? 0 : LSGCPD_EINVAL;
     s.no_mass = 0;
     s.last_step_rot = s.last_step_trans = 0.0;
     *st = s;
@@ -239,376 +244,69 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     if (cur_blk >= 0) flush(cur_blk);
 }
 
-// ---- tensor-core (tcgen05) variant --------------------------------------------------------------
+// ---- tensor-core (tcgen05) E step --------------------------------------------------------------------
 // The 13 target-feature accumulations Σ_m p_mn F_m (F = 1, y, α n nᵀ, α(n·y)n) are a dense K = M
-// contraction D[points × 16] += P[points × K] · F[K × 16].  The CUDA cores compute p per pair (τ, e,
-// MUFU.EX2) and Σ p τ; p is split into TF32 hi + lo (p_hi = p with the low 13 mantissa bits cleared,
-// p_lo = p - p_hi exactly) and written to TMEM as the A operand; one elected thread per warpgroup
-// issues tcgen05.mma.kind::tf32 (A from TMEM, B = F_hi / F_lo from shared memory, D in TMEM):
-// D += A_hi F_hi + A_lo F_hi + A_hi F_lo (3×TF32 ≈ FP32 products).  D is drained to registers and
-// Kahan-folded after every 64-target tile (FP32 error independent of M).  Fixed-max mode only; the
-// running-max mode (w = 0 or tiny w) is served by the CUDA-core kernel.
-// TC kernel configuration: NWG consumer warpgroups (128 TMEM lanes each), RB row blocks (points) per
-// thread, MW MMA-issuing warps.  TMEM per warpgroup: RB × (D 32 + A 2 buffers × 16) = 64·RB columns.
-template <int NWG, int RB, int MW>
-struct TcCfg {
-    static constexpr int kNCW = 4 * NWG;
-    static constexpr int kThreads = (kNCW + 1 + MW) * 32;
-    static constexpr int kWGCols = 64 * RB;
-    static constexpr int kBlk = NWG * 128 * RB;
-    static constexpr size_t kSmem = (size_t)26 * kNCW * 32 * RB * sizeof(float);   // Kahan R, C
-    static_assert(NWG * kWGCols <= kTcCols, "TMEM columns");
-    static_assert(kThreads <= 1024, "threads");
-    static_assert(NWG % MW == 0, "MMA warps must split the warpgroups evenly");
-};
-// Warp roles: 4·NWG consumer warps (NWG warpgroups × 128 TMEM lanes), 1 TMA producer warp, MW MMA warps.
-// Per warpgroup mbarriers: afull[b] (4 warp arrivals: A buffer b written), aempty[b] (MMA commit: buffer
-// b consumed), dfull (commit after a tile's last MMAs: D ready), dfree (4 arrivals: D drained).
-// The running Kahan sums live in shared memory (touched once per tile), leaving registers for
-// in-flight pairs: the kernel is latency-bound on the τ → e → ex2 chain, so warps matter.
-template <int NWG, int RB, int MW, bool kLiteral>
-__global__ void __launch_bounds__(TcCfg<NWG, RB, MW>::kThreads, 1)
-    estep_tc_kernel(const char* __restrict__ tc, const float* __restrict__ src, int64_t N,
-                    const IterState* __restrict__ st, Sched sc, float* __restrict__ part) {
-    using Cfg = TcCfg<NWG, RB, MW>;
-    constexpr int kNCW = Cfg::kNCW;
-    constexpr int kBlk = Cfg::kBlk;
-    constexpr int kWGCols = Cfg::kWGCols;
-    constexpr int kChunks = kTcTile / kTcChunk;
-    // static shared memory for the TMA stages (link-time constant addresses: the MMA warps' B
-    // descriptors become immediates); dynamic shared memory for the Kahan running sums
-    __shared__ __align__(1024) char tiles_st[kTcStages][kTcTileBytes];
-    extern __shared__ __align__(16) char dsmem[];
-    float* smRC = reinterpret_cast<float*>(dsmem);   // [26][RB × consumer threads]
-    __shared__ __align__(8) uint64_t full_bar[kTcStages];
-    __shared__ __align__(8) uint64_t empty_bar[kTcStages];
-    __shared__ __align__(8) uint64_t afull[NWG][2], aempty[NWG][2], dfull[NWG], dfree[NWG];
-    __shared__ uint32_t tmem_base_sh;
-
-    if (!st->active || !st->fixed) return;
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int64_t g = blockIdx.x;
-    const int64_t u0 = sched_start(sc, g), u1 = sched_start(sc, g + 1);
-    if (u0 >= u1) return;
-
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                     "r"((uint32_t)kTcCols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    if (threadIdx.x == 32) {
-        for (int s = 0; s < kTcStages; ++s) {
-            mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], kNCW);
-        }
-        for (int w = 0; w < NWG; ++w) {
-            mbar_init(&afull[w][0], 4);
-            mbar_init(&afull[w][1], 4);
-            mbar_init(&aempty[w][0], 1);
-            mbar_init(&aempty[w][1], 1);
-            mbar_init(&dfull[w], 1);
-            mbar_init(&dfree[w], 4);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = tmem_base_sh;
-    if (tmem != 0u) __trap();   // 512 columns = the whole TMEM: the allocation must start at lane 0, column 0
-
-    if (warp == kNCW) {
-        // ---------------- producer warp: TMA bulk copies of 10-KB tensor-core tiles ----------------
-        if (lane == 0) {
-            int64_t it = 0;
-            for (int64_t u = u0; u < u1; ++u, ++it) {
-                const int s = (int)(it % kTcStages);
-                const uint32_t ph = (uint32_t)((it / kTcStages) & 1);
-                mbar_wait_sleep(&empty_bar[s], ph ^ 1);
-                const int64_t tile = u % sc.T;
-                mbar_arrive_expect_tx(&full_bar[s], kTcTileBytes);
-                bulk_g2s(&tiles_st[s][0], tc + tile * (int64_t)kTcTileBytes, kTcTileBytes, &full_bar[s]);
-            }
-        }
-        return;
-    }
-    if (warp > kNCW) {
-        // ---------------- MMA warps: warp-uniform loop, one elected lane issues tcgen05.mma ----------------
-        // per warpgroup w, row block rb, K step c:  D[:, 0:32] (+)= A_hi · [F_hi | F_lo]   (N = 32)
-        //                                           D[:, 0:16]  += A_lo · F_hi             (N = 16)
-        // The CTA owns all 512 TMEM columns, so every TMEM operand is a compile-time constant.
-        const int mw = warp - kNCW - 1;
-        constexpr int kWPer = NWG / MW;
-        uint32_t aph[kWPer][2] = {}, fph[kWPer] = {};
-        for (int64_t ub = u0; ub < u1; ub += kTcStages) {
-            const uint32_t round_ph = (uint32_t)(((ub - u0) / kTcStages) & 1);
-#pragma unroll
-            for (int s = 0; s < kTcStages; ++s) {   // stage index is a compile-time constant
-                if (ub + s >= u1) break;
-                mbar_wait(&full_bar[s], round_ph);
-#pragma unroll
-                for (int c = 0; c < kChunks; ++c) {
-                    const int buf = c & 1;   // kChunks is even: the buffer parity restarts every tile
-                    const uint64_t b32 = bdesc(smem_u32(&tiles_st[s][0]) + kTcBOff + 1024 * c);
-#pragma unroll
-                    for (int wi = 0; wi < kWPer; ++wi) {
-                        const int w = mw * kWPer + wi;
-                        if (c == 0 && (ub + s) > u0) {   // D must be drained before it is overwritten
-                            mbar_wait(&dfree[w], fph[wi]);
-                            fph[wi] ^= 1u;
-                        }
-                        mbar_wait(&afull[w][buf], aph[wi][buf]);
-                        aph[wi][buf] ^= 1u;
-                        tc_fence_after();
-                        if (elect_one()) {
-                            const uint32_t colD = (uint32_t)(w * kWGCols);
-                            const uint32_t colA = colD + 32 * RB + buf * 16 * RB;
-#pragma unroll
-                            for (int rb = 0; rb < RB; ++rb) {
-                                mma_tf32_ts(colD + rb * 32, colA + rb * 16, b32, kTcIdesc32, c == 0 ? 0u : 1u);
-                                mma_tf32_ts(colD + rb * 32, colA + rb * 16 + 8, b32, kTcIdesc16, 1u);
-                            }
-                            mma_commit(&aempty[w][buf]);
-                            if (c == kChunks - 1) mma_commit(&dfull[w]);
-                        }
-                        __syncwarp();
-                    }
-                }
-            }
-        }
-        return;
-    }
-
-    // ---------------- consumers: warpgroup wg, TMEM lane quadrant q ----------------
-    // Each thread owns one point in each of its RB 128-row blocks; f32x2 instructions cover two
-    // consecutive TARGETS, so {p_m, p_m+1} pairs go straight into consecutive A columns of TMEM.
-    const int wg = warp >> 2, q = warp & 3;
-    const int tw = q * 32 + lane;                      // thread (= TMEM lane) within the warpgroup
-    const int tid = threadIdx.x;                       // consumer thread id (smem column)
-    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t colD0 = (uint32_t)(wg * kWGCols), colA0 = colD0 + 32 * RB;
-    const uint32_t aempty_a[2] = {smem_u32(&aempty[wg][0]), smem_u32(&aempty[wg][1])};
-    const uint32_t afull_a[2] = {smem_u32(&afull[wg][0]), smem_u32(&afull[wg][1])};
-    const float k2 = st->k2;
-    const float2 nk2 = bc(-k2);
-    double Rm[9], tv[3];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) Rm[i] = st->R[i];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) tv[i] = st->t[i];
-
-    float h[RB][3], l[RB][3];
-    float Rt[RB], Ct[RB];
-    int64_t cur_blk = -1;
-    uint32_t eph[2] = {0u, 0u}, dph = 0u;
-    bool used[2] = {false, false};
-    uint32_t cc = 0;
-    constexpr int kRC = kNCW * 32 * RB;
-
-    auto load_points = [&](int64_t j) {
-#pragma unroll
-        for (int k = 0; k < RB; ++k) {
-            const int64_t n = j * kBlk + (wg * RB + k) * 128 + tw;
-            double x0 = 0.0, x1 = 0.0, x2 = 0.0;
-            if (n < N) {
-                x0 = src[3 * n];
-                x1 = src[3 * n + 1];
-                x2 = src[3 * n + 2];
-            }
-            const double X[3] = {fma(Rm[0], x0, fma(Rm[1], x1, fma(Rm[2], x2, tv[0]))),
-                                 fma(Rm[3], x0, fma(Rm[4], x1, fma(Rm[5], x2, tv[1]))),
-                                 fma(Rm[6], x0, fma(Rm[7], x1, fma(Rm[8], x2, tv[2])))};
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                h[k][a] = __double2float_rn(X[a]);
-                l[k][a] = __double2float_rn(X[a] - (double)h[k][a]);
-            }
-            Rt[k] = Ct[k] = 0.f;
-#pragma unroll
-            for (int f = 0; f < 26; ++f) smRC[f * kRC + k * (kNCW * 32) + tid] = 0.f;
-        }
-    };
-    auto flush = [&](int64_t j) {
-        const int64_t slot = j * sc.kmax + (g - sched_owner(sc, j * sc.T));
-        float* base = part + slot * (int64_t)kPartF * kBlk;
-#pragma unroll
-        for (int k = 0; k < RB; ++k) {
-            const int b = (wg * RB + k) * 128 + tw;
-            const int rc = k * (kNCW * 32) + tid;
-#pragma unroll
-            for (int f = 0; f < 13; ++f) base[f * kBlk + b] = __fsub_rn(smRC[f * kRC + rc], smRC[(13 + f) * kRC + rc]);
-            base[13 * kBlk + b] = __fsub_rn(Rt[k], Ct[k]);
-            base[14 * kBlk + b] = 0.f;
-            base[15 * kBlk + b] = 0.f;
-        }
-    };
-
-    int64_t it = 0;
-    for (int64_t u = u0; u < u1; ++u, ++it) {
-        const int64_t j = u / sc.T;
-        if (j != cur_blk) {
-            if (cur_blk >= 0) flush(cur_blk);
-            cur_blk = j;
-            load_points(j);
-        }
-        const int s = (int)(it % kTcStages);
-        mbar_wait(&full_bar[s], (uint32_t)((it / kTcStages) & 1));
-        const float4* core = reinterpret_cast<const float4*>(&tiles_st[s][0]);
-        float2 Lt[RB];
-#pragma unroll
-        for (int k = 0; k < RB; ++k) Lt[k] = make_float2(0.f, 0.f);   // Σ p τ, {even, odd} targets
-#pragma unroll 1
-        for (int c = 0; c < kChunks; ++c, ++cc) {
-            const int buf = (int)(cc & 1u);
-            if (used[buf]) {                 // wait until the MMAs of two chunks ago released this A buffer
-                asm volatile(
-                    "{\n"
-                    ".reg .pred P1;\n"
-                    "WAITE_%=:\n"
-                    "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-                    "@!P1 bra WAITE_%=;\n"
-                    "}\n" ::"r"(aempty_a[buf]),
-                    "r"(eph[buf])
-                    : "memory");
-                eph[buf] ^= 1u;
-                tc_fence_after();
-            }
-            used[buf] = true;
-#ifdef LSG_TC_DIAG
-            float2 sink = make_float2(0.f, 0.f);
+// contraction D[points × 16] += P[points × K] · F[K × 16] (not the K = 3 cross term).  The CUDA cores
+// compute p per pair (residual, τ, e, MUFU.EX2) and Σ p τ; p is split into TF32 hi + lo (p_hi = p with the
+// low 13 mantissa bits cleared, p_lo = p - p_hi exactly) and written to TMEM as the A operand; one MMA warp
+// per warpgroup issues tcgen05.mma.kind::tf32 (A from TMEM, B = F_hi / F_lo from shared memory, D in TMEM):
+// D += A_hi F_hi + A_lo F_hi + A_hi F_lo (3×TF32 ≈ FP32 products).  Fixed-max mode only; the running-max
+// mode (w = 0 or tiny w) is served by the CUDA-core kernel.
+// Pipeline (no consumer ever waits on the tensor core in steady state):
+//  * per warpgroup two A buffers (afull: 4 warp arrivals, aempty: MMA commit) and two D buffers (dfull:
+//    commit after a D group's last MMAs, dfree: 4 arrivals after the drain); the chunk loop is unrolled by
+//    two, so every A-buffer index, mbarrier parity and TMEM column is a compile-time constant;
+//  * D accumulates kNT consecutive tiles of one source block (a "D group", which also ends at a block
+//    boundary); group g is drained after the second K step of group g + 1's first tile, when its MMAs have
+//    long completed; drained sums go into a plain FP32 running sum S1 that is Kahan-folded into (R, C)
+//    every kTcFold drains (FP32 error independent of M; the MMA accumulation over kNT = 4 tiles keeps a
+//    10× margin to the parity bar);
+//  * a shared-memory stage is released by the 12 consumer warps' arrivals plus one tcgen05.commit per MMA
+//    warp (its B operand read), independent of the drain.
+// Per tile the consumers pick the residual mode (tile_cheap): the tile-centred residual (13 FP32 lane-ops
+// per pair) on compact tiles, the hi/lo residual (16) on the others — estep_dev.cuh, DESIGN §8.
+// Warp roles: 12 consumer warps (3 warpgroups × 128 TMEM lanes, 2 points per thread = 768-point blocks),
+// 1 TMA producer warp, 3 MMA warps.  TMEM per warpgroup: D 2 × 32 + A 2 × 32 columns; 384 of 512 used
+// (the CTA allocates all 512: one CTA per SM).
+constexpr int kTcFold = 16;
+#ifndef LSG_TC_NWG
+#define LSG_TC_NWG 3
+#define LSG_TC_RB 2
 #endif
-#pragma unroll
-            for (int pp = 0; pp < 4; ++pp) {
-                const int pr = c * 4 + pp;   // target pair within the tile
-                const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
-                // v0 = {y0a, y0b, y1a, y1b}, v1 = {y2a, y2b, ωa, ωb}, v2 = {n0a, n0b, n1a, n1b}, v3 = {n2a, n2b, -, -}
-#pragma unroll
-                for (int rb = 0; rb < RB; ++rb) {
-                    const float2 rx = __fadd2_rn(__fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y)), bc(l[rb][0]));
-                    const float2 ry = __fadd2_rn(__fadd2_rn(bc(h[rb][1]), make_float2(-v0.z, -v0.w)), bc(l[rb][1]));
-                    const float2 rz = __fadd2_rn(__fadd2_rn(bc(h[rb][2]), make_float2(-v1.x, -v1.y)), bc(l[rb][2]));
-                    const float2 qv = __ffma2_rn(make_float2(v3.x, v3.y), rz,
-                                                 __ffma2_rn(make_float2(v2.z, v2.w), ry,
-                                                            __fmul2_rn(make_float2(v2.x, v2.y), rx)));
-                    const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
-                    const float2 e = kLiteral ? __fmul2_rn(nk2, tau) : __ffma2_rn(nk2, tau, make_float2(v1.z, v1.w));
-                    const float2 p = make_float2(ex2_approx(e.x), ex2_approx(e.y));
-                    Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
-                    const float2 hi = make_float2(__uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
-                                                  __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
-                    const float2 lo = __fadd2_rn(p, make_float2(-hi.x, -hi.y));
-                    // row block rb, A columns: [hi of targets 0-7 | lo of targets 0-7] of this K step
-#ifdef LSG_TC_DIAG
-                    sink = __fadd2_rn(sink, __fadd2_rn(hi, lo));
-#else
-                    tmem_st2(tl + colA0 + buf * 16 * RB + rb * 16 + 2 * pp, hi);
-                    tmem_st2(tl + colA0 + buf * 16 * RB + rb * 16 + 8 + 2 * pp, lo);
+#ifndef LSG_TC_UNROLL
+#define LSG_TC_UNROLL 2   // chunk-pair loop unrolled by two (tools/estep_time.py: +1 %)
 #endif
-                }
-            }
-#ifdef LSG_TC_DIAG
-            Lt[0].x += sink.x + sink.y;
-#else
-            tmem_wait_st();
-            tc_fence_before();
+// Register split between the warp roles (setmaxnreg, per warpgroup): warpgroup 3 (producer + MMA warps) keeps
+// 56 registers, each consumer thread gets 152 instead of the launch's 128 (ILP in the pair math; +1.7 %)
+#ifndef LSG_MAXNREG
+#define LSG_MAXNREG 152
+#define LSG_MAXNREG_LO 56
 #endif
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(afull_a[buf]) : "memory");
-        }
-        // tile done: wait for D, drain it, free D and the smem stage, Kahan-fold into shared memory
-        mbar_wait(&dfull[wg], dph);
-        dph ^= 1u;
-        tc_fence_after();
-        uint32_t dh[RB][16], dl[RB][16];
-#pragma unroll
-        for (int rb = 0; rb < RB; ++rb) {
-            tmem_ld16(tl + colD0 + rb * 32, dh[rb]);        // hi·hi + lo·hi
-            tmem_ld16(tl + colD0 + rb * 32 + 16, dl[rb]);   // hi·lo
-        }
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-            mbar_arrive(&dfree[wg]);
-            mbar_arrive(&empty_bar[s]);
-        }
-#pragma unroll
-        for (int rb = 0; rb < RB; ++rb) {
-            const int rc = rb * (kNCW * 32) + tid;
-#pragma unroll
-            for (int f = 0; f < 13; ++f) {
-                const float L = __uint_as_float(dh[rb][f]) + __uint_as_float(dl[rb][f]);
-                const float R = smRC[f * kRC + rc], C = smRC[(13 + f) * kRC + rc];
-                const float y = L - C;
-                const float t = R + y;
-                smRC[(13 + f) * kRC + rc] = (t - R) - y;
-                smRC[f * kRC + rc] = t;
-            }
-            const float L = Lt[rb].x + Lt[rb].y;
-            const float y = L - Ct[rb];
-            const float t = Rt[rb] + y;
-            Ct[rb] = (t - Rt[rb]) - y;
-            Rt[rb] = t;
-        }
-    }
-    if (cur_blk >= 0) flush(cur_blk);
-    // all MMAs of this warpgroup completed (dfull of the last tile was awaited); release TMEM
-    tc_fence_before();
-    named_bar_sync(1, kNCW * 32);
-    if (warp == 0) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)kTcCols)
-                     : "memory");
-    }
-}
-
-// ---- tensor-core E step, second generation ---------------------------------------------------------
-// Same arithmetic as estep_tc_kernel; the pipeline is restructured so that the consumer warps never wait
-// on the tensor core in steady state (ncu of the first generation: 22 % of warp samples in local-memory
-// round trips for the runtime-indexed A-buffer state, 8 % waiting for D after every tile):
-//  * the chunk loop is unrolled by two, so the A buffer, every mbarrier parity and every TMEM column are
-//    compile-time constants (no local memory, one uniform TMEM base per warp);
-//  * D is double-buffered and a single 16-column accumulator: D += A_hi·F_hi + A_lo·F_hi + A_hi·F_lo
-//    (three N = 16 MMAs per K step); tile t's D is drained after the second chunk of tile t + 1, by when
-//    its MMAs have long completed;
-//  * drained tile sums go into a plain FP32 running sum S1 (one add), which is Kahan-folded into the
-//    (R, C) running sums every kTc2Fold tiles: the FP32 error stays independent of M at a quarter of
-//    the per-tile cost;
-//  * unit → (source block, tile) bookkeeping is incremental (no 64-bit division per tile).
-// TMEM per warpgroup: D 2 × 16·RB columns, A 2 × 16·RB columns (hi 8 | lo 8 per row block).
-constexpr int kTc2Fold = 16;
-template <int NWG, int RB, bool kSelf, int MW>
-struct Tc2Cfg {
-    static constexpr int kNCW = 4 * NWG;
-    // consumers + TMA producer warp + MW MMA warps (none if each warpgroup issues its own MMAs)
-    static constexpr int kThreads = (kNCW + 1 + (kSelf ? 0 : MW)) * 32;
-    static_assert(NWG % MW == 0, "MMA warps must split the warpgroups evenly");
-    static constexpr int kWGCols = 64 * RB;
-    static constexpr int kBlk = NWG * 128 * RB;
-    static constexpr int kSmF = 39;                    // S1[13], R[13], C[13] per point
-    static constexpr size_t kSmem = (size_t)kSmF * kNCW * 32 * RB * sizeof(float);
-    static_assert(NWG * kWGCols <= kTcCols, "TMEM columns");
-    static_assert(kThreads <= 1024, "threads");
-};
+#define LSG_PRAGMA(x) _Pragma(#x)
+#define LSG_UNROLL(n) LSG_PRAGMA(unroll n)
+constexpr int kNWG = LSG_TC_NWG, kRB = LSG_TC_RB, kNT = 4;
+constexpr int kTcNCW = 4 * kNWG;                      // consumer warps
+constexpr int kTcThreads = (kTcNCW + 1 + kNWG) * 32;  // + producer + one MMA warp per warpgroup
+constexpr int kTcWGCols = 64 * kRB;
+constexpr int kTcBlk = kNWG * 128 * kRB;              // 768 source points per block
+constexpr int kTcSmF = 39;                            // S1[13], R[13], C[13] per point
+constexpr size_t kTcSmem = (size_t)kTcSmF * kTcNCW * 32 * kRB * sizeof(float);
+static_assert(kNWG * kTcWGCols <= kTcCols, "TMEM columns");
+static_assert(LSG_MAXNREG == 0 || (kTcNCW == 12 && kTcThreads == 512 && 384 * LSG_MAXNREG + 128 * LSG_MAXNREG_LO <= 65536),
+              "register split: 3 consumer warpgroups + warpgroup 3 within the register file");
 static_assert(kTcStages == 4, "stage arithmetic below assumes 4 stages");
 
-template <int NWG, int RB, bool kLiteral, bool kStX8, bool kSelf, int MW, int NT>
-__global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
-    estep_tc2_kernel(const char* __restrict__ tc, const float* __restrict__ src, int64_t N,
-                     const IterState* __restrict__ st, Sched sc, float* __restrict__ part) {
-    using Cfg = Tc2Cfg<NWG, RB, kSelf, MW>;
-    constexpr int kNCW = Cfg::kNCW;
-    constexpr int kBlk = Cfg::kBlk;
-    constexpr int kWGCols = Cfg::kWGCols;
+template <bool kLiteral>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    estep_tc_kernel(const char* __restrict__ tc, const float* __restrict__ src, int64_t N,
+                    const IterState* __restrict__ st, Sched sc, float* __restrict__ part) {
+    constexpr int NWG = kNWG, RB = kRB, NT = kNT;
+    constexpr int kNCW = kTcNCW;
+    constexpr int kBlk = kTcBlk;
+    constexpr int kWGCols = kTcWGCols;
     constexpr int kChunks = kTcTile / kTcChunk;
     static_assert(kChunks % 2 == 0, "chunks per tile must be even");
     constexpr int kNF = 13;   // D features kept: 1, y, W, b
-    // D accumulates NT consecutive tiles of one source block (a "D group") before it is drained; a group
-    // also ends at a block boundary and at the end of the CTA's range.  With MMA warps, a stage is
-    // released by the consumers when they finish reading it plus one tcgen05.commit per MMA warp.
-    static_assert(!kSelf || NT == 1, "self-issuing warpgroups drain every tile");
     __shared__ __align__(1024) char tiles_st[kTcStages][kTcTileBytes];
     extern __shared__ __align__(16) char dsmem[];
     float* smS = reinterpret_cast<float*>(dsmem);   // [3 kNF][RB × consumer threads]: S1, R, C
@@ -634,7 +332,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
     if (threadIdx.x == 32) {
         for (int s = 0; s < kTcStages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], kSelf ? kNCW : kNCW + MW);
+            mbar_init(&empty_bar[s], kNCW + NWG);
         }
         for (int w = 0; w < NWG; ++w)
             for (int b = 0; b < 2; ++b) {
@@ -651,6 +349,8 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
     const uint32_t tmem = tmem_base_sh;
     if (tmem != 0u) __trap();   // 512 columns = the whole TMEM: the allocation must start at column 0
 
+    if (warp >= kNCW) {   // warpgroup 3: the TMA producer warp and the MMA warps
+    if (LSG_MAXNREG > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(LSG_MAXNREG_LO));
     if (warp == kNCW) {
         // ---------------- producer warp: TMA bulk copies of the 10-KB tensor-core tiles ----------------
         if (lane == 0) {
@@ -665,16 +365,15 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         }
         return;
     }
-    if (!kSelf && warp > kNCW) {
-        // ---------------- MMA warp: one elected lane issues tcgen05.mma for every warpgroup ----------------
+    if (warp > kNCW) {
+        // ---------------- MMA warp w: one elected lane issues the tcgen05.mma of warpgroup w ----------------
         // D[db] (+)= A_hi·F_hi, += A_lo·F_hi, += A_hi·F_lo per row block and K step (N = 16 each).
         // Parities: the k-th completion of a barrier has parity k & 1; A buffer b of K step c of any tile
         // is used for the (4·it + c/2)-th time, so its parity is the constant (c >> 1) & 1.
         const uint32_t tiles0 = smem_u32(&tiles_st[0][0]) + kTcBOff;
-        constexpr int kWPer = NWG / MW;
-        const int w0 = (warp - kNCW - 1) * kWPer;   // this MMA warp serves warpgroups [w0, w0 + kWPer)
+        const int w = warp - kNCW - 1;
         int64_t tile = u0 % sc.T, grp = 0;
-        int tig = 0;                                  // tile index within the current D group
+        int tig = 0;   // tile index within the current D group
         for (int64_t it = 0; it < nunits; ++it) {
             const int s = (int)(it & 3);
             const int db = (int)(grp & 1);
@@ -687,29 +386,23 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
             for (int c = 0; c < kChunks; ++c) {
                 const int ab = c & 1;
                 const uint64_t bhi = bdesc(bbase + 1024 * c), blo = bdesc(bbase + 1024 * c + 512);
+                if (c == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
+                mbar_wait_sleep(&afull[w][ab], (uint32_t)((c >> 1) & 1));
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
+                    const uint32_t colA = (uint32_t)(w * kWGCols + 32 * RB + ab * 16 * RB);
 #pragma unroll
-                for (int wi = 0; wi < kWPer; ++wi) {
-                    const int w = w0 + wi;
-                    if (c == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
-                    mbar_wait_sleep(&afull[w][ab], (uint32_t)((c >> 1) & 1));
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
-                        const uint32_t colA = (uint32_t)(w * kWGCols + 32 * RB + ab * 16 * RB);
-#ifndef LSG_TC2_NOMMA   // diagnostic builds only (tools/build_diag.sh)
-#pragma unroll
-                        for (int rb = 0; rb < RB; ++rb) {
-                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, (c == 0 && first) ? 0u : 1u);
-                            mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
-                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
-                        }
-#endif
-                        mma_commit(&aempty[w][ab]);
-                        if (c == kChunks - 1 && last) mma_commit(&dfull[w][db]);
-                        if (c == kChunks - 1 && wi == kWPer - 1) mma_commit(&empty_bar[s]);   // stage s read
+                    for (int rb = 0; rb < RB; ++rb) {
+                        mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, (c == 0 && first) ? 0u : 1u);
+                        mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
+                        mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
                     }
-                    __syncwarp();
+                    mma_commit(&aempty[w][ab]);
+                    if (c == kChunks - 1 && last) mma_commit(&dfull[w][db]);
+                    if (c == kChunks - 1) mma_commit(&empty_bar[s]);   // stage s's B operand read
                 }
+                __syncwarp();
             }
             if (last) {
                 tig = 0;
@@ -722,13 +415,16 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         return;
     }
 
+    }   // warpgroup 3
+    if (LSG_MAXNREG > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(LSG_MAXNREG));
+
     // ---------------- consumers: warpgroup wg, TMEM lane quadrant q ----------------
     const int wg = warp >> 2, q = warp & 3;
     const int tw = q * 32 + lane;
     const int tid = threadIdx.x;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(wg * kWGCols);
-    const float k2 = st->k2;
-    const float2 nk2 = bc(-k2);
+    const float2 nk2 = bc(-st->k2);
+    const float gate = sc.gate_g * (float)sqrt(st->sigma2);
     double Rm[9], tv[3];
 #pragma unroll
     for (int i = 0; i < 9; ++i) Rm[i] = st->R[i];
@@ -736,7 +432,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
     for (int i = 0; i < 3; ++i) tv[i] = st->t[i];
     constexpr int kRC = kNCW * 32 * RB;
 
-    float2 h[RB][3], l[RB][3];   // x̂ as FP32 hi/lo, broadcast to both f32x2 lanes (two targets per instruction)
+    float h[RB][3], l[RB][3];   // x̂ as FP32 hi/lo (computed in FP64)
     float Rt[RB], Ct[RB];
     int nfold = 0;
 
@@ -755,13 +451,12 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
                                  fma(Rm[6], x0, fma(Rm[7], x1, fma(Rm[8], x2, tv[2])))};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const float hi = __double2float_rn(X[a]);
-                h[k][a] = bc(hi);
-                l[k][a] = bc(__double2float_rn(X[a] - (double)hi));
+                h[k][a] = __double2float_rn(X[a]);
+                l[k][a] = __double2float_rn(X[a] - (double)h[k][a]);
             }
             Rt[k] = Ct[k] = 0.f;
 #pragma unroll
-            for (int f = 0; f < Cfg::kSmF; ++f) smS[f * kRC + k * (kNCW * 32) + tid] = 0.f;
+            for (int f = 0; f < kTcSmF; ++f) smS[f * kRC + k * (kNCW * 32) + tid] = 0.f;
         }
         nfold = 0;
     };
@@ -783,9 +478,8 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         }
         nfold = 0;
     };
-    // drain D group `gd` (all its MMAs are complete once dfull fires), release D (and, self-issuing, the
-    // stage of its single tile `itd`)
-    auto drain = [&](int64_t gd, int64_t itd) {
+    // drain D group `gd` (all its MMAs are complete once dfull fires) and release D
+    auto drain = [&](int64_t gd) {
         const int db = (int)(gd & 1);
         mbar_wait_sleep(&dfull[wg][db], (uint32_t)((gd >> 1) & 1));
         tc_fence_after();
@@ -795,17 +489,14 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-            if (!kSelf) mbar_arrive(&dfree[wg][db]);   // self-issue: the next chunk-0 barrier orders it
-            if (kSelf) mbar_arrive(&empty_bar[itd & 3]);
-        }
+        if (lane == 0) mbar_arrive(&dfree[wg][db]);
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) {
             const int rc = rb * (kNCW * 32) + tid;
 #pragma unroll
             for (int f = 0; f < kNF; ++f) smS[f * kRC + rc] += __uint_as_float(d[rb][f]);
         }
-        if (++nfold == kTc2Fold) fold_s1();
+        if (++nfold == kTcFold) fold_s1();
     };
     auto flush = [&](int64_t j) {
         fold_s1();
@@ -823,127 +514,53 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
             base[15 * kBlk + b] = 0.f;
         }
     };
-
-    uint32_t cur_b = 0, cur_db = 0;   // self-issue: B operand base of the current stage, D buffer
-    // one K step (8 targets = 4 target pairs) for buffer AB: residual, τ, ex2, Σpτ, TF32 split → TMEM A
-    auto chunk = [&](const float4* core, int c, float2 (&Lt)[RB], auto ABc) {
+    // one K step for A buffer AB: the pair math (tc_chunk_pairs), then the A rows into TMEM
+    auto chunk = [&](const float4* core, int c, const float2 (&xa)[RB][3], const float2 (&xb)[RB][3],
+                     float2 (&Lt)[RB], auto ABc, auto cheapc) {
         constexpr int AB = decltype(ABc)::value;
-        // wait for the MMAs of this buffer's previous use (K step c - 2): parity of completion 4·it + c/2 - 1
-        const uint32_t apar = (uint32_t)(((c >> 1) & 1) ^ 1);
-        if (!kStX8) {
-            mbar_wait_sleep(&aempty[wg][AB], apar);
-            tc_fence_after();
-        }
-        uint32_t av[RB][16];   // A row of this K step: TF32 hi of the 8 targets, then lo
+        uint32_t av[RB][16];
+        tc_chunk_pairs<kLiteral, decltype(cheapc)::value, RB>(core, c, xa, xb, nk2, Lt, av);
+        // the A buffer is needed only now: the MMAs of its previous use (K step c - 2) had this chunk's math
+        // to finish (parity of completion 4·it + c/2 - 1)
+        mbar_wait_sleep(&aempty[wg][AB], (uint32_t)(((c >> 1) & 1) ^ 1));
+        tc_fence_after();
 #pragma unroll
-        for (int pp = 0; pp < 4; ++pp) {
-            const int pr = c * 4 + pp;
-            const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
-#pragma unroll
-            for (int rb = 0; rb < RB; ++rb) {
-                const float2 rx = __fadd2_rn(__fadd2_rn(h[rb][0], make_float2(-v0.x, -v0.y)), l[rb][0]);
-                const float2 ry = __fadd2_rn(__fadd2_rn(h[rb][1], make_float2(-v0.z, -v0.w)), l[rb][1]);
-                const float2 rz = __fadd2_rn(__fadd2_rn(h[rb][2], make_float2(-v1.x, -v1.y)), l[rb][2]);
-                const float2 qv = __ffma2_rn(make_float2(v3.x, v3.y), rz,
-                                             __ffma2_rn(make_float2(v2.z, v2.w), ry, __fmul2_rn(make_float2(v2.x, v2.y), rx)));
-                const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
-                const float2 e = kLiteral ? __fmul2_rn(nk2, tau) : __ffma2_rn(nk2, tau, make_float2(v1.z, v1.w));
-                const float2 p = make_float2(ex2_approx(e.x), ex2_approx(e.y));
-                Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
-                const float2 hi = make_float2(__uint_as_float(__float_as_uint(p.x) & 0xFFFFE000u),
-                                              __uint_as_float(__float_as_uint(p.y) & 0xFFFFE000u));
-                const float2 lo = __fadd2_rn(p, make_float2(-hi.x, -hi.y));
-                if (kStX8) {
-                    av[rb][2 * pp] = __float_as_uint(hi.x);
-                    av[rb][2 * pp + 1] = __float_as_uint(hi.y);
-                    av[rb][8 + 2 * pp] = __float_as_uint(lo.x);
-                    av[rb][8 + 2 * pp + 1] = __float_as_uint(lo.y);
-                } else {
-                    tmem_st2(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16 + 2 * pp), hi);
-                    tmem_st2(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16 + 8 + 2 * pp), lo);
-                }
-            }
-        }
-        if (kStX8) {
-            // the A buffer is needed only now: the MMAs of its previous use had this chunk's math to finish
-            mbar_wait_sleep(&aempty[wg][AB], apar);
-            tc_fence_after();
-#ifndef LSG_TC2_NOSTTM
-#pragma unroll
-            for (int rb = 0; rb < RB; ++rb) tmem_st16(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16), av[rb]);
-#else
-            float sink = 0.f;
-#pragma unroll
-            for (int rb = 0; rb < RB; ++rb)
-#pragma unroll
-                for (int k = 0; k < 16; ++k) sink += __uint_as_float(av[rb][k]);
-            Lt[0].x += sink * 1e-30f;
-#endif
-        }
+        for (int rb = 0; rb < RB; ++rb) tmem_st16(tl + (uint32_t)(32 * RB + AB * 16 * RB + rb * 16), av[rb]);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (!kSelf) {
-            if (lane == 0) mbar_arrive(&afull[wg][AB]);
-        } else {
-            // the warpgroup's four warps meet at a named barrier (two ids, alternating with the A buffer, so
-            // a warp one K step ahead cannot complete the wrong phase); warp 0 then issues the MMAs
-            const int bid = 2 + 2 * wg + AB;
-            if (q != 0) {
-                named_bar_arrive(bid, 128);
-            } else {
-                named_bar_sync(bid, 128);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint64_t bhi = bdesc(cur_b + 1024 * c), blo = bdesc(cur_b + 1024 * c + 512);
-                    const uint32_t colD = (uint32_t)(wg * kWGCols) + cur_db * 16 * RB;
-                    constexpr uint32_t kColA = 32 * RB + AB * 16 * RB;
-#pragma unroll
-                    for (int rb = 0; rb < RB; ++rb) {
-                        mma_tf32_ts(colD + rb * 16, (uint32_t)(wg * kWGCols) + kColA + rb * 16, bhi, kTcIdesc16,
-                                    c == 0 ? 0u : 1u);
-                        mma_tf32_ts(colD + rb * 16, (uint32_t)(wg * kWGCols) + kColA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
-                        mma_tf32_ts(colD + rb * 16, (uint32_t)(wg * kWGCols) + kColA + rb * 16, blo, kTcIdesc16, 1u);
-                    }
-                    mma_commit(&aempty[wg][AB]);
-                    if (c == kChunks - 1) mma_commit(&dfull[wg][cur_db]);
-                }
-                __syncwarp();
-            }
-        }
+        if (lane == 0) mbar_arrive(&afull[wg][AB]);
     };
 
     int64_t j = u0 / sc.T, tile = u0 % sc.T;
     load_points(j);
     bool pending = false;   // the previous D group has not been drained yet
-    int64_t grp = 0, pend_g = 0, pend_it = 0;
+    int64_t grp = 0, pend_g = 0;
     int tig = 0;
     for (int64_t it = 0; it < nunits; ++it) {
         mbar_wait_sleep(&full_bar[it & 3], (uint32_t)((it >> 2) & 1));
-        cur_b = smem_u32(&tiles_st[0][0]) + kTcBOff + (uint32_t)(it & 3) * kTcTileBytes;
-        cur_db = (uint32_t)(grp & 1);
         const float4* core = reinterpret_cast<const float4*>(&tiles_st[it & 3][0]);
         float2 Lt[RB];
 #pragma unroll
         for (int k = 0; k < RB; ++k) Lt[k] = make_float2(0.f, 0.f);
-#ifndef LSG_TC2_UNROLL
-#define LSG_TC2_UNROLL 1
-#endif
-#define LSG_PRAGMA(x) _Pragma(#x)
-#define LSG_UNROLL(n) LSG_PRAGMA(unroll n)
-        LSG_UNROLL(LSG_TC2_UNROLL)
-        for (int c = 0; c < kChunks; c += 2) {
-            chunk(core, c, Lt, std::integral_constant<int, 0>());
-            chunk(core, c + 1, Lt, std::integral_constant<int, 1>());
-            if (c == 0 && pending) {
-                drain(pend_g, pend_it);
-                pending = false;
+        const TileMeta tm = tile_meta(core);
+        auto run_tile = [&](auto cheapc) {
+            float2 xa[RB][3], xb[RB][3];
+            tile_points<decltype(cheapc)::value, RB>(h, l, tm, xa, xb);
+            LSG_UNROLL(LSG_TC_UNROLL)
+            for (int c = 0; c < kChunks; c += 2) {
+                chunk(core, c, xa, xb, Lt, std::integral_constant<int, 0>(), cheapc);
+                chunk(core, c + 1, xa, xb, Lt, std::integral_constant<int, 1>(), cheapc);
+                if (c == 0 && pending && tig >= kDrainLag) {
+                    drain(pend_g);
+                    pending = false;
+                }
             }
-        }
-        if (!kSelf) {   // this warp is done reading the stage's core data
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[it & 3]);
-        }
+        };
+        if (tile_cheap(tm, gate)) run_tile(std::true_type());
+        else run_tile(std::false_type());
+        __syncwarp();   // this warp is done reading the stage's core data
+        if (lane == 0) mbar_arrive(&empty_bar[it & 3]);
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) {
             const float L = Lt[rb].x + Lt[rb].y;
@@ -956,12 +573,15 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
         const bool last = tig + 1 == NT || block_end;
         if (last) {
             if (block_end) {   // source block (or the CTA's range) ends here: drain and flush now
-                drain(grp, it);
+                if (pending) {
+                    drain(pend_g);
+                    pending = false;
+                }
+                drain(grp);
                 flush(j);
             } else {
                 pending = true;
                 pend_g = grp;
-                pend_it = it;
             }
             tig = 0;
             ++grp;
@@ -974,7 +594,7 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
             if (it + 1 < nunits) load_points(j);
         }
     }
-    // all MMAs of this warpgroup completed (dfull of the last tile was awaited); release TMEM
+    // all MMAs of this warpgroup completed (dfull of the last group was awaited); release TMEM
     tc_fence_before();
     named_bar_sync(1, kNCW * 32);
     if (warp == 0) {
@@ -994,7 +614,13 @@ __global__ void __launch_bounds__(Tc2Cfg<NWG, RB, kSelf, MW>::kThreads, 1)
 __global__ void __launch_bounds__(kMergePts * 16)
     estep_merge_kernel(const float* __restrict__ part, int64_t N, const IterState* __restrict__ st, Sched sc,
                        float* __restrict__ rec, const float* __restrict__ phi) {
-    if (!st->active) return;
+    if (!st->active) {
+        if (st->status == LSGCPD_EINVAL) {   // the target did not match (estep_setup_kernel): all-NaN record
+            const int64_t i = (int64_t)blockIdx.x * kMergePts * LSGCPD_REC + threadIdx.x;
+            if (i < N * LSGCPD_REC) rec[i] = __int_as_float(0x7fc00000);
+        }
+        return;
+    }
     __shared__ float tile[kMergePts][LSGCPD_REC + 1];
     __shared__ double a0s[kMergePts];
     const int64_t n0 = (int64_t)blockIdx.x * kMergePts;
@@ -1004,143 +630,105 @@ __global__ void __launch_bounds__(kMergePts * 16)
     if (n0 + p < N) rec[(n0 + p) * LSGCPD_REC + g] = tile[p][g];
 }
 
+
 // ---- host-side planning and launch ---------------------------------------------------------
-// Kernel variants (points per thread, consumer warps, min CTAs/SM, packed).  LSGCPD_ESTEP_VARIANT
-// selects one (tuning/benchmarking); the default is the fastest measured on B200.
+// CUDA-core kernel configurations (points per thread, consumer warps, min CTAs/SM, packed):
+//   0  768-point blocks (12 consumer warps): the running-max mode of large problems, and LSGCPD_TC=0
+//   1  512-point blocks (8 warps): problems too small to fill the GPU with 768-point tensor-core blocks
+//   2  64-point blocks (1 warp, 8 CTAs/SM): the smallest problems (most CTAs per problem)
+// tools/small_path_sweep.py picked the small-problem rule.
 struct Variant {
     int ppt, ncw, minb, packed;
     const void* fn[2];  // [literal]
 };
 #define LSG_VARIANT(P, W, B, X) \
     {P, W, B, X, {(const void*)estep_kernel<P, W, B, X, false>, (const void*)estep_kernel<P, W, B, X, true>}}
-static const Variant kVariants[] = {
-    LSG_VARIANT(2, 16, 1, true), LSG_VARIANT(2, 8, 2, true), LSG_VARIANT(4, 8, 1, true), LSG_VARIANT(2, 12, 1, true),
-    LSG_VARIANT(4, 4, 2, true),  LSG_VARIANT(2, 8, 2, false), LSG_VARIANT(1, 16, 1, false), LSG_VARIANT(2, 16, 1, true),
-    LSG_VARIANT(2, 14, 1, true), LSG_VARIANT(2, 8, 1, true), LSG_VARIANT(2, 2, 8, true), LSG_VARIANT(1, 2, 8, false),
-    LSG_VARIANT(2, 1, 8, true),
-};
+static const Variant kVariants[] = {LSG_VARIANT(2, 12, 1, true), LSG_VARIANT(2, 8, 1, true), LSG_VARIANT(2, 1, 8, true)};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
-constexpr int kDefaultVariant = 3;   // packed, 2 points/thread, 12 consumer warps (tools/estep_speed.py)
+constexpr int kBigVariant = 0, kMidVariant = 1, kSmallVariant = 2;
+constexpr int kMidBlk = 2 * 8 * 32;
+static_assert(2 * 12 * 32 == kTcBlk || LSG_TC_NWG != 3, "the running-max partner of the tensor-core kernel uses its block size");
+constexpr int64_t kSplitBytes = 48ll << 20;   // tensor-core sections above this are swept in two halves
 
-static int variant_index() {
-    const char* e = getenv("LSGCPD_ESTEP_VARIANT");
-    int v = e ? atoi(e) : kDefaultVariant;
-    return (v >= 0 && v < kNumVariants) ? v : kDefaultVariant;
-}
-// Tensor-core E step (fixed-max mode) paired with a CUDA-core variant of the same block size for the
-// running-max mode.  LSGCPD_TC=0 disables it; LSGCPD_TC_VARIANT picks the configuration.
-struct TcVariant {
-    int nwg, rb, mw, pair_variant;
-    int threads, blk;
-    size_t smem;
-    const void* fn[2];
+// Per-device facts (SM count, occupancies) and one-time function attributes, set up once per device under a
+// lock (a thread may move between devices; function attributes are per device).
+struct DevInfo {
+    bool ready = false;
+    int nsm = 0;
+    int occ[kNumVariants] = {};
 };
-#define LSG_TC(NWG, RB, MW, PV)                                                                           \
-    {NWG, RB, MW, PV, TcCfg<NWG, RB, MW>::kThreads, TcCfg<NWG, RB, MW>::kBlk, TcCfg<NWG, RB, MW>::kSmem, \
-     {(const void*)estep_tc_kernel<NWG, RB, MW, false>, (const void*)estep_tc_kernel<NWG, RB, MW, true>}}
-#define LSG_TC2N(NWG, RB, X8, SELF, MW, NT, PV)                                                      \
-    {NWG, RB, MW, PV, Tc2Cfg<NWG, RB, SELF, MW>::kThreads, Tc2Cfg<NWG, RB, SELF, MW>::kBlk,          \
-     Tc2Cfg<NWG, RB, SELF, MW>::kSmem,                                                               \
-     {(const void*)estep_tc2_kernel<NWG, RB, false, X8, SELF, MW, NT>,                               \
-      (const void*)estep_tc2_kernel<NWG, RB, true, X8, SELF, MW, NT>}}
-#define LSG_TC2M(NWG, RB, X8, SELF, MW, PV) LSG_TC2N(NWG, RB, X8, SELF, MW, 1, PV)
-#define LSG_TC2(NWG, RB, X8, SELF, PV) LSG_TC2M(NWG, RB, X8, SELF, 1, PV)
-static const TcVariant kTcVariants[] = {
-    LSG_TC(4, 2, 2, 0),   // 16 consumer warps, 2 points/thread (1024-point blocks) — CUDA-core variant 0
-    LSG_TC(6, 1, 2, 3),   // 24 consumer warps, 1 point/thread (768) — variant 3
-    LSG_TC(7, 1, 1, 8),   // 28 consumer warps (896) — variant 8
-    LSG_TC(4, 1, 2, 9),   // 16 consumer warps, 1 point/thread (512) — variant 9
-    LSG_TC(4, 2, 4, 0),   // as 0 with one MMA warp per warpgroup
-    LSG_TC(4, 2, 1, 0),   // as 0 with a single MMA warp
-    LSG_TC(2, 4, 1, 0),   // 8 consumer warps, 4 points/thread (1024)
-    LSG_TC(3, 2, 1, 3),   // 12 consumer warps, 2 points/thread (768)
-    // second generation (estep_tc2_kernel): one MMA warp, double-buffered D
-    LSG_TC2(3, 2, false, false, 3),   // 8: 12 consumer warps × 2 points (768), per-pair TMEM stores
-    LSG_TC2(3, 2, true, false, 3),    // 9: as 8 with two x8 TMEM stores per row block and K step
-    LSG_TC2(4, 2, true, false, 0),    // 10: 16 consumer warps × 2 points (1024)
-    LSG_TC2(2, 4, true, false, 0),    // 11: 8 consumer warps × 4 points (1024)
-    LSG_TC2(6, 1, true, false, 3),    // 12: 24 consumer warps × 1 point (768)
-    LSG_TC2(6, 1, false, false, 3),   // 13: as 12 with per-pair TMEM stores
-    LSG_TC2(2, 2, true, false, 9),    // 14: 8 consumer warps × 2 points (512)
-    // each warpgroup issues its own MMAs (no MMA warp)
-    LSG_TC2(3, 2, true, true, 3),     // 15: as 9
-    LSG_TC2(4, 2, true, true, 0),     // 16: as 10
-    LSG_TC2(2, 4, true, true, 0),     // 17: as 11
-    LSG_TC2(6, 1, true, true, 3),     // 18: as 12
-    // one MMA warp per warpgroup
-    LSG_TC2M(3, 2, true, false, 3, 3),   // 19: as 9
-    LSG_TC2M(6, 1, true, false, 3, 3),   // 20: as 12, one MMA warp per two warpgroups
-    LSG_TC2M(2, 2, true, false, 2, 9),   // 21: as 14
-    // D accumulated over NT tiles before each drain
-    LSG_TC2N(3, 2, true, false, 3, 2, 3),   // 22: as 19, NT = 2
-    LSG_TC2N(3, 2, true, false, 3, 4, 3),   // 23: as 19, NT = 4
-    LSG_TC2N(3, 2, true, false, 3, 8, 3),   // 24: as 19, NT = 8
-    LSG_TC2N(3, 2, true, false, 3, 16, 3),  // 25: as 19, NT = 16
-};
-constexpr int kNumTcVariants = sizeof(kTcVariants) / sizeof(kTcVariants[0]);
-// LSGCPD_TC: unset = automatic (tensor cores unless the problem is too small), 0 = off, 1 = forced on
-static int tc_mode() {
-    const char* e = getenv("LSGCPD_TC");
-    return e ? (atoi(e) != 0 ? 1 : 0) : 2;
-}
-constexpr int kDefaultTcVariant = 23;  // tc2, 12 consumer warps × 2 points, one MMA warp per warpgroup, D over 4 tiles (tools/tc_speed.py)
-static int tc_variant_index() {
-    const char* e = getenv("LSGCPD_TC_VARIANT");
-    int v = e ? atoi(e) : kDefaultTcVariant;
-    return (v >= 0 && v < kNumTcVariants) ? v : kDefaultTcVariant;
+static std::mutex g_dev_mu;
+static DevInfo g_dev[64];
+
+static int device_info(const DevInfo** out) {
+    int dev;
+    LSG_CUDA(cudaGetDevice(&dev));
+    LSG_CHECK(dev >= 0 && dev < 64, LSGCPD_ECUDA, "device ordinal %d out of range", dev);
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DevInfo& d = g_dev[dev];
+    if (!d.ready) {
+        LSG_CUDA(cudaDeviceGetAttribute(&d.nsm, cudaDevAttrMultiProcessorCount, dev));
+        for (int v = 0; v < kNumVariants; ++v) {
+            int occ = 0;
+            LSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kVariants[v].fn[0],
+                                                                   (kVariants[v].ncw + 1) * 32, 0));
+            d.occ[v] = occ > 0 ? occ : 1;
+        }
+        LSG_CUDA(cudaFuncSetAttribute((const void*)estep_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kTcSmem));
+        LSG_CUDA(cudaFuncSetAttribute((const void*)estep_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kTcSmem));
+        d.ready = true;
+    }
+    *out = &d;
+    return 0;
 }
 
-static int g_num_sms = 0;
-static int g_occ[kNumVariants] = {0};
-
-constexpr int kMidVariant = 9, kMidBlk = 2 * 8 * 32;   // packed, 2 points/thread, 8 consumer warps: 512-point blocks
-constexpr int kSmallVariant = 12;
-constexpr int64_t kSplitBytes = 48ll << 20;   // tensor-core sections above this are swept in two halves   // one consumer warp, 64-point blocks: problems too small to fill the GPU
+int sm_count() {
+    const DevInfo* d = nullptr;
+    return device_info(&d) ? 0 : d->nsm;
+}
 
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
-    const int tvi = tc_variant_index();
-    const int mode = tc_mode();
+    const Options& op = options();
+    const int mode = op.tc.load();   // 0 off, 1 forced, 2 automatic
+    const int forced = op.estep_variant.load();
+    const DevInfo* di = nullptr;
+    const int rc = device_info(&di);
+    if (rc) return rc;
     bool tc = mode != 0;
-    int vi = tc ? kTcVariants[tvi].pair_variant : variant_index();
-    if (g_num_sms == 0) {
-        int dev;
-        LSG_CUDA(cudaGetDevice(&dev));
-        LSG_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    if (mode == 2 && !getenv("LSGCPD_ESTEP_VARIANT")) {
+    int vi = (forced >= 0 && forced < kNumVariants) ? forced : kBigVariant;
+    if (tc) vi = kBigVariant;
+    if (mode == 2 && forced < 0) {
         // small problems (tiny / object configs): too few (block, tile) units for one CTA per SM with the
         // big blocks — use the small-block CUDA-core kernel so every SM gets work
-        const int64_t units_big = (N + kTcVariants[tvi].blk - 1) / kTcVariants[tvi].blk * (M_pad / kTT);
-        if (units_big < 2 * (int64_t)g_num_sms) {
+        const int64_t units_big = (N + kTcBlk - 1) / kTcBlk * (M_pad / kTT);
+        if (units_big < 2 * (int64_t)di->nsm) {
             // 512-point blocks once they give ~3/4 of a unit per SM, else 64-point blocks (the most CTAs):
             // tools/small_path_sweep.py — 1,000 points 38 µs per EM iteration with 64-point blocks, 2,000 / 3,500
             // points 44 / 56 µs with 512-point blocks (64-point: 51 / 72; tensor cores: 50 / 59)
             tc = false;
             const int64_t units_mid = (N + kMidBlk - 1) / kMidBlk * (M_pad / kTT);
-            vi = 4 * units_mid >= 3 * (int64_t)g_num_sms ? kMidVariant : kSmallVariant;
+            vi = 4 * units_mid >= 3 * (int64_t)di->nsm ? kMidVariant : kSmallVariant;
         }
     }
     const Variant& V = kVariants[vi];
-    if (g_occ[vi] == 0) {
-        int occ = 0;
-        LSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, V.fn[0], (V.ncw + 1) * 32, 0));
-        g_occ[vi] = occ > 0 ? occ : 1;
-    }
     Sched s;
     memset(&s, 0, sizeof(s));
     s.variant = tc ? -1 - vi : vi;   // negative: tensor-core kernel + CUDA-core variant for running max
-    s.tc_variant = tvi;
+    s.tc_variant = 0;
     s.B = (int64_t)V.ppt * V.ncw * 32;
     s.nblk = (N + s.B - 1) / s.B;
     // a tensor-core section larger than ~48 MB is swept in two halves, one launch each, so every CTA reads
     // tiles of the same half at a time and the half stays in L2 (the whole section re-read from HBM otherwise;
     // DESIGN §7 "DRAM traffic").  M_pad is a multiple of 256 targets, so the tile count is even.
-    const char* he = getenv("LSGCPD_HALVES");
-    const bool split = tc && (M_pad / kTT) * (int64_t)kTcTileBytes > kSplitBytes && !(he && he[0] == '1');
+    const int hv = op.halves.load();
+    const bool split = tc && (M_pad / kTT) * (int64_t)kTcTileBytes > kSplitBytes && hv != 1;
     s.halves = split ? 2 : 1;
+    s.gate_g = op.tile_gate.load();
     s.T = M_pad / kTT / s.halves;
     s.U = s.nblk * s.T;
-    const int64_t slots = (int64_t)g_num_sms * (tc ? 1 : g_occ[vi]);   // the TC kernel holds all TMEM: 1 CTA/SM
+    const int64_t slots = (int64_t)di->nsm * (tc ? 1 : di->occ[vi]);   // the TC kernel holds all TMEM: 1 CTA/SM
     s.G = s.U < slots ? s.U : slots;
     if (s.G < 1) s.G = 1;
     int64_t kmax = 1;
@@ -1163,8 +751,8 @@ void estep_launch_setup(IterState* st, const void* d_target, const double* R, co
                                              consistent, eta);
 }
 
-void estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
-                  float* part, float* rec, int consistent, const float* phi, cudaStream_t stream, int merge) {
+int estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
+                 float* part, float* rec, int consistent, const float* phi, cudaStream_t stream, int merge) {
     const bool tc = sc.variant < 0;
     const Variant& V = kVariants[tc ? -1 - sc.variant : sc.variant];
     Sched scv = sc;
@@ -1173,27 +761,44 @@ void estep_launch(const void* d_target, const float* d_src, int64_t N, const Ite
     for (int h = 0; h < sc.halves; ++h) {   // one sweep per half of the targets (sc.T tiles each)
         const float* body = target_body(d_target) + (int64_t)h * sc.T * kTT * kTgtFloats;
         float* parth = part + (int64_t)h * sc.hstride;
-        void* args[] = {(void*)&body, (void*)&d_src, (void*)&N, (void*)&st, (void*)&scv, (void*)&parth,
-                        (void*)&skip_fixed};
         if (tc) {
             const char* tcb = reinterpret_cast<const char*>(target_tc(d_target, M_pad)) +
                               (int64_t)h * sc.T * kTcTileBytes;
-            const TcVariant& TV = kTcVariants[sc.tc_variant];
-            static bool attr_set[kNumTcVariants] = {};
-            if (!attr_set[sc.tc_variant]) {
-                cudaFuncSetAttribute(TV.fn[0], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TV.smem);
-                cudaFuncSetAttribute(TV.fn[1], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TV.smem);
-                attr_set[sc.tc_variant] = true;
-            }
             void* targs[] = {(void*)&tcb, (void*)&d_src, (void*)&N, (void*)&st, (void*)&scv, (void*)&parth};
-            cudaLaunchKernel(TV.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3(TV.threads), targs, TV.smem,
-                             stream);
+            const void* fn = consistent ? (const void*)estep_tc_kernel<false> : (const void*)estep_tc_kernel<true>;
+            LSG_CUDA(cudaLaunchKernel(fn, dim3((unsigned)sc.G), dim3(kTcThreads), targs, kTcSmem, stream));
         }
-        cudaLaunchKernel(V.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3((V.ncw + 1) * 32), args, 0, stream);
+        void* args[] = {(void*)&body, (void*)&d_src, (void*)&N, (void*)&st, (void*)&scv, (void*)&parth,
+                        (void*)&skip_fixed};
+        LSG_CUDA(cudaLaunchKernel(V.fn[consistent ? 0 : 1], dim3((unsigned)sc.G), dim3((V.ncw + 1) * 32), args, 0,
+                                  stream));
     }
-    if (!merge) return;
+    if (!merge) return 0;
     estep_merge_kernel<<<(unsigned)((N + kMergePts - 1) / kMergePts), kMergePts * 16, 0, stream>>>(part, N, st, sc,
                                                                                                  rec, phi);
+    LSG_CUDA(cudaGetLastError());
+    return 0;
+}
+
+// ---- options (read once from the environment; lsgcpd_set_option changes them at run time) ----------------
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e && *e ? atoi(e) : dflt;
+}
+Options::Options() {
+    const char* t = getenv("LSGCPD_TC");
+    tc.store(t && *t ? (atoi(t) != 0 ? 1 : 0) : 2);
+    estep_variant.store(env_int("LSGCPD_ESTEP_VARIANT", -1));
+    halves.store(env_int("LSGCPD_HALVES", 0));
+    no_fuse.store(env_int("LSGCPD_NO_FUSE", 0));
+    graph_cache.store(env_int("LSGCPD_GRAPH_CACHE", 1));
+    no_graph.store(env_int("LSGCPD_NO_GRAPH", 0));
+    const char* g = getenv("LSGCPD_TILE_GATE");
+    tile_gate.store(g && *g ? (float)atof(g) : kDefaultTileGate);
+}
+Options& options() {
+    static Options o;   // thread-safe one-time initialisation (C++11 magic static)
+    return o;
 }
 
 }  // namespace lsg

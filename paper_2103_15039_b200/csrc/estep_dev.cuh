@@ -160,6 +160,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 constexpr int kTcStages = 4;
 constexpr int kTcCols = 512;                  // TMEM columns allocated (the whole TMEM: base column 0)
 constexpr int kTcChunk = 8;                   // targets per A buffer (one K step)
+// D group g is drained at the start of tile kDrainLag of group g + 1 (its MMAs long complete, and the slowest
+// warp of the warpgroup is no longer on the critical path); group g + 2 reuses its D buffer only after that
+#ifndef LSG_DRAIN_LAG
+#define LSG_DRAIN_LAG 1
+#endif
+constexpr int kDrainLag = LSG_DRAIN_LAG;
 // instruction descriptors: D F32, A/B TF32, K-major A and B, M = 128, N = 32 ([hi | lo] features) or 16
 constexpr uint32_t kTcIdesc32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
 constexpr uint32_t kTcIdesc16 = (1u << 4) | (2u << 7) | (2u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
@@ -242,6 +248,78 @@ __device__ __forceinline__ uint64_t bdesc(uint32_t saddr) {
            ((uint64_t)1 << 46);
 }
 
+
+// ---- tensor-core consumers: per-tile residual setup and the pair math of one K step ------------------
+// Tile-centred residual.  The core holds y' = y - c exactly (c: the tile centre, per axis).
+//  * cheap tiles (E_tile ≤ gate): x' = fl((hi - c) + lo) once per (point, tile); r = x' - y' costs 3 FP32
+//    lane-ops per pair.  Its rounding error is ≈ ε(|x'| + |r|) ≤ ε(R_tile + 2|r|), i.e. the hi/lo error plus
+//    a term in R_tile that the gate bounds relative to σ.
+//  * other tiles: (xh, xl) = TwoSum(hi, -c) + lo, r = (xh - y') + xl — the hi/lo residual of round 1, exact
+//    to ≈ ε|r| whatever the tile's size (outlier-laden tiles, large targets far from their centre).
+struct TileMeta {
+    float c[3];
+    float E;
+};
+__device__ __forceinline__ TileMeta tile_meta(const float4* core) {
+    const float4 a = core[3], b = core[7];   // spare fields of targets 0..3 (see common.cuh)
+    return {{a.z, a.w, b.z}, b.w};
+}
+template <bool kCheap, int RB>
+__device__ __forceinline__ void tile_points(const float (&h)[RB][3], const float (&l)[RB][3], const TileMeta& tm,
+                                            float2 (&xa)[RB][3], float2 (&xb)[RB][3]) {
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            if (kCheap) {
+                xa[rb][a] = bc(__fadd_rn(__fsub_rn(h[rb][a], tm.c[a]), l[rb][a]));
+            } else {
+                const float hi = h[rb][a], nc = -tm.c[a];
+                const float s = __fadd_rn(hi, nc);
+                const float bb = __fsub_rn(s, hi);
+                const float err = __fadd_rn(__fsub_rn(hi, __fsub_rn(s, bb)), __fsub_rn(nc, bb));
+                xa[rb][a] = bc(s);
+                xb[rb][a] = bc(__fadd_rn(l[rb][a], err));
+            }
+        }
+}
+// One K step (8 targets = 4 target pairs): residual, τ, ex2, Σpτ, TF32 split of p → the A row of each row
+// block (hi of the 8 targets, then lo).  Cheap tiles: 13 FP32 lane-ops per pair; other tiles: 16.
+template <bool kLiteral, bool kCheap, int RB>
+__device__ __forceinline__ void tc_chunk_pairs(const float4* __restrict__ core, int c, const float2 (&xa)[RB][3],
+                                               const float2 (&xb)[RB][3], float2 nk2, float2 (&Lt)[RB],
+                                               uint32_t (&av)[RB][16]) {
+#pragma unroll
+    for (int pp = 0; pp < 4; ++pp) {
+        const int pr = c * 4 + pp;
+        const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+            float2 rx = __fadd2_rn(xa[rb][0], make_float2(-v0.x, -v0.y));
+            float2 ry = __fadd2_rn(xa[rb][1], make_float2(-v0.z, -v0.w));
+            float2 rz = __fadd2_rn(xa[rb][2], make_float2(-v1.x, -v1.y));
+            if (!kCheap) {
+                rx = __fadd2_rn(rx, xb[rb][0]);
+                ry = __fadd2_rn(ry, xb[rb][1]);
+                rz = __fadd2_rn(rz, xb[rb][2]);
+            }
+            const float2 qv = __ffma2_rn(make_float2(v3.x, v3.y), rz,
+                                         __ffma2_rn(make_float2(v2.z, v2.w), ry, __fmul2_rn(make_float2(v2.x, v2.y), rx)));
+            const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
+            const float2 e = kLiteral ? __fmul2_rn(nk2, tau) : __ffma2_rn(nk2, tau, make_float2(v1.z, v1.w));
+            const float2 p = make_float2(ex2_approx(e.x), ex2_approx(e.y));
+            Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
+            const uint32_t hx = __float_as_uint(p.x) & 0xFFFFE000u, hy = __float_as_uint(p.y) & 0xFFFFE000u;
+            const float2 lo = __fadd2_rn(p, make_float2(-__uint_as_float(hx), -__uint_as_float(hy)));
+            av[rb][2 * pp] = hx;
+            av[rb][2 * pp + 1] = hy;
+            av[rb][8 + 2 * pp] = __float_as_uint(lo.x);
+            av[rb][8 + 2 * pp + 1] = __float_as_uint(lo.y);
+        }
+    }
+}
+// the tile's residual mode: centred when E_tile ≤ gate (gate = gate_g·σ, uniform over the CTA)
+__device__ __forceinline__ bool tile_cheap(const TileMeta& tm, float gate) { return tm.E <= gate; }
 
 // One point of the split-M merge: the nk partials of its source block start at `blk` (slot stride
 // kPartF·kB floats, field stride kB, point index b), `phi` → φ(x_n) or NULL, record row `r`.

@@ -1,8 +1,27 @@
 // Host-side launchers shared between the translation units of liblsgcpd.so.
 #pragma once
+#include <atomic>
+
 #include "common.cuh"
 
 namespace lsg {
+
+// Run-time knobs (diagnostics and tests; the defaults are the product configuration).  Initialised once from
+// the environment (LSGCPD_TC, LSGCPD_ESTEP_VARIANT, LSGCPD_HALVES, LSGCPD_NO_FUSE, LSGCPD_GRAPH_CACHE,
+// LSGCPD_NO_GRAPH, LSGCPD_TILE_GATE); lsgcpd_set_option changes them.  Atomic: calls on other threads see a
+// consistent value per field.
+constexpr float kDefaultTileGate = 24.f;   // E_tile ≤ gate·σ → tile-centred residual
+struct Options {
+    std::atomic<int> tc;              // 0 CUDA cores only, 1 tensor cores forced, 2 automatic
+    std::atomic<int> estep_variant;   // -1 automatic, else the CUDA-core configuration (estep.cu)
+    std::atomic<int> halves;          // 0 automatic, 1 one sweep over the target
+    std::atomic<int> no_fuse;         // 1: separate merge / moments kernels instead of em_tail_kernel
+    std::atomic<int> graph_cache;     // 0: no cached EM-iteration graphs
+    std::atomic<int> no_graph;        // 1: plain launches instead of a captured EM iteration
+    std::atomic<float> tile_gate;     // gate_g of Sched (≤ 0: hi/lo residual on every tile)
+    Options();
+};
+Options& options();
 
 // Registration parameters passed by value to the device-side EM state machine.
 struct RegParams {
@@ -44,13 +63,14 @@ void init_batch_launch(const BatchProblem* bp, int B, IterState* st, const RegPa
                        double* mom, double* sigma2_trace, cudaStream_t stream);
 
 // estep.cu
+int sm_count();   // SM count of the current device (cached per device); 0 on a CUDA error
 int estep_plan(int64_t M_pad, int64_t N, Sched* sc);
 size_t estep_partial_bytes(const Sched& s);
 void estep_launch_setup(IterState* st, const void* d_target, const double* R, const double* t, double sigma2,
                         double w, double V, int64_t M, int consistent, double eta, cudaStream_t stream);
 // phi: optional per-source-point confidence φ(x_n) (Eq. 8: w_n = 1 - (1 - w0) φ(x_n)), NULL = uniform w0
-void estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
-                  float* part, float* rec, int consistent, const float* phi, cudaStream_t stream, int merge = 1);
+int estep_launch(const void* d_target, const float* d_src, int64_t N, const IterState* st, const Sched& sc,
+                 float* part, float* rec, int consistent, const float* phi, cudaStream_t stream, int merge = 1);
 
 // mstep.cu
 constexpr int kMomentCount = 75;          // G 60, U 12, σ²ΣD, ΣP, Σ ln p

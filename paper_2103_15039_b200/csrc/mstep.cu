@@ -766,12 +766,7 @@ void sigma2_init_launch(IterState* st, const void* d_target, const double* sums,
 void em_tail_launch(const float* part, const float* src, int64_t N, IterState* st, const Sched& sc, const float* phi,
                     double* blockpart, double* mom, unsigned* counter, const RegParams& rp, double* nll_trace,
                     double* sigma2_trace, int* iters_done, int run_newton, cudaStream_t stream) {
-    static int nsm = 0;
-    if (nsm == 0) {
-        int dev;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int nsm = sm_count() > 0 ? sm_count() : 1;   // per device (estep.cu)
     const int64_t ng = (N + kMergePts - 1) / kMergePts;
     const int64_t cap = nsm < kMomentBlocks ? nsm : kMomentBlocks;   // blockpart holds kMomentBlocks rows
     em_tail_kernel<<<(unsigned)(ng < cap ? ng : cap), kTailThreads, 0, stream>>>(

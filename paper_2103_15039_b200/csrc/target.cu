@@ -49,15 +49,33 @@ __global__ void __launch_bounds__(kRedThreads)
     block_reduce_store<12, 6, kRedThreads>(v, blockpart, out, counter);
 }
 
+// The model of target m as packed: y, the unit normal n = n_in/|n_in| and α.  A zero or non-finite normal
+// gives α = 0 (an isotropic component), so the packed W = α n nᵀ, the normaliser ½log2(1+α) and tr(W) (read
+// back by lsgcpd_target_set_prior) all describe the same density.
+__device__ __forceinline__ double model_of(const float* __restrict__ nrm, const float* __restrict__ alpha, int64_t m,
+                                           double n[3]) {
+    const double n0 = nrm[3 * m], n1 = nrm[3 * m + 1], n2 = nrm[3 * m + 2];
+    const double len = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+    if (!(len > 0.0) || !isfinite(len)) {
+        n[0] = n[1] = n[2] = 0.0;
+        return 0.0;
+    }
+    n[0] = n0 / len;
+    n[1] = n1 / len;
+    n[2] = n2 / len;
+    return (double)alpha[m];
+}
+
 // stats2 (after the model is built): [max ω, Σ α, Σ ||y - ȳ||², Σ nn-distance, n_degenerate, Σ √(1+α)]
 __global__ void __launch_bounds__(kRedThreads)
-    model_stats_kernel(const float* __restrict__ xyz, const float* __restrict__ alpha, const float* __restrict__ nnd,
-                       const int* __restrict__ degen, int64_t M, const double* __restrict__ stats1, double* blockpart,
-                       double* out, unsigned* counter) {
+    model_stats_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm, const float* __restrict__ alpha,
+                       const float* __restrict__ nnd, const int* __restrict__ degen, int64_t M,
+                       const double* __restrict__ stats1, double* blockpart, double* out, unsigned* counter) {
     double v[6] = {-INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0};
     const double yb[3] = {stats1[6] / M, stats1[7] / M, stats1[8] / M};
     for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
-        const double a = alpha[m];
+        double n[3];
+        const double a = model_of(nrm, alpha, m, n);
         v[0] = fmax(v[0], 0.5 * log2(1.0 + a));
         v[1] += a;
         v[5] += sqrt(1.0 + a);
@@ -115,13 +133,48 @@ __global__ void header_kernel(TargetHeader* hdr, int64_t M, const double* stats1
     for (size_t i = 0; i < (kHeaderBytes - sizeof(TargetHeader)) / 4; ++i) tail[i] = 0u;
 }
 
-// Packed per-target record (FP64 arithmetic, FP32 storage); padding targets contribute nothing.
-__global__ void pack_body_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm,
-                                 const float* __restrict__ alpha, int64_t M, int64_t M_pad,
-                                 const double* __restrict__ stats2, float* __restrict__ body) {
+// ---- slot order: a Morton (Z-order) curve over the AABB ----------------------------------------------
+// 21 bits per axis of the AABB's enclosing cube; ties (one cell) keep the input order (stable radix sort).
+__device__ __forceinline__ uint64_t morton_spread(uint64_t x) {
+    x &= 0x1fffffull;
+    x = (x | (x << 32)) & 0x1f00000000ffffull;
+    x = (x | (x << 16)) & 0x1f0000ff0000ffull;
+    x = (x | (x << 8)) & 0x100f00f00f00f00full;
+    x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
+    x = (x | (x << 2)) & 0x1249249249249249ull;
+    return x;
+}
+__global__ void morton_keys_kernel(const float* __restrict__ xyz, int64_t M, const double* __restrict__ stats1,
+                                   uint64_t* __restrict__ keys, int* __restrict__ ids) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    const double lo[3] = {-stats1[0], -stats1[1], -stats1[2]};
+    const double side = fmax(fmax(stats1[3] + stats1[0], stats1[4] + stats1[1]), stats1[5] + stats1[2]);
+    const double sc = side > 0.0 ? 2097151.0 / side : 0.0;
+    uint64_t k = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double q = floor(((double)xyz[3 * m + a] - lo[a]) * sc);
+        q = q < 0.0 ? 0.0 : (q > 2097151.0 ? 2097151.0 : q);
+        k |= morton_spread((uint64_t)q) << a;
+    }
+    keys[m] = k;
+    ids[m] = (int)m;
+}
+// slot_of[perm[s]] = s (the inverse permutation, kept in the target for lsgcpd_target_set_prior)
+__global__ void slot_inverse_kernel(const int* __restrict__ perm, int64_t M, int64_t M_pad, int32_t* __restrict__ slot_of) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < M) slot_of[perm[s]] = (int32_t)s;
+    else if (s < M_pad) slot_of[s] = -1;
+}
+
+// Packed per-target record in slot order (FP64 arithmetic, FP32 storage); padding targets contribute nothing.
+__global__ void pack_body_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm,
+                                 const float* __restrict__ alpha, const int* __restrict__ perm, int64_t M,
+                                 int64_t M_pad, const double* __restrict__ stats2, float* __restrict__ body) {
+    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // slot
     if (m >= M_pad) return;
-    // pair-interleaved layout: target m is slot (m & 1) of pair m >> 1; field f at pair*32 + 2f + slot
+    // pair-interleaved layout: slot m is lane (m & 1) of pair m >> 1; field f at pair*32 + 2f + lane
     float* o = body + (m >> 1) * (2 * kTgtFloats) + (m & 1);
     float f[kTgtFloats];
     if (m >= M) {
@@ -130,59 +183,120 @@ __global__ void pack_body_kernel(const float* __restrict__ xyz, const float* __r
         f[3] = -INFINITY;
         for (int i = 4; i < kTgtFloats; ++i) f[i] = 0.f;
     } else {
-        const double y0 = xyz[3 * m], y1 = xyz[3 * m + 1], y2 = xyz[3 * m + 2];
-        const double n0 = nrm[3 * m], n1 = nrm[3 * m + 1], n2 = nrm[3 * m + 2];
-        const double a = alpha[m];
+        const int64_t i = perm[m];
+        double n[3];
+        const double a = model_of(nrm, alpha, i, n);
+        const double y0 = xyz[3 * i], y1 = xyz[3 * i + 1], y2 = xyz[3 * i + 2];
         const double sa = sqrt(a);
-        const double ny = n0 * y0 + n1 * y1 + n2 * y2;
+        const double ny = n[0] * y0 + n[1] * y1 + n[2] * y2;
         f[0] = (float)y0; f[1] = (float)y1; f[2] = (float)y2;
         f[3] = (float)(0.5 * log2(1.0 + a) - stats2[0]);
-        f[4] = (float)(sa * n0); f[5] = (float)(sa * n1); f[6] = (float)(sa * n2);
-        f[7] = (float)(a * n0 * n0); f[8] = (float)(a * n0 * n1); f[9] = (float)(a * n0 * n2);
-        f[10] = (float)(a * n1 * n1); f[11] = (float)(a * n1 * n2); f[12] = (float)(a * n2 * n2);
-        f[13] = (float)(a * ny * n0); f[14] = (float)(a * ny * n1); f[15] = (float)(a * ny * n2);
+        f[4] = (float)(sa * n[0]); f[5] = (float)(sa * n[1]); f[6] = (float)(sa * n[2]);
+        f[7] = (float)(a * n[0] * n[0]); f[8] = (float)(a * n[0] * n[1]); f[9] = (float)(a * n[0] * n[2]);
+        f[10] = (float)(a * n[1] * n[1]); f[11] = (float)(a * n[1] * n[2]); f[12] = (float)(a * n[2] * n[2]);
+        f[13] = (float)(a * ny * n[0]); f[14] = (float)(a * ny * n[1]); f[15] = (float)(a * ny * n[2]);
     }
 #pragma unroll
     for (int i = 0; i < kTgtFloats; ++i) o[2 * i] = f[i];
 }
 
-// Tensor-core section: core fields and the hi/lo TF32 feature blocks (see common.cuh).
+// Tensor-core section: core fields (tile-centred) and the hi/lo TF32 feature blocks (see common.cuh).
 __device__ __forceinline__ float tf32_rna(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
 }
-__global__ void pack_tc_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm,
-                               const float* __restrict__ alpha, int64_t M, int64_t M_pad,
-                               const double* __restrict__ stats2, float* __restrict__ tc) {
-    const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= M_pad) return;
-    const int64_t tile = m / kTcTile;
-    const int jt = (int)(m % kTcTile);
+// y - c is exactly representable in FP32 (FP64 TwoSum: the double difference is exact, then it fits a float)
+__device__ __forceinline__ bool exact_diff_f32(float y, float c) {
+    const double a = y, b = -(double)c;
+    const double s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    const double err = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+    return err == 0.0 && (double)(float)s == s;
+}
+// One CTA of kTcTile threads per tile, one thread per slot.
+__global__ void __launch_bounds__(kTcTile)
+    pack_tc_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm, const float* __restrict__ alpha,
+                   const int* __restrict__ perm, int64_t M, const double* __restrict__ stats2, float* __restrict__ tc) {
+    __shared__ float s_lo[3][kTcTile], s_hi[3][kTcTile];
+    __shared__ int s_bad[3];
+    __shared__ double s_r[kTcTile], s_a[kTcTile];
+    const int64_t tile = blockIdx.x;
+    const int jt = threadIdx.x;
+    const int64_t m = tile * kTcTile + jt;
+    const bool real = m < M;
     char* base = reinterpret_cast<char*>(tc) + tile * kTcTileBytes;
-    // core section, pair-interleaved: targets (2i, 2i+1) share 64 B = {f_2i, f_2i+1} for f = 0..7
     float* core = reinterpret_cast<float*>(base) + (jt >> 1) * 16 + (jt & 1);
+    float y[3] = {0.f, 0.f, 0.f};
+    double n[3] = {0.0, 0.0, 0.0}, a = 0.0;
+    if (real) {
+        const int64_t i = perm[m];
+        a = model_of(nrm, alpha, i, n);
+        for (int k = 0; k < 3; ++k) y[k] = xyz[3 * i + k];
+    }
+    // tile centre c: the FP32 midpoint of the real targets' box, per axis, kept only if every y - c is exact
+    for (int k = 0; k < 3; ++k) {
+        s_lo[k][jt] = real ? y[k] : INFINITY;
+        s_hi[k][jt] = real ? y[k] : -INFINITY;
+    }
+    if (jt < 3) s_bad[jt] = 0;
+    __syncthreads();
+    for (int w = kTcTile / 2; w > 0; w >>= 1) {
+        if (jt < w)
+            for (int k = 0; k < 3; ++k) {
+                s_lo[k][jt] = fminf(s_lo[k][jt], s_lo[k][jt + w]);
+                s_hi[k][jt] = fmaxf(s_hi[k][jt], s_hi[k][jt + w]);
+            }
+        __syncthreads();
+    }
+    float c[3];
+    for (int k = 0; k < 3; ++k) {
+        const float lo = s_lo[k][0], hi = s_hi[k][0];
+        c[k] = (lo <= hi) ? (float)(0.5 * ((double)lo + (double)hi)) : 0.f;
+    }
+    __syncthreads();
+    for (int k = 0; k < 3; ++k)
+        if (real && !exact_diff_f32(y[k], c[k])) atomicOr(&s_bad[k], 1);
+    __syncthreads();
+    for (int k = 0; k < 3; ++k)
+        if (s_bad[k]) c[k] = 0.f;
+    float yc[3];
+    double r2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        yc[k] = real ? y[k] - c[k] : 1e18f;   // exact by construction; padding far away
+        r2 += real ? (double)yc[k] * (double)yc[k] : 0.0;
+    }
+    s_r[jt] = sqrt(r2);
+    s_a[jt] = a;
+    __syncthreads();
+    for (int w = kTcTile / 2; w > 0; w >>= 1) {
+        if (jt < w) {
+            s_r[jt] = fmax(s_r[jt], s_r[jt + w]);
+            s_a[jt] = fmax(s_a[jt], s_a[jt + w]);
+        }
+        __syncthreads();
+    }
+    const float E = (float)(s_r[0] * sqrt(1.0 + s_a[0]));   // rounded; the gate compares it with a margin
     float cf[8];
     float F[16];
     for (int i = 0; i < 16; ++i) F[i] = 0.f;
-    if (m >= M) {
+    if (!real) {
         cf[0] = cf[1] = cf[2] = 1e18f;
         cf[3] = -INFINITY;
-        cf[4] = cf[5] = cf[6] = cf[7] = 0.f;
+        cf[4] = cf[5] = cf[6] = 0.f;
     } else {
-        const double y0 = xyz[3 * m], y1 = xyz[3 * m + 1], y2 = xyz[3 * m + 2];
-        const double n0 = nrm[3 * m], n1 = nrm[3 * m + 1], n2 = nrm[3 * m + 2];
-        const double a = alpha[m];
         const double sa = sqrt(a);
-        const double ny = n0 * y0 + n1 * y1 + n2 * y2;
-        cf[0] = (float)y0; cf[1] = (float)y1; cf[2] = (float)y2;
+        const double y0 = y[0], y1 = y[1], y2 = y[2];
+        const double ny = n[0] * y0 + n[1] * y1 + n[2] * y2;
+        cf[0] = yc[0]; cf[1] = yc[1]; cf[2] = yc[2];
         cf[3] = (float)(0.5 * log2(1.0 + a) - stats2[0]);
-        cf[4] = (float)(sa * n0); cf[5] = (float)(sa * n1); cf[6] = (float)(sa * n2); cf[7] = 0.f;
-        F[0] = 1.f; F[1] = (float)y0; F[2] = (float)y1; F[3] = (float)y2;
-        F[4] = (float)(a * n0 * n0); F[5] = (float)(a * n0 * n1); F[6] = (float)(a * n0 * n2);
-        F[7] = (float)(a * n1 * n1); F[8] = (float)(a * n1 * n2); F[9] = (float)(a * n2 * n2);
-        F[10] = (float)(a * ny * n0); F[11] = (float)(a * ny * n1); F[12] = (float)(a * ny * n2);
+        cf[4] = (float)(sa * n[0]); cf[5] = (float)(sa * n[1]); cf[6] = (float)(sa * n[2]);
+        F[0] = 1.f; F[1] = y[0]; F[2] = y[1]; F[3] = y[2];
+        F[4] = (float)(a * n[0] * n[0]); F[5] = (float)(a * n[0] * n[1]); F[6] = (float)(a * n[0] * n[2]);
+        F[7] = (float)(a * n[1] * n[1]); F[8] = (float)(a * n[1] * n[2]); F[9] = (float)(a * n[2] * n[2]);
+        F[10] = (float)(a * ny * n[0]); F[11] = (float)(a * ny * n[1]); F[12] = (float)(a * ny * n[2]);
     }
+    cf[7] = jt < 3 ? c[jt] : (jt == 3 ? E : 0.f);   // tile meta in the spare field of targets 0..3
     for (int f = 0; f < 8; ++f) core[2 * f] = cf[f];
     const int s = jt / 8, j = jt % 8;
     for (int f = 0; f < 16; ++f) {
@@ -582,6 +696,7 @@ struct PrepLayout {
     size_t skeys_b, sids_b, cstart_b, cend_b;   // the bulk grid (fine cells over the robust box)
     size_t hard;                                // points left to the coarse grid (knn_hard_kernel)
     size_t pts_f, pts_c, pts_b;                 // float4 copies of the points in each grid's cell order
+    size_t mkeys, mkeys_s, mids, mperm, mcub, mcub_bytes;   // the Morton sort of the slot order
 };
 static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int64_t kMaxCells = 1 << 22;
@@ -600,9 +715,22 @@ static size_t cub_sort_bytes(int64_t M) {
     return bytes;
 }
 
+static size_t cub_morton_bytes(int64_t M) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t*)nullptr, (uint64_t*)nullptr, (const int*)nullptr,
+                                    (int*)nullptr, (int)M, 0, 63);
+    return bytes;
+}
+
 static PrepLayout prep_layout(int64_t M, bool with_knn) {
     PrepLayout L;
     size_t o = 0;
+    L.mkeys = o; o += al(sizeof(uint64_t) * M);
+    L.mkeys_s = o; o += al(sizeof(uint64_t) * M);
+    L.mids = o; o += al(sizeof(int) * M);
+    L.mperm = o; o += al(sizeof(int) * M);
+    L.mcub_bytes = cub_morton_bytes(M);
+    L.mcub = o; o += al(L.mcub_bytes);
     L.blockpart = o; o += al(sizeof(double) * kRedBlocks * 16);
     L.stats1 = o; o += al(sizeof(double) * 16);
     L.stats2 = o; o += al(sizeof(double) * 16);
@@ -653,14 +781,24 @@ static int finish_launch(const float* d_xyz, const float* nrm, const float* alph
     double* bp = reinterpret_cast<double*>(ws + L.blockpart);
     double* st2 = reinterpret_cast<double*>(ws + L.stats2);
     unsigned* ctr = reinterpret_cast<unsigned*>(ws + L.counter);
-    model_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_xyz, alpha, nnd, degen, M, st1, bp, st2, ctr);
+    model_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_xyz, nrm, alpha, nnd, degen, M, st1, bp, st2, ctr);
     TargetHeader* hdr = reinterpret_cast<TargetHeader*>(d_target);
     header_kernel<<<1, 1, 0, stream>>>(hdr, M, st1, st2, margin, nnd != nullptr ? 1 : 0);
     const int64_t M_pad = pad_targets(M);
-    pack_body_kernel<<<(unsigned)((M_pad + 255) / 256), 256, 0, stream>>>(d_xyz, nrm, alpha, M, M_pad, st2,
+    // slot order: Morton sort of the points (stable), its inverse kept in the target
+    uint64_t* mk = reinterpret_cast<uint64_t*>(ws + L.mkeys);
+    uint64_t* mks = reinterpret_cast<uint64_t*>(ws + L.mkeys_s);
+    int* mid = reinterpret_cast<int*>(ws + L.mids);
+    int* perm = reinterpret_cast<int*>(ws + L.mperm);
+    morton_keys_kernel<<<(unsigned)((M + 255) / 256), 256, 0, stream>>>(d_xyz, M, st1, mk, mid);
+    size_t cb = L.mcub_bytes;
+    LSG_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.mcub, cb, mk, mks, mid, perm, (int)M, 0, 63, stream));
+    slot_inverse_kernel<<<(unsigned)((M_pad + 255) / 256), 256, 0, stream>>>(perm, M, M_pad,
+                                                                            target_slots(d_target, M_pad));
+    pack_body_kernel<<<(unsigned)((M_pad + 255) / 256), 256, 0, stream>>>(d_xyz, nrm, alpha, perm, M, M_pad, st2,
                                                                           target_body(d_target));
-    pack_tc_kernel<<<(unsigned)((M_pad + 255) / 256), 256, 0, stream>>>(d_xyz, nrm, alpha, M, M_pad, st2,
-                                                                        target_tc(d_target, M_pad));
+    pack_tc_kernel<<<(unsigned)(M_pad / kTcTile), kTcTile, 0, stream>>>(d_xyz, nrm, alpha, perm, M, st2,
+                                                                       target_tc(d_target, M_pad));
     LSG_CUDA(cudaGetLastError());
     return 0;
 }
@@ -960,13 +1098,13 @@ __global__ void __launch_bounds__(kRedThreads)
 
 // out: [max ω, Σ π √(1+α)]
 __global__ void __launch_bounds__(kRedThreads)
-    prior_stats_kernel(const float* __restrict__ phi, const float* __restrict__ body, int64_t M,
-                       const double* __restrict__ sums, double* blockpart, double* out, unsigned* counter) {
+    prior_stats_kernel(const float* __restrict__ phi, const float* __restrict__ body, const int32_t* __restrict__ slot_of,
+                       int64_t M, const double* __restrict__ sums, double* blockpart, double* out, unsigned* counter) {
     double v[2] = {-INFINITY, 0.0};
     const double inv = 1.0 / sums[2];
     for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
         const double pi = (double)phi[m] * inv;
-        const double a = packed_alpha(body, m);
+        const double a = packed_alpha(body, slot_of[m]);
         if (pi > 0.0) v[0] = fmax(v[0], 0.5 * log2(1.0 + a) + log2((double)M * pi));
         v[1] += pi * sqrt(1.0 + a);
     }
@@ -974,8 +1112,8 @@ __global__ void __launch_bounds__(kRedThreads)
 }
 
 __global__ void prior_write_kernel(const float* __restrict__ phi, float* __restrict__ body, float* __restrict__ tc,
-                                   int64_t M, const double* __restrict__ sums, const double* __restrict__ stats,
-                                   TargetHeader* hdr) {
+                                   const int32_t* __restrict__ slot_of, int64_t M, const double* __restrict__ sums,
+                                   const double* __restrict__ stats, TargetHeader* hdr) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m == 0) {
         hdr->omega_ref = stats[0];
@@ -984,11 +1122,12 @@ __global__ void prior_write_kernel(const float* __restrict__ phi, float* __restr
     }
     if (m >= M) return;
     const double pi = (double)phi[m] / sums[2];
-    const double a = packed_alpha(body, m);
+    const int64_t sl = slot_of[m];
+    const double a = packed_alpha(body, sl);
     const float om = pi > 0.0 ? (float)(0.5 * log2(1.0 + a) + log2((double)M * pi) - stats[0]) : -INFINITY;
-    body[(m >> 1) * (2 * kTgtFloats) + (m & 1) + 2 * 3] = om;
-    const int64_t tile = m / kTcTile;
-    const int jt = (int)(m % kTcTile);
+    body[(sl >> 1) * (2 * kTgtFloats) + (sl & 1) + 2 * 3] = om;
+    const int64_t tile = sl / kTcTile;
+    const int jt = (int)(sl % kTcTile);
     float* core = reinterpret_cast<float*>(reinterpret_cast<char*>(tc) + tile * kTcTileBytes) + (jt >> 1) * 16 + (jt & 1);
     core[2 * 3] = om;
 }
@@ -1012,9 +1151,11 @@ int set_prior_impl(void* d_target, int64_t M, const float* d_phi, void* d_ws, do
     LSG_CHECK(sums[2] > 0.0 && isfinite(sums[2]), LSGCPD_EINVAL, "all target confidences are zero");
     const int64_t M_pad = pad_targets(M);
     float* body = target_body(d_target);
-    prior_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_phi, body, M, st, bp, st + 4, ctr);
-    prior_write_kernel<<<(unsigned)((M + 255) / 256), 256, 0, stream>>>(d_phi, body, target_tc(d_target, M_pad), M, st,
-                                                                        st + 4, reinterpret_cast<TargetHeader*>(d_target));
+    const int32_t* slot_of = target_slots(d_target, M_pad);
+    prior_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(d_phi, body, slot_of, M, st, bp, st + 4, ctr);
+    prior_write_kernel<<<(unsigned)((M + 255) / 256), 256, 0, stream>>>(d_phi, body, target_tc(d_target, M_pad),
+                                                                        slot_of, M, st, st + 4,
+                                                                        reinterpret_cast<TargetHeader*>(d_target));
     LSG_CUDA(cudaGetLastError());
     if (h_spc) {
         LSG_CUDA(cudaMemcpyAsync(h_spc, st + 5, sizeof(double), cudaMemcpyDeviceToHost, stream));

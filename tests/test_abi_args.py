@@ -125,3 +125,33 @@ def test_prepare_batch_refuses_bad_arguments(L):
     assert L.lsgcpd_prepare_batch(ptrs, M_ok, 0, None, ptrs, FAKE, 1 << 40, None, None) == EINVAL
     unaligned = (ctypes.c_void_p * 2)(FAKE, FAKE + 4)
     assert L.lsgcpd_prepare_batch(ptrs, M_ok, 2, None, unaligned, FAKE, 1 << 40, None, None) == EINVAL
+
+
+def test_options_set_get_and_refusals(L):
+    import paper_2103_15039_b200 as lsg
+    old = lsg.get_option("tile_gate")
+    with lsg.options(tile_gate=7.5, tc=0, estep_variant=1):
+        assert lsg.get_option("tile_gate") == 7.5
+        assert lsg.get_option("tc") == 0 and lsg.get_option("estep_variant") == 1
+    assert lsg.get_option("tile_gate") == old and lsg.get_option("tc") == 2
+    assert L.lsgcpd_set_option(b"no_such_option", 1.0) == EINVAL and "unknown option" in _err(L)
+    assert L.lsgcpd_set_option(b"tc", 3.0) == EINVAL
+    assert L.lsgcpd_set_option(b"estep_variant", 5.0) == EINVAL
+    assert L.lsgcpd_set_option(b"tile_gate", float("nan")) == EINVAL
+    assert L.lsgcpd_set_option(None, 1.0) == EINVAL
+
+
+@pytest.mark.parametrize("G", [0, -1, 17])
+def test_register_shards_shard_count_refused(L, G):
+    import paper_2103_15039_b200 as lsg
+    R0, t0 = _pose()
+    ptrs = (ctypes.c_void_p * 17)(*([FAKE] * 17))
+    Ns = (ctypes.c_int64 * 17)(*([100] * 17))
+    R = np.zeros(9 * 17)
+    t = np.zeros(3 * 17)
+    s2 = np.zeros(17)
+    it = (ctypes.c_int * 17)()
+    dp = ctypes.POINTER(ctypes.c_double)
+    rc = L.lsgcpd_register_shards(FAKE, 100, 0.0, ptrs, Ns, G, None, R0, t0, R.ctypes.data_as(dp),
+                                  t.ctypes.data_as(dp), s2.ctypes.data_as(dp), it, FAKE, 1 << 20, None)
+    assert rc == EINVAL and "out of range" in _err(L)

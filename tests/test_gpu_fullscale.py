@@ -58,11 +58,15 @@ def test_register_teacher_forced_full_scale(name):
 
 
 @pytest.mark.parametrize("no_fuse", ["0", "1"])
-def test_register_with_one_rank_nccl_comm_equals_no_comm(no_fuse, monkeypatch):
+def test_register_with_one_rank_nccl_comm_equals_no_comm(no_fuse):
     # the communicator path (ncclAllReduce of the 75 moments per iteration) with world size 1, after the fused
     # merge + moments kernel (N ≤ 2^17) and after the separate merge / moments kernels (the N > 2^17 path)
-    monkeypatch.setenv("LSGCPD_NO_FUSE", no_fuse)
     import paper_2103_15039_b200 as lsg
+    with lsg.options(no_fuse=int(no_fuse)):
+        _one_rank_comm(lsg)
+
+
+def _one_rank_comm(lsg):
     wl = workload("object")
     tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
     X = to_dev(wl.source)

@@ -81,7 +81,10 @@ def test_register_full_size_vs_golden(name):
     gpu = lsg.register(tgt, to_dev(wl.source), g["iters"], w=wl.w, traces=True)
     assert gpu["status"] == 0 and gpu["iters"] == g["iters"]
     _close(gpu["R"], gpu["t"], np.array(g["R"]), np.array(g["t"]), g["extent"])
-    assert gpu["sigma2"] == pytest.approx(g["sigma2"], rel=1e-3)
+    # final σ² to 2e-5 relative (achieved in round 1: 5e-8 / 5e-6 / 9e-7, profiles/r01k_golden_errors.txt) and
+    # the whole σ² trace to 1e-4 (lidar's early iterations: 3.9e-5)
+    assert gpu["sigma2"] == pytest.approx(g["sigma2"], rel=2e-5)
+    np.testing.assert_allclose(gpu["sigma2_trace"], np.array(g["sigma2_trace"])[: len(gpu["sigma2_trace"])], rtol=1e-4)
 
 
 def test_register_nll_monotone_and_deterministic():
@@ -149,7 +152,7 @@ def test_register_tolerance_stops_early_and_matches_a_fixed_count():
 
 
 @pytest.mark.parametrize("name,conf", [("tiny", False), ("object", True)])
-def test_fused_em_tail_equals_separate_kernels(name, conf, monkeypatch):
+def test_fused_em_tail_equals_separate_kernels(name, conf):
     # N ≤ 2^17: merge + moments + Newton run as one kernel (em_tail_kernel); LSGCPD_NO_FUSE=1 selects the
     # separate merge / moments / Newton kernels.  Same records, different FP64 summation order of the moments:
     # the registrations agree to FP64 rounding, with and without per-point confidence weights.
@@ -159,15 +162,15 @@ def test_fused_em_tail_equals_separate_kernels(name, conf, monkeypatch):
     phi = to_dev(np.random.default_rng(2).uniform(0.3, 1.0, wl.N).astype(np.float32)) if conf else None
     kw = dict(w=wl.w, traces=True, src_conf=phi) if conf else dict(w=wl.w, traces=True)
     fused = lsg.register(tgt, to_dev(wl.source), 30, **kw)
-    monkeypatch.setenv("LSGCPD_NO_FUSE", "1")
-    sep = lsg.register(tgt, to_dev(wl.source), 30, **kw)
+    with lsg.options(no_fuse=1):
+        sep = lsg.register(tgt, to_dev(wl.source), 30, **kw)
     assert fused["iters"] == sep["iters"] == 30
     _close(fused["R"], fused["t"], sep["R"], sep["t"], tgt.extent, tol=1e-9)
     np.testing.assert_allclose(fused["sigma2_trace"], sep["sigma2_trace"], rtol=1e-9)
     np.testing.assert_allclose(fused["nll"], sep["nll"], rtol=1e-10)
 
 
-def test_graph_cache_replay_and_update_match_fresh_graphs(monkeypatch):
+def test_graph_cache_replay_and_update_match_fresh_graphs():
     # lsgcpd_register keeps the instantiated EM-iteration graph of recent calls: a repeated call replays it, a
     # call with other buffers of the same sizes updates it in place (cudaGraphExecUpdate).  Both must give
     # exactly what a freshly captured graph gives (LSGCPD_GRAPH_CACHE=0).
@@ -179,8 +182,8 @@ def test_graph_cache_replay_and_update_match_fresh_graphs(monkeypatch):
         tgt = lsg.prepare_target(to_dev(w.target), w.knn_k)
         probs.append(lsg.Registrar(tgt, to_dev(w.source), 25))
     cached = [p(w=0.1) for p in probs] + [probs[0](w=0.1), probs[1](w=0.2)]
-    monkeypatch.setenv("LSGCPD_GRAPH_CACHE", "0")
-    fresh = [p(w=0.1) for p in probs] + [probs[0](w=0.1), probs[1](w=0.2)]
+    with lsg.options(graph_cache=0):
+        fresh = [p(w=0.1) for p in probs] + [probs[0](w=0.1), probs[1](w=0.2)]
     for a, b in zip(cached, fresh):
         assert a["iters"] == b["iters"] == 25
         np.testing.assert_array_equal(a["R"], b["R"])
@@ -207,4 +210,4 @@ def test_register_object_extensions_vs_golden(name):
         assert np.linalg.norm(np.asarray(gpu["t"]) - np.array(g["t"])) <= 1e-4 * g["extent"]
     else:
         _close(gpu["R"], gpu["t"], np.array(g["R"]), np.array(g["t"]), g["extent"])
-    assert gpu["sigma2"] == pytest.approx(g["sigma2"], rel=1e-3)
+    assert gpu["sigma2"] == pytest.approx(g["sigma2"], rel=2e-5)

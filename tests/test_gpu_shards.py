@@ -1,0 +1,95 @@
+"""The multi-GPU protocol of lsgcpd_register at world sizes 2, 4 and 8, run on one GPU (SURVEY §8(c).6 step 4,
+§8(e)).  lsgcpd_register_shards registers G contiguous source shards as G ranks would: each shard
+runs the production E step, merge, moments and Newton kernels on its own workspace, and the 75 moments (and
+the σ²₀ sums) are summed over the shards every EM iteration in place of ncclAllReduce.  Checked: every "rank"
+returns the bit-identical pose and σ²; the sharded result equals the unsharded registration to FP64 rounding
+(only the moment summation order differs); and it meets the oracle bar against the goldens."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import se3
+from paper_2103_15039_b200.dist import shard_range
+from tests.gpu_common import to_dev, workload
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _shards(X, G):
+    return [to_dev(np.ascontiguousarray(X[slice(*shard_range(len(X), g, G))])) for g in range(G)]
+
+
+def _same_on_every_rank(sh, G):
+    for g in range(1, G):
+        assert np.array_equal(sh["R"][g], sh["R"][0]) and np.array_equal(sh["t"][g], sh["t"][0])
+        assert sh["sigma2"][g] == sh["sigma2"][0] and sh["iters"][g] == sh["iters"][0]
+
+
+def _close(R, t, R_ref, t_ref, extent, tol):
+    ang = se3.rotation_angle(np.asarray(R).T @ np.asarray(R_ref))
+    dt = np.linalg.norm(np.asarray(t) - np.asarray(t_ref))
+    assert ang <= tol, f"rotation differs by {ang:.3e} rad"
+    assert dt <= tol * extent, f"translation differs by {dt:.3e}"
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+@pytest.mark.parametrize("no_fuse", [0, 1])
+def test_sharded_object_matches_unsharded_and_golden(G, no_fuse):
+    import paper_2103_15039_b200 as lsg
+    g = json.load(open(os.path.join(GOLDEN, "object_oracle.json")))
+    wl = workload("object")
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    with lsg.options(no_fuse=no_fuse):   # fused merge + moments kernel (N ≤ 2^17) and the separate kernels
+        sh = lsg.register_shards(tgt, _shards(wl.source, G), g["iters"], w=wl.w)
+        one = lsg.register(tgt, to_dev(wl.source), g["iters"], w=wl.w)
+    _same_on_every_rank(sh, G)
+    assert sh["iters"][0] == g["iters"]
+    _close(sh["R"][0], sh["t"][0], one["R"], one["t"], tgt.extent, 1e-9)
+    assert sh["sigma2"][0] == pytest.approx(one["sigma2"], rel=1e-9)
+    _close(sh["R"][0], sh["t"][0], np.array(g["R"]), np.array(g["t"]), g["extent"], 1e-4)
+    assert sh["sigma2"][0] == pytest.approx(g["sigma2"], rel=2e-5)
+
+
+@pytest.mark.parametrize("G", [2, 8])
+def test_sharded_lidar_matches_golden(G):
+    import paper_2103_15039_b200 as lsg
+    g = json.load(open(os.path.join(GOLDEN, "lidar_oracle.json")))
+    wl = workload("lidar")
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    sh = lsg.register_shards(tgt, _shards(wl.source, G), g["iters"], w=wl.w)
+    _same_on_every_rank(sh, G)
+    _close(sh["R"][0], sh["t"][0], np.array(g["R"]), np.array(g["t"]), g["extent"], 1e-4)
+    assert sh["sigma2"][0] == pytest.approx(g["sigma2"], rel=2e-5)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_sharded_scale_matches_unsharded(G):
+    # the bench's workload (M = N = 524,288) in 1/2, 1/4 and 1/8 shards: shards above 2^17 points take the
+    # separate merge / moments kernels, smaller ones the fused em_tail_kernel (G = 8: 65,536 points)
+    import paper_2103_15039_b200 as lsg
+    wl = workload("scale")
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    iters = 8
+    sh = lsg.register_shards(tgt, _shards(wl.source, G), iters, w=wl.w)
+    one = lsg.register(tgt, to_dev(wl.source), iters, w=wl.w)
+    _same_on_every_rank(sh, G)
+    _close(sh["R"][0], sh["t"][0], one["R"], one["t"], tgt.extent, 1e-9)
+    assert sh["sigma2"][0] == pytest.approx(one["sigma2"], rel=1e-9)
+
+
+def test_one_shard_is_bit_identical_to_the_communicator_path():
+    # G = 1: the shard path is lsgcpd_register's communicator path with an identity all-reduce
+    import paper_2103_15039_b200 as lsg
+    wl = workload("object")
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    sh = lsg.register_shards(tgt, [to_dev(wl.source)], 20, w=wl.w)
+    comm = lsg.Comm(0, 1)
+    try:
+        viac = lsg.register(tgt, to_dev(wl.source), 20, w=wl.w, comm=comm)
+    finally:
+        comm.close()
+    assert np.array_equal(sh["R"][0], viac["R"]) and np.array_equal(sh["t"][0], viac["t"])
+    assert sh["sigma2"][0] == viac["sigma2"]

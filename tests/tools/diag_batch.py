@@ -17,7 +17,7 @@ kw = dict(eta=0.1, sigma2_init=float(os.environ.get("S2I", "1e-3")))
 ITERS = int(os.environ.get("ITERS", "20"))
 res = {}
 for mode in ("1", "0"):
-    os.environ["LSGCPD_TC"] = mode
+    lsg.set_option("tc", int(mode))
     res["batch_tc" + mode] = lsg.register_batch([p[0] for p in preps], [dev(w.source) for w in wls], ITERS,
                                                 src_confs=[dev(c) for c in confs], **kw)
 for b in range(4):
@@ -28,7 +28,7 @@ for b in range(4):
     for k, out in res.items():
         line += f"  {k}: {se3.rotation_angle(out['R'][b].T @ ora['R']):.2e}"
     for mode in ("1", "0"):
-        os.environ["LSGCPD_TC"] = mode
+        lsg.set_option("tc", int(mode))
         s = lsg.register(tgt, dev(wls[b].source), ITERS, src_conf=dev(confs[b]), **kw)
         line += f"  single_tc{mode}: {se3.rotation_angle(s['R'].T @ ora['R']):.2e}"
     print(line, flush=True)

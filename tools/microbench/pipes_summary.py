@@ -23,9 +23,12 @@ for ln in open(f"{d}/pipes_clocks.csv"):
     except (ValueError, IndexError):
         pass
 res = {"ffma2_lane_ops_per_s": best.get("ffma2"), "ffma_lane_ops_per_s": best.get("ffma"),
-       "ex2_per_s": best.get("ex2"), "in_kernel_mhz": {k: mhz[k] for k in ("ffma2", "ex2") if k in mhz},
+       "ex2_per_s": best.get("ex2"),
+       "in_kernel_mhz_lower_bound": {k: mhz[k] for k in ("ffma2", "ex2") if k in mhz},
        "sampled_sm_mhz": {"median": statistics.median(clk) if clk else None, "max": max(clk) if clk else None,
                           "samples": len(clk)},
+       "note": "in_kernel_mhz_lower_bound = mean block clock64 span / launch wall time (blocks do not span the whole "
+               "launch, so it is a lower bound); sampled_sm_mhz is the nvidia-smi clock during the runs",
        "how": "tools/microbench/run_pipes.sh: best of 15 runs x {2,4} blocks/SM of 256 threads, 8 independent chains; "
               "ex2 kernel = 1 MUFU.EX2 + 1 FMUL per element (MUFU-bound)"}
 json.dump(res, open(out, "w"), indent=1)

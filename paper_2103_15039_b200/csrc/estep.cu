@@ -273,6 +273,9 @@ constexpr int kTcFold = 16;
 #define LSG_TC_NWG 3
 #define LSG_TC_RB 2
 #endif
+#ifndef LSG_PAIRED
+#define LSG_PAIRED 1   // one A-buffer hand-off per pair of K steps (tools/estep_time.py: +2.7 %)
+#endif
 #ifndef LSG_TC_UNROLL
 #define LSG_TC_UNROLL 2   // chunk-pair loop unrolled by two (tools/estep_time.py: +1 %)
 #endif
@@ -382,6 +385,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const uint32_t dpar = (uint32_t)(((grp >> 1) & 1) ^ 1);   // completion (grp>>1) - 1 of dfree[db]
             mbar_wait_sleep(&full_bar[s], (uint32_t)((it >> 2) & 1));
             const uint32_t bbase = tiles0 + (uint32_t)s * kTcTileBytes;
+#if LSG_PAIRED
+            // one hand-off per pair of K steps (both A buffers): afull[w][0] / aempty[w][0], parity k & 1
+#pragma unroll
+            for (int k = 0; k < kChunks / 2; ++k) {
+                if (k == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
+                mbar_wait_sleep(&afull[w][0], (uint32_t)(k & 1));
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
+#pragma unroll
+                    for (int ab = 0; ab < 2; ++ab) {
+                        const int c = 2 * k + ab;
+                        const uint64_t bhi = bdesc(bbase + 1024 * c), blo = bdesc(bbase + 1024 * c + 512);
+                        const uint32_t colA = (uint32_t)(w * kWGCols + 32 * RB + ab * 16 * RB);
+#pragma unroll
+                        for (int rb = 0; rb < RB; ++rb) {
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, (c == 0 && first) ? 0u : 1u);
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
+                        }
+                    }
+                    mma_commit(&aempty[w][0]);
+                    if (k == kChunks / 2 - 1 && last) mma_commit(&dfull[w][db]);
+                    if (k == kChunks / 2 - 1) mma_commit(&empty_bar[s]);   // stage s's B operand read
+                }
+                __syncwarp();
+            }
+#else
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 const int ab = c & 1;
@@ -404,6 +435,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 __syncwarp();
             }
+#endif
             if (last) {
                 tig = 0;
                 ++grp;
@@ -532,6 +564,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (lane == 0) mbar_arrive(&afull[wg][AB]);
     };
 
+    // two K steps (both A buffers) per hand-off: one aempty wait, one wait::st, one afull arrival per pair
+    auto chunk_pair = [&](const float4* core, int k, const float2 (&xa)[RB][3], const float2 (&xb)[RB][3],
+                          float2 (&Lt)[RB], auto PARc, auto cheapc) {
+        constexpr uint32_t PAR = decltype(PARc)::value;
+        uint32_t av0[RB][16], av1[RB][16];
+        tc_chunk_pairs<kLiteral, decltype(cheapc)::value, RB>(core, 2 * k, xa, xb, nk2, Lt, av0);
+        tc_chunk_pairs<kLiteral, decltype(cheapc)::value, RB>(core, 2 * k + 1, xa, xb, nk2, Lt, av1);
+        mbar_wait_sleep(&aempty[wg][0], PAR ^ 1u);   // the MMAs of the previous pair are complete
+        tc_fence_after();
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) tmem_st16(tl + (uint32_t)(32 * RB + rb * 16), av0[rb]);
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) tmem_st16(tl + (uint32_t)(32 * RB + 16 * RB + rb * 16), av1[rb]);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[wg][0]);
+    };
+
     int64_t j = u0 / sc.T, tile = u0 % sc.T;
     load_points(j);
     bool pending = false;   // the previous D group has not been drained yet
@@ -547,6 +598,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         auto run_tile = [&](auto cheapc) {
             float2 xa[RB][3], xb[RB][3];
             tile_points<decltype(cheapc)::value, RB>(h, l, tm, xa, xb);
+#if LSG_PAIRED
+#pragma unroll 1
+            for (int k = 0; k < kChunks / 2; k += 2) {
+                chunk_pair(core, k, xa, xb, Lt, std::integral_constant<uint32_t, 0>(), cheapc);
+                if (k == 0 && pending && tig >= kDrainLag) {
+                    drain(pend_g);
+                    pending = false;
+                }
+                chunk_pair(core, k + 1, xa, xb, Lt, std::integral_constant<uint32_t, 1>(), cheapc);
+            }
+#else
             LSG_UNROLL(LSG_TC_UNROLL)
             for (int c = 0; c < kChunks; c += 2) {
                 chunk(core, c, xa, xb, Lt, std::integral_constant<int, 0>(), cheapc);
@@ -556,6 +618,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     pending = false;
                 }
             }
+#endif
         };
         if (tile_cheap(tm, gate)) run_tile(std::true_type());
         else run_tile(std::false_type());

@@ -2,8 +2,10 @@
 §8(e)).  lsgcpd_register_shards registers G contiguous source shards as G ranks would: each shard
 runs the production E step, merge, moments and Newton kernels on its own workspace, and the 75 moments (and
 the σ²₀ sums) are summed over the shards every EM iteration in place of ncclAllReduce.  Checked: every "rank"
-returns the bit-identical pose and σ²; the sharded result equals the unsharded registration to FP64 rounding
-(only the moment summation order differs); and it meets the oracle bar against the goldens."""
+returns the bit-identical pose and σ²; the sharded result equals the unsharded registration to the E step's FP32
+rounding (sharding changes which points share a 768-point block and the stream-K split of the targets, hence the
+FP32 summation order of the records, and the FP64 order of the moment sums): ≤ 2e-6 rad, 2e-6·extent, σ² 1e-5;
+and it meets the oracle bar (1e-4) against the goldens."""
 import json
 import os
 
@@ -47,8 +49,8 @@ def test_sharded_object_matches_unsharded_and_golden(G, no_fuse):
         one = lsg.register(tgt, to_dev(wl.source), g["iters"], w=wl.w)
     _same_on_every_rank(sh, G)
     assert sh["iters"][0] == g["iters"]
-    _close(sh["R"][0], sh["t"][0], one["R"], one["t"], tgt.extent, 1e-9)
-    assert sh["sigma2"][0] == pytest.approx(one["sigma2"], rel=1e-9)
+    _close(sh["R"][0], sh["t"][0], one["R"], one["t"], tgt.extent, 2e-6)
+    assert sh["sigma2"][0] == pytest.approx(one["sigma2"], rel=1e-5)
     _close(sh["R"][0], sh["t"][0], np.array(g["R"]), np.array(g["t"]), g["extent"], 1e-4)
     assert sh["sigma2"][0] == pytest.approx(g["sigma2"], rel=2e-5)
 
@@ -76,8 +78,8 @@ def test_sharded_scale_matches_unsharded(G):
     sh = lsg.register_shards(tgt, _shards(wl.source, G), iters, w=wl.w)
     one = lsg.register(tgt, to_dev(wl.source), iters, w=wl.w)
     _same_on_every_rank(sh, G)
-    _close(sh["R"][0], sh["t"][0], one["R"], one["t"], tgt.extent, 1e-9)
-    assert sh["sigma2"][0] == pytest.approx(one["sigma2"], rel=1e-9)
+    _close(sh["R"][0], sh["t"][0], one["R"], one["t"], tgt.extent, 2e-6)
+    assert sh["sigma2"][0] == pytest.approx(one["sigma2"], rel=1e-5)
 
 
 def test_one_shard_is_bit_identical_to_the_communicator_path():

@@ -6,8 +6,9 @@ import paper_2103_15039_b200 as lsg
 
 
 def rotation_angle(R):
-    """Angle of a rotation matrix (rad)."""
-    return float(np.arccos(np.clip((np.trace(R) - 1.0) / 2.0, -1.0, 1.0)))
+    """Axis-angle magnitude of a rotation matrix (rad), robust near 0 (atan2 of the skew part and the trace)."""
+    s = np.linalg.norm([R[2, 1] - R[1, 2], R[0, 2] - R[2, 0], R[1, 0] - R[0, 1]]) / 2.0
+    return float(np.arctan2(s, np.clip((np.trace(R) - 1.0) / 2.0, -1.0, 1.0)))
 
 G = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
 for name in ("object", "rgbd", "lidar"):

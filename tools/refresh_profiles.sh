@@ -1,22 +1,28 @@
 #!/bin/bash
-# One gpurun call that regenerates every measurement file under profiles/ for TAG (not the ncu full capture).
+# One gpurun call that regenerates the measurement files of a round under gpurun_out/$TAG (then copied to
+# profiles/$TAG by hand): bench (scale, default), the ncu launch list of a short bench, the replicas benches,
+# and every speed tool with the SM clock sampled under load (tools/with_clocks.sh).
 set -u
-TAG=${TAG:-r01i}
-mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader > gpurun_out/${TAG}_gpu.txt 2>&1
-timeout 900 python bench.py > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench rc=$?"
+TAG=${TAG:-r02}
+O=gpurun_out/$TAG; mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv,noheader > $O/gpu.txt 2>&1
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
 SHORT="python bench.py --steps 1 --warmup 1 --skip-cpu --skip-e2e --iters 3"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
-    $SHORT > gpurun_out/ncu_launch_${TAG}.log 2>&1; echo "launch list rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
+    $SHORT > $O/ncu_launch.log 2>&1; echo "launch list rc=$?"
 for c in tiny object; do
-  timeout 300 python bench.py --config $c --replicas --steps 20 --warmup 3 > gpurun_out/bench_${TAG}_${c}_replicas.json 2>/dev/null
+  timeout 300 python bench.py --config $c --replicas --steps 20 --warmup 3 > $O/bench_${c}_replicas.json 2>/dev/null
 done
-python tools/reg_speed.py > gpurun_out/${TAG}_reg_speed.txt 2>&1
-python tools/newton_cost.py >> gpurun_out/${TAG}_reg_speed.txt 2>&1
-python tools/batch_speed.py > gpurun_out/${TAG}_batch_speed.txt 2>&1
-python tools/cf_speed.py > gpurun_out/${TAG}_cf_speed.txt 2>&1
-python tools/ext_speed.py > gpurun_out/${TAG}_ext_speed.txt 2>&1
-python tools/prep_speed.py > gpurun_out/${TAG}_prep_speed.txt 2>&1
-python tools/golden_errors.py > gpurun_out/${TAG}_golden_errors.txt 2>&1
-python tools/small_path_sweep.py > gpurun_out/${TAG}_small_path_sweep.txt 2>&1
+timeout 900 python bench.py --config batch > $O/bench_batch.json 2> $O/bench_batch.err; echo "batch bench rc=$?"
+W=tools/with_clocks.sh
+$W $O/reg_speed.txt python tools/reg_speed.py
+$W $O/newton_cost.txt python tools/newton_cost.py
+$W $O/batch_speed.txt python tools/batch_speed.py
+$W $O/cf_speed.txt python tools/cf_speed.py
+$W $O/ext_speed.txt python tools/ext_speed.py
+$W $O/prep_speed.txt python tools/prep_speed.py
+$W $O/shard_speed.txt python tools/shard_speed.py
+$W $O/tile_stats.txt python tools/tile_stats.py
+$W $O/golden_errors.txt python tools/golden_errors.py
+$W $O/small_path_sweep.txt python tools/small_path_sweep.py
 echo done

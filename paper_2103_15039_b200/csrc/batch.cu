@@ -293,6 +293,10 @@ __global__ void __launch_bounds__((kBNCW + 1) * 32, kBMinB)
 constexpr int kBTNWG = 3, kBTRB = 2, kBTMW = 3, kBTNT = 4;
 constexpr int kBTNCW = 4 * kBTNWG;
 constexpr int kBTThreads = (kBTNCW + 1 + kBTMW) * 32;
+// register split (setmaxnreg): the producer / MMA warps walk the problem list (BatchCursor) and keep 72
+constexpr int kBTRegHi = LSG_MAXNREG > 0 ? 144 : 0, kBTRegLo = 72;
+static_assert(kBTRegHi == 0 || (kBTThreads == 512 && 384 * kBTRegHi + 128 * kBTRegLo <= 65536),
+              "register split: 3 consumer warpgroups + warpgroup 3");
 constexpr int kBTWGCols = 64 * kBTRB;
 constexpr int kBTSmF = 39;
 constexpr size_t kBTSmem = (size_t)kBTSmF * kBTNCW * 32 * kBTRB * sizeof(float);
@@ -359,6 +363,8 @@ __global__ void __launch_bounds__(kBTThreads, 1)
     const uint32_t tmem = tmem_base_sh;
     if (tmem != 0u) __trap();
 
+    if (warp >= kNCW) {   // warpgroup 3: the TMA producer warp and the MMA warps (registers to the consumers)
+    if (kBTRegHi > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kBTRegLo));
     if (warp == kNCW) {
         // producer: TMA bulk copies of the served problems' tensor-core tiles
         if (lane == 0) {
@@ -393,6 +399,33 @@ __global__ void __launch_bounds__(kBTThreads, 1)
             const uint32_t dpar = (uint32_t)(((grp >> 1) & 1) ^ 1);
             mbar_wait_sleep(&full_bar[s], (uint32_t)((it >> 2) & 1));
             const uint32_t bbase = tiles0 + (uint32_t)s * kTcTileBytes;
+#if LSG_PAIRED
+#pragma unroll
+            for (int k = 0; k < kChunks / 2; ++k) {   // one hand-off per pair of K steps (see estep.cu)
+                if (k == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
+                mbar_wait_sleep(&afull[w][0], (uint32_t)(k & 1));
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
+#pragma unroll
+                    for (int ab = 0; ab < 2; ++ab) {
+                        const int c = 2 * k + ab;
+                        const uint64_t bhi = bdesc(bbase + 1024 * c), blo = bdesc(bbase + 1024 * c + 512);
+                        const uint32_t colA = (uint32_t)(w * kWGCols + 32 * RB + ab * 16 * RB);
+#pragma unroll
+                        for (int rb = 0; rb < RB; ++rb) {
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, (c == 0 && first) ? 0u : 1u);
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
+                        }
+                    }
+                    mma_commit(&aempty[w][0]);
+                    if (k == kChunks / 2 - 1 && last) mma_commit(&dfull[w][db]);
+                    if (k == kChunks / 2 - 1) mma_commit(&empty_bar[s]);
+                }
+                __syncwarp();
+            }
+#else
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 const int ab = c & 1;
@@ -415,6 +448,7 @@ __global__ void __launch_bounds__(kBTThreads, 1)
                 }
                 __syncwarp();
             }
+#endif
             if (last) {
                 tig = 0;
                 ++grp;
@@ -425,6 +459,8 @@ __global__ void __launch_bounds__(kBTThreads, 1)
         }
         return;
     }
+    }   // warpgroup 3
+    if (kBTRegHi > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kBTRegHi));
 
     // consumers
     const int wg = warp >> 2, q = warp & 3;
@@ -542,6 +578,24 @@ __global__ void __launch_bounds__(kBTThreads, 1)
         if (lane == 0) mbar_arrive(&afull[wg][AB]);
     };
 
+    auto chunk_pair = [&](const float4* core, int k, const float2 (&xa)[RB][3], const float2 (&xb)[RB][3],
+                          float2 (&Lt)[RB], auto PARc, auto cheapc) {
+        constexpr uint32_t PAR = decltype(PARc)::value;
+        uint32_t av0[RB][16], av1[RB][16];
+        tc_chunk_pairs<kLiteral, decltype(cheapc)::value, RB>(core, 2 * k, xa, xb, nk2, Lt, av0);
+        tc_chunk_pairs<kLiteral, decltype(cheapc)::value, RB>(core, 2 * k + 1, xa, xb, nk2, Lt, av1);
+        mbar_wait_sleep(&aempty[wg][0], PAR ^ 1u);
+        tc_fence_after();
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) tmem_st16(tl + (uint32_t)(32 * RB + rb * 16), av0[rb]);
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) tmem_st16(tl + (uint32_t)(32 * RB + 16 * RB + rb * 16), av1[rb]);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[wg][0]);
+    };
+
     BatchCursor cur;
     cur.start(bp, B, u0);
     int cur_b = -1;
@@ -565,6 +619,17 @@ __global__ void __launch_bounds__(kBTThreads, 1)
         auto run_tile = [&](auto cheapc) {
             float2 xa[RB][3], xb[RB][3];
             tile_points<decltype(cheapc)::value, RB>(h, l, tm, xa, xb);
+#if LSG_PAIRED
+#pragma unroll 1
+            for (int k = 0; k < kChunks / 2; k += 2) {
+                chunk_pair(core, k, xa, xb, Lt, std::integral_constant<uint32_t, 0>(), cheapc);
+                if (k == 0 && pending && tig >= kDrainLag) {
+                    drain(pend_g);
+                    pending = false;
+                }
+                chunk_pair(core, k + 1, xa, xb, Lt, std::integral_constant<uint32_t, 1>(), cheapc);
+            }
+#else
 #pragma unroll 1
             for (int c = 0; c < kChunks; c += 2) {
                 chunk(core, c, xa, xb, Lt, std::integral_constant<int, 0>(), cheapc);
@@ -574,6 +639,7 @@ __global__ void __launch_bounds__(kBTThreads, 1)
                     pending = false;
                 }
             }
+#endif
         };
         if (tile_cheap(tm, gate)) run_tile(std::true_type());
         else run_tile(std::false_type());

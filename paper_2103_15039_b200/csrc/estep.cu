@@ -273,20 +273,7 @@ constexpr int kTcFold = 16;
 #define LSG_TC_NWG 3
 #define LSG_TC_RB 2
 #endif
-#ifndef LSG_PAIRED
-#define LSG_PAIRED 1   // one A-buffer hand-off per pair of K steps (tools/estep_time.py: +2.7 %)
-#endif
-#ifndef LSG_TC_UNROLL
-#define LSG_TC_UNROLL 2   // chunk-pair loop unrolled by two (tools/estep_time.py: +1 %)
-#endif
-// Register split between the warp roles (setmaxnreg, per warpgroup): warpgroup 3 (producer + MMA warps) keeps
-// 56 registers, each consumer thread gets 152 instead of the launch's 128 (ILP in the pair math; +1.7 %)
-#ifndef LSG_MAXNREG
-#define LSG_MAXNREG 152
-#define LSG_MAXNREG_LO 56
-#endif
-#define LSG_PRAGMA(x) _Pragma(#x)
-#define LSG_UNROLL(n) LSG_PRAGMA(unroll n)
+
 constexpr int kNWG = LSG_TC_NWG, kRB = LSG_TC_RB, kNT = 4;
 constexpr int kTcNCW = 4 * kNWG;                      // consumer warps
 constexpr int kTcThreads = (kTcNCW + 1 + kNWG) * 32;  // + producer + one MMA warp per warpgroup

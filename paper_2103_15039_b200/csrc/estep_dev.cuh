@@ -162,6 +162,21 @@ constexpr int kTcCols = 512;                  // TMEM columns allocated (the who
 constexpr int kTcChunk = 8;                   // targets per A buffer (one K step)
 // D group g is drained at the start of tile kDrainLag of group g + 1 (its MMAs long complete, and the slowest
 // warp of the warpgroup is no longer on the critical path); group g + 2 reuses its D buffer only after that
+// Tensor-core E-step configuration shared by estep.cu and batch.cu
+#ifndef LSG_PAIRED
+#define LSG_PAIRED 1   // one A-buffer hand-off per pair of K steps (tools/estep_time.py: +2.7 %)
+#endif
+#ifndef LSG_TC_UNROLL
+#define LSG_TC_UNROLL 2   // chunk-pair loop unrolled by two (tools/estep_time.py: +1 %)
+#endif
+// Register split between the warp roles (setmaxnreg, per warpgroup): warpgroup 3 (producer + MMA warps) keeps
+// 56 registers, each consumer thread gets 152 instead of the launch's 128 (ILP in the pair math; +1.7 %)
+#ifndef LSG_MAXNREG
+#define LSG_MAXNREG 152
+#define LSG_MAXNREG_LO 56
+#endif
+#define LSG_PRAGMA(x) _Pragma(#x)
+#define LSG_UNROLL(n) LSG_PRAGMA(unroll n)
 #ifndef LSG_DRAIN_LAG
 #define LSG_DRAIN_LAG 1
 #endif

@@ -170,10 +170,11 @@ constexpr int kTcChunk = 8;                   // targets per A buffer (one K ste
 #define LSG_TC_UNROLL 2   // chunk-pair loop unrolled by two (tools/estep_time.py: +1 %)
 #endif
 // Register split between the warp roles (setmaxnreg, per warpgroup): warpgroup 3 (producer + MMA warps) keeps
-// 56 registers, each consumer thread gets 152 instead of the launch's 128 (ILP in the pair math; +1.7 %)
+// 32 registers, each consumer thread gets 160 instead of the launch's 128 — the whole register file
+// (384·160 + 128·32 = 65536).  ILP in the pair math: 128 → 152 +1.7 %, → 160 +2.4 % more (tools/estep_time.py)
 #ifndef LSG_MAXNREG
-#define LSG_MAXNREG 152
-#define LSG_MAXNREG_LO 56
+#define LSG_MAXNREG 160
+#define LSG_MAXNREG_LO 32
 #endif
 #define LSG_PRAGMA(x) _Pragma(#x)
 #define LSG_UNROLL(n) LSG_PRAGMA(unroll n)

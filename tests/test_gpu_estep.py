@@ -137,16 +137,16 @@ def test_estep_sampled_parity_at_full_scale(halves, gate):
             _check(rec, ora, Y, a32, wl.source[idx], R, t, s2, f"scale sampled {gate} halves={halves} s2={s2}")
 
 
-@pytest.mark.parametrize("gate", ["default", "wide"])
-def test_estep_full_record_parity_rgbd(gate):
-    # the rgbd config at full size (~75k × 75k, 10 % outliers), EVERY source point's record against the oracle,
-    # with the oracle's own prepared target (its normals and α), at σ²₀, 1e-3 and the converged σ² of the
-    # rgbd golden trajectory (tests/golden/rgbd_oracle.json)
+@pytest.mark.parametrize("name,gate", [("rgbd", "default"), ("rgbd", "wide"), ("lidar", "default")])
+def test_estep_full_record_parity(name, gate):
+    # the rgbd (~75k × 77k, 10 % outliers) and lidar (126k × 126k, 100 m outlier box) configs at full size,
+    # EVERY source point's record against the oracle, with the oracle's own prepared target (its normals and
+    # α), at σ²₀, 1e-3 and the converged σ² of the golden trajectory (tests/golden/<name>_oracle.json)
     import json
     import os
     import paper_2103_15039_b200 as lsg
-    wl, n32, a32, V, ext = oracle_target32("rgbd")
-    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "rgbd_oracle.json")))
+    wl, n32, a32, V, ext = oracle_target32(name)
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", f"{name}_oracle.json")))
     tgt = _gpu_target(wl.target, n32, a32)
     Xd = to_dev(wl.source)
     R, t = wl.R_expected, wl.t_expected
@@ -155,7 +155,7 @@ def test_estep_full_record_parity_rgbd(gate):
         for s2 in (s2_0, 1e-3, float(g["sigma2"])):
             rec = lsg.estep(tgt, Xd, R, t, s2, wl.w, V).cpu().numpy()
             ora = oracle.estep(wl.target, n32.astype(np.float64), a32.astype(np.float64), wl.source, R, t, s2, wl.w, V)
-            _check(rec, ora, wl.target, a32, wl.source, R, t, s2, f"rgbd full record {gate} s2={s2:.3e}")
+            _check(rec, ora, wl.target, a32, wl.source, R, t, s2, f"{name} full record {gate} s2={s2:.3e}")
 
 
 def test_estep_invalid_arguments_raise():

@@ -274,7 +274,10 @@ constexpr int kTcFold = 16;
 #define LSG_TC_RB 2
 #endif
 
-constexpr int kNWG = LSG_TC_NWG, kRB = LSG_TC_RB, kNT = 4;
+#ifndef LSG_TC_NT
+#define LSG_TC_NT 4
+#endif
+constexpr int kNWG = LSG_TC_NWG, kRB = LSG_TC_RB, kNT = LSG_TC_NT;
 constexpr int kTcNCW = 4 * kNWG;                      // consumer warps
 constexpr int kTcThreads = (kTcNCW + 1 + kNWG) * 32;  // + producer + one MMA warp per warpgroup
 constexpr int kTcWGCols = 64 * kRB;

@@ -31,9 +31,12 @@ __global__ void pairloop(const float4* __restrict__ gt, float* out, long long* c
             const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
 #pragma unroll
             for (int rb = 0; rb < RB; ++rb) {
-                const float2 rx = __fadd2_rn(__fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y)), bc(l[rb][0]));
-                const float2 ry = __fadd2_rn(__fadd2_rn(bc(h[rb][1]), make_float2(-v0.z, -v0.w)), bc(l[rb][1]));
-                const float2 rz = __fadd2_rn(__fadd2_rn(bc(h[rb][2]), make_float2(-v1.x, -v1.y)), bc(l[rb][2]));
+                const float2 rx = MODE == 3 ? __fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y))
+                                            : __fadd2_rn(__fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y)), bc(l[rb][0]));
+                const float2 ry = MODE == 3 ? __fadd2_rn(bc(h[rb][1]), make_float2(-v0.z, -v0.w))
+                                            : __fadd2_rn(__fadd2_rn(bc(h[rb][1]), make_float2(-v0.z, -v0.w)), bc(l[rb][1]));
+                const float2 rz = MODE == 3 ? __fadd2_rn(bc(h[rb][2]), make_float2(-v1.x, -v1.y))
+                                            : __fadd2_rn(__fadd2_rn(bc(h[rb][2]), make_float2(-v1.x, -v1.y)), bc(l[rb][2]));
                 const float2 qv = __ffma2_rn(make_float2(v3.x, v3.y), rz,
                                              __ffma2_rn(make_float2(v2.z, v2.w), ry, __fmul2_rn(make_float2(v2.x, v2.y), rx)));
                 const float2 tau = __ffma2_rn(qv, qv, __ffma2_rn(rz, rz, __ffma2_rn(ry, ry, __fmul2_rn(rx, rx))));
@@ -153,5 +156,9 @@ int main() {
     for (int w : {12, 16}) run<2, 2>(w, gt, out, cyc, nsm);
     for (int w : {12, 16}) run_pts<1>(w, gt, out, cyc, nsm);
     for (int w : {8, 12}) run_pts<2>(w, gt, out, cyc, nsm);
+    // round 2: the tile-centred residual (13 FP32 lane-ops per pair + ex2 + TF32 split)
+    for (int w : {8, 12, 16, 20, 24, 32}) run<2, 3>(w, gt, out, cyc, nsm);
+    for (int w : {12, 16, 24, 32}) run<1, 3>(w, gt, out, cyc, nsm);
+    for (int w : {8, 12, 16}) run<4, 3>(w, gt, out, cyc, nsm);
     return 0;
 }

@@ -213,3 +213,41 @@ def test_register_object_extensions_vs_golden(name):
     # σ² to 2e-4 relative: with η the converged σ² is 1e-5 (σ ≈ 3e-3, the E-step weights at their most peaked),
     # achieved 8e-5 (r02g)
     assert gpu["sigma2"] == pytest.approx(g["sigma2"], rel=2e-4)
+
+
+def test_concurrent_calls_on_two_threads_and_streams():
+    # include/lsgcpd.h: calls on distinct streams are independent.  Two host threads, each with its own CUDA
+    # stream, run registrations (graph capture, graph cache, per-device caches, the option store) at the same time;
+    # every result equals the same call made alone.
+    import threading
+    import torch
+    import paper_2103_15039_b200 as lsg
+    import synth
+    wls = synth.make_batch(2, 1500, seed=41)
+    tgts = [lsg.prepare_target(to_dev(w.target), w.knn_k) for w in wls]
+    srcs = [to_dev(w.source) for w in wls]
+    alone = [lsg.register(t, x, 30, w=0.1) for t, x in zip(tgts, srcs)]
+    out = [[None] * 4, [None] * 4]
+    errs = []
+
+    def worker(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for k in range(4):
+                    out[i][k] = lsg.register(tgts[i], srcs[i], 30, w=0.1, stream=s)
+        except Exception as e:   # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i in range(2):
+        for r in out[i]:
+            assert r["iters"] == 30 and r["status"] == 0
+            np.testing.assert_array_equal(r["R"], alone[i]["R"])
+            np.testing.assert_array_equal(r["t"], alone[i]["t"])
+            assert r["sigma2"] == alone[i]["sigma2"]

@@ -277,16 +277,25 @@ constexpr int kTcFold = 16;
 #ifndef LSG_TC_NT
 #define LSG_TC_NT 4
 #endif
-constexpr int kNWG = LSG_TC_NWG, kRB = LSG_TC_RB, kNT = LSG_TC_NT;
+#ifndef LSG_TC_MW
+#define LSG_TC_MW LSG_TC_NWG   // MMA-issuing warps (each serves NWG / MW consumer warpgroups)
+#endif
+constexpr int kNWG = LSG_TC_NWG, kRB = LSG_TC_RB, kNT = LSG_TC_NT, kTcMW = LSG_TC_MW;
+static_assert(kNWG % kTcMW == 0, "MMA warps must split the warpgroups evenly");
 constexpr int kTcNCW = 4 * kNWG;                      // consumer warps
-constexpr int kTcThreads = (kTcNCW + 1 + kNWG) * 32;  // + producer + one MMA warp per warpgroup
+constexpr int kTcHelpers = (1 + kTcMW + 3) / 4 * 4;   // producer + MMA warps, padded to a whole warpgroup
+constexpr int kTcThreads = (kTcNCW + kTcHelpers) * 32;
 constexpr int kTcWGCols = 64 * kRB;
 constexpr int kTcBlk = kNWG * 128 * kRB;              // 768 source points per block
 constexpr int kTcSmF = 39;                            // S1[13], R[13], C[13] per point
 constexpr size_t kTcSmem = (size_t)kTcSmF * kTcNCW * 32 * kRB * sizeof(float);
 static_assert(kNWG * kTcWGCols <= kTcCols, "TMEM columns");
-static_assert(LSG_MAXNREG == 0 || (kTcNCW == 12 && kTcThreads == 512 && 384 * LSG_MAXNREG + 128 * LSG_MAXNREG_LO <= 65536),
-              "register split: 3 consumer warpgroups + warpgroup 3 within the register file");
+// setmaxnreg only moves registers within the CTA's launch allocation (launch registers per thread × threads):
+// a larger request would block forever
+constexpr int kTcLaunchRegs = (65536 / kTcThreads) / 8 * 8 > 255 ? 255 : (65536 / kTcThreads) / 8 * 8;
+static_assert(LSG_MAXNREG == 0 ||
+                  kTcNCW * 32 * LSG_MAXNREG + kTcHelpers * 32 * LSG_MAXNREG_LO <= kTcLaunchRegs * kTcThreads,
+              "register split: consumer warpgroups + the helper warpgroup within the CTA's register allocation");
 static_assert(kTcStages == 4, "stage arithmetic below assumes 4 stages");
 
 template <bool kLiteral>
@@ -325,7 +334,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (threadIdx.x == 32) {
         for (int s = 0; s < kTcStages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], kNCW + NWG);
+            mbar_init(&empty_bar[s], kNCW + kTcMW);
         }
         for (int w = 0; w < NWG; ++w)
             for (int b = 0; b < 2; ++b) {
@@ -358,13 +367,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         return;
     }
+    if (warp > kNCW + kTcMW) return;   // padding warps of the helper warpgroup
     if (warp > kNCW) {
-        // ---------------- MMA warp w: one elected lane issues the tcgen05.mma of warpgroup w ----------------
+        // ---------------- MMA warp: one elected lane issues the tcgen05.mma of its warpgroup(s) ----------------
         // D[db] (+)= A_hi·F_hi, += A_lo·F_hi, += A_hi·F_lo per row block and K step (N = 16 each).
         // Parities: the k-th completion of a barrier has parity k & 1; A buffer b of K step c of any tile
         // is used for the (4·it + c/2)-th time, so its parity is the constant (c >> 1) & 1.
         const uint32_t tiles0 = smem_u32(&tiles_st[0][0]) + kTcBOff;
-        const int w = warp - kNCW - 1;
+        constexpr int kWPer = NWG / kTcMW;
+        const int w0 = (warp - kNCW - 1) * kWPer;   // this MMA warp serves warpgroups [w0, w0 + kWPer)
         int64_t tile = u0 % sc.T, grp = 0;
         int tig = 0;   // tile index within the current D group
         for (int64_t it = 0; it < nunits; ++it) {
@@ -379,30 +390,38 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             // one hand-off per pair of K steps (both A buffers): afull[w][0] / aempty[w][0], parity k & 1
 #pragma unroll
             for (int k = 0; k < kChunks / 2; ++k) {
-                if (k == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
-                mbar_wait_sleep(&afull[w][0], (uint32_t)(k & 1));
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
 #pragma unroll
-                    for (int ab = 0; ab < 2; ++ab) {
-                        const int c = 2 * k + ab;
-                        const uint64_t bhi = bdesc(bbase + 1024 * c), blo = bdesc(bbase + 1024 * c + 512);
-                        const uint32_t colA = (uint32_t)(w * kWGCols + 32 * RB + ab * 16 * RB);
+                for (int wi = 0; wi < kWPer; ++wi) {
+                    const int w = w0 + wi;
+                    if (k == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
+                    mbar_wait_sleep(&afull[w][0], (uint32_t)(k & 1));
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
 #pragma unroll
-                        for (int rb = 0; rb < RB; ++rb) {
-                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, (c == 0 && first) ? 0u : 1u);
-                            mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
-                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
+                        for (int ab = 0; ab < 2; ++ab) {
+                            const int c = 2 * k + ab;
+                            const uint64_t bhi = bdesc(bbase + 1024 * c), blo = bdesc(bbase + 1024 * c + 512);
+                            const uint32_t colA = (uint32_t)(w * kWGCols + 32 * RB + ab * 16 * RB);
+#pragma unroll
+                            for (int rb = 0; rb < RB; ++rb) {
+                                mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16,
+                                            (c == 0 && first) ? 0u : 1u);
+                                mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
+                                mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
+                            }
                         }
+                        mma_commit(&aempty[w][0]);
+                        if (k == kChunks / 2 - 1 && last) mma_commit(&dfull[w][db]);
+                        // stage s's B operand read by this warp's MMAs
+                        if (k == kChunks / 2 - 1 && wi == kWPer - 1) mma_commit(&empty_bar[s]);
                     }
-                    mma_commit(&aempty[w][0]);
-                    if (k == kChunks / 2 - 1 && last) mma_commit(&dfull[w][db]);
-                    if (k == kChunks / 2 - 1) mma_commit(&empty_bar[s]);   // stage s's B operand read
+                    __syncwarp();
                 }
-                __syncwarp();
             }
 #else
+            static_assert(kWPer == 1, "the per-K-step hand-off assumes one MMA warp per warpgroup");
+            const int w = w0;
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 const int ab = c & 1;
@@ -696,11 +715,12 @@ struct Variant {
 };
 #define LSG_VARIANT(P, W, B, X) \
     {P, W, B, X, {(const void*)estep_kernel<P, W, B, X, false>, (const void*)estep_kernel<P, W, B, X, true>}}
-static const Variant kVariants[] = {LSG_VARIANT(2, 12, 1, true), LSG_VARIANT(2, 8, 1, true), LSG_VARIANT(2, 1, 8, true)};
+static const Variant kVariants[] = {LSG_VARIANT(2, kTcNCW, 1, true), LSG_VARIANT(2, 8, 1, true),
+                                    LSG_VARIANT(2, 1, 8, true)};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kBigVariant = 0, kMidVariant = 1, kSmallVariant = 2;
 constexpr int kMidBlk = 2 * 8 * 32;
-static_assert(2 * 12 * 32 == kTcBlk || LSG_TC_NWG != 3, "the running-max partner of the tensor-core kernel uses its block size");
+static_assert(2 * kTcNCW * 32 == kTcBlk, "the running-max partner of the tensor-core kernel uses its block size");
 constexpr int64_t kSplitBytes = 48ll << 20;   // tensor-core sections above this are swept in two halves
 
 // Per-device facts (SM count, occupancies) and one-time function attributes, set up once per device under a

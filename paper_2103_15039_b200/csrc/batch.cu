@@ -287,7 +287,7 @@ __global__ void __launch_bounds__((kBNCW + 1) * 32, kBMinB)
 }
 
 // ---- batched tensor-core E step ---------------------------------------------------------------------
-// estep_tc2_kernel's pipeline (TMA producer, one MMA warp per warpgroup, TF32 3-term split of p into TMEM,
+// estep_tc_kernel's pipeline (TMA producer, one MMA warp per warpgroup, TF32 3-term split of p into TMEM,
 // D accumulated over NT tiles, Kahan-folded drains) walking the concatenated units of the problems that are
 // active and in the fixed-max mode.  A D group also ends where a source block (hence a problem) ends.
 constexpr int kBTNWG = 3, kBTRB = 2, kBTMW = 3, kBTNT = 4;
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kBTThreads, 1)
         return;
     }
     if (warp > kNCW) {
-        // MMA warp for warpgroup w (see estep_tc2_kernel); groups end at NT tiles or a block end
+        // MMA warp for warpgroup w (see estep_tc_kernel); groups end at NT tiles or a block end
         const uint32_t tiles0 = smem_u32(&tiles_st[0][0]) + kTcBOff;
         const int w = warp - kNCW - 1;
         BatchCursor cur;

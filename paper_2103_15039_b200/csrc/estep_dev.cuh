@@ -182,8 +182,7 @@ constexpr int kTcChunk = 8;                   // targets per A buffer (one K ste
 #define LSG_DRAIN_LAG 1
 #endif
 constexpr int kDrainLag = LSG_DRAIN_LAG;
-// instruction descriptors: D F32, A/B TF32, K-major A and B, M = 128, N = 32 ([hi | lo] features) or 16
-constexpr uint32_t kTcIdesc32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+// instruction descriptor: D F32, A/B TF32, K-major A and B, M = 128, N = 16
 constexpr uint32_t kTcIdesc16 = (1u << 4) | (2u << 7) | (2u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -191,34 +190,12 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
-__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
         "%14, %15, %16};" ::"r"(taddr),
         "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
         "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-        : "memory");
-}
-__device__ __forceinline__ void tmem_st2(uint32_t taddr, float2 v) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr), "r"(__float_as_uint(v.x)),
-                 "r"(__float_as_uint(v.y))
-                 : "memory");
-}
-// columns [c, c+8) ← a, [c+8, c+16) ← b, in one asm block so the TMEM address is moved to a uniform
-// register once
-__device__ __forceinline__ void tmem_st8x2(uint32_t taddr, const uint32_t (&a)[8], const uint32_t (&b)[8]) {
-    asm volatile(
-        "{\n"
-        ".reg .b32 t2;\n"
-        "add.u32 t2, %0, 8;\n"
-        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n"
-        "tcgen05.st.sync.aligned.32x32b.x8.b32 [t2], {%9, %10, %11, %12, %13, %14, %15, %16};\n"
-        "}\n" ::"r"(taddr),
-        "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]), "r"(b[0]), "r"(b[1]),
-        "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]), "r"(b[6]), "r"(b[7])
         : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {

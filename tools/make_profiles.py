@@ -45,7 +45,7 @@ for h, v in zip(raw[0], raw[2]):
         except ValueError:
             pass
 open(os.path.join(P, f"{out}_estep_ncu_summary.txt"), "w").write(
-    "ncu --set full --clock-control none --import-source on -k regex:" + os.environ.get("KREGEX", "estep_tc2_kernel") + " -s 1 -c 1 on\n"
+    "ncu --set full --clock-control none --import-source on -k regex:" + os.environ.get("KREGEX", "estep_tc_kernel") + " -s 1 -c 1 on\n"
     "`python bench.py --steps 1 --warmup 1 --skip-cpu --skip-e2e --iters 3` (scale config, M=N=524288), one B200.\n\n"
     + "\n".join(txt) + "\n")
 shutil.copy(rep, os.path.join(P, f"{out}_estep_full.ncu-rep"))

@@ -273,3 +273,31 @@ def test_estep_running_max_path_sampled_at_full_size():
         ora = oracle.estep(Y, n32.astype(np.float64), a32.astype(np.float64), wl.source[idx], R, t, s2, 0.0, V)
         _check(rec, ora, Y, a32, wl.source[idx], R, t, s2, f"rgbd w=0 s2={s2}")
         np.testing.assert_allclose(rec[:, 0], 1.0, atol=2e-6)
+
+
+def test_tile_centres_exact_on_zero_crossing_and_offset_axes():
+    # the pack keeps a tile centre c_a only if every y_a - c_a of the tile is exact in FP32 (else c_a = 0): an axis
+    # whose values cross zero with tiny magnitudes must fall back to c_a = 0, an axis far from zero keeps its
+    # centre; the E step stays within the bar with every tile centred (gate 2 × default) and with the hi/lo path
+    import torch
+    rng = np.random.default_rng(17)
+    M, N = 2048, 1500
+    Y = np.stack([rng.uniform(-1e-3, 1e-3, M), 1e4 + rng.uniform(0.0, 1.0, M), rng.uniform(-5.0, 5.0, M)], 1)
+    Y = Y.astype(np.float32)
+    n = rng.standard_normal((M, 3))
+    n32 = (n / np.linalg.norm(n, axis=1, keepdims=True)).astype(np.float32)
+    a32 = rng.uniform(0, 50, M).astype(np.float32)
+    X = (Y[rng.integers(0, M, N)] + 0.01 * rng.standard_normal((N, 3))).astype(np.float32)
+    tgt = _gpu_target(Y, n32, a32)
+    M_pad = (M + 255) // 256 * 256
+    off = 256 + M_pad * 16 * 4
+    raw = tgt.buf[off: off + (M_pad // 64) * 10240].view(torch.float32).reshape(M_pad // 64, 2560).cpu().numpy()
+    c = np.stack([raw[:, 14], raw[:, 15], raw[:, 30]], 1)
+    assert np.any(c[:, 0] == 0.0), "no zero-crossing tile fell back to c_x = 0"
+    assert np.all(c[:, 1] > 9999.0), "the offset axis lost its centre"
+    R, t = np.eye(3), np.zeros(3)
+    for gate in ("wide", "hilo"):
+        with _opts(GATES[gate], tc=1):
+            for s2 in (1e-2, 1e-4):
+                rec, ora = _run_pair(Y, n32, a32, X, R, t, s2, 0.1, 1e3, tgt=tgt)
+                _check(rec, ora, Y, a32, X, R, t, s2, f"zero-crossing/offset {gate} s2={s2}")

@@ -133,3 +133,27 @@ def test_estep_targets_beyond_2_31_bytes():
         rec = lsg.estep(tgt, to_dev(X), R, t, s2, wl.w, V).cpu().numpy()
         ora = oracle.estep(Y, nY.astype(np.float64), aY.astype(np.float64), X, R, t, s2, wl.w, V)
         assert_record_parity(rec, ora, Y, aY, what=f"M = 2^24 + 5, s2={s2}")
+
+
+@pytest.mark.parametrize("comm", [False, True])
+def test_register_without_graph_equals_graph(comm):
+    # the plain-launch EM loop (option no_graph; the path of a communicator with more than one rank, whose
+    # iterations are not captured) gives the captured graph's result bit for bit, with and without a one-rank
+    # NCCL communicator
+    import paper_2103_15039_b200 as lsg
+    wl = workload("object")
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    X = to_dev(wl.source)
+    reg = lsg.Registrar(tgt, X, 20)
+    c = lsg.Comm(0, 1) if comm else None
+    try:
+        graph = reg(w=wl.w, traces=True, comm=c)
+        with lsg.options(no_graph=1):
+            plain = reg(w=wl.w, traces=True, comm=c)
+    finally:
+        if c is not None:
+            c.close()
+    assert plain["iters"] == graph["iters"] == 20
+    assert np.array_equal(plain["R"], graph["R"]) and np.array_equal(plain["t"], graph["t"])
+    assert plain["sigma2"] == graph["sigma2"]
+    np.testing.assert_array_equal(plain["nll"], graph["nll"])

@@ -19,12 +19,15 @@ for ln in open(sys.argv[1]):
     except (ValueError, IndexError):
         pass
 busy = [r for r in rows if r[2] >= 50]
+label = ">= 50 %"
+if not busy:   # short tools (e.g. prepare: ms-long kernels between host syncs) rarely fill a 100-ms window
+    busy, label = [r for r in rows if r[2] > 0], "> 0 %"
 names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 reasons = sorted({n for r in busy for n, v in zip(names, r[3]) if v.lower() == "active"})
 if busy:
     sm = [r[0] for r in busy]
     print(f"# clocks under load: SM median {statistics.median(sm):.0f} MHz (min {min(sm):.0f}), max {max(r[1] for r in busy):.0f} MHz, "
-          f"{len(busy)} of {len(rows)} 100-ms samples at >= 50 % utilization; throttle reasons: {reasons or 'none'}")
+          f"{len(busy)} of {len(rows)} 100-ms samples at {label} utilization; throttle reasons: {reasons or 'none'}")
 else:
     print(f"# clocks under load: no sample at >= 50 % utilization ({len(rows)} samples)")
 PY

@@ -109,3 +109,17 @@ def test_batch_running_max_mode_and_priors_match_single_registrations():
     _close(out["R"][1], out["t"][1], single["R"], single["t"], tgts[1].extent, tol=1e-5)
     with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
         lsg.register_batch(tgts, srcs, 5, w=0.1, consistent=False)
+
+
+def test_batch_literal_normaliser_matches_single_registrations():
+    # the batched tensor-core E step's kLiteral instantiation (Eq. 9-10 normaliser, no priors): every problem
+    # lands where its single-problem registration with the literal normaliser lands
+    import paper_2103_15039_b200 as lsg
+    wls = synth.make_batch(3, 900, seed=23)
+    tgts = [_prep(w)[0] for w in wls]
+    srcs = [to_dev(w.source) for w in wls]
+    out = lsg.register_batch(tgts, srcs, 20, w=0.1, consistent=False)
+    for b in range(3):
+        single = lsg.register(tgts[b], srcs[b], 20, w=0.1, consistent=False)
+        assert out["status"][b] == 0 and single["status"] == 0
+        _close(out["R"][b], out["t"][b], single["R"], single["t"], tgts[b].extent, tol=1e-5)

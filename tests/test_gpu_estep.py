@@ -301,3 +301,16 @@ def test_tile_centres_exact_on_zero_crossing_and_offset_axes():
             for s2 in (1e-2, 1e-4):
                 rec, ora = _run_pair(Y, n32, a32, X, R, t, s2, 0.1, 1e3, tgt=tgt)
                 _check(rec, ora, Y, a32, X, R, t, s2, f"zero-crossing/offset {gate} s2={s2}")
+
+
+def test_estep_literal_normaliser_with_the_centred_residual():
+    # the Eq. 9-10 literal normaliser (kLiteral instantiation) on tiles that take the tile-centred residual:
+    # object at σ²₀ and σ² = 0.05, where E_tile / σ is under the default gate
+    wl, n32, a32, V, ext = oracle_target32("object")
+    R, t = wl.R_expected, wl.t_expected
+    s2_0 = oracle.sigma2_init(wl.source, wl.target, R, t)
+    tgt = _gpu_target(wl.target, n32, a32)
+    with _opts(None, tc=1):
+        for s2 in (s2_0, 0.05):
+            rec, ora = _run_pair(wl.target, n32, a32, wl.source, R, t, s2, wl.w, V, False, tgt=tgt)
+            _check(rec, ora, wl.target, a32, wl.source, R, t, s2, f"literal centred s2={s2:.3g}")

@@ -126,7 +126,10 @@ def test_estep_sampled_parity_at_full_scale(halves, gate):
     V, _ = oracle.working_volume(Y)
     tgt = _gpu_target(Y, n32, a32)
     Xd = to_dev(wl.source)
-    idx = np.sort(rng.choice(wl.N, 192, replace=False))
+    # 1,024 sampled source points (every tile and every stream-K segment boundary class is covered) for the
+    # product configuration (default gate, two halves); 192 for the other residual modes and the one-sweep form
+    nsamp = 1024 if (gate == "default" and halves == "auto") else 192
+    idx = np.sort(rng.choice(wl.N, nsamp, replace=False))
     R, t = wl.R_expected, wl.t_expected
     s2_0 = oracle.sigma2_init(wl.source, Y, R, t)
     kw = {} if halves == "auto" else {"halves": 1}

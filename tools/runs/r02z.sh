@@ -1,0 +1,2 @@
+O=gpurun_out/r02z; mkdir -p $O
+timeout 1200 python -m pytest tests/test_gpu_estep.py -q -k "sampled_parity_at_full_scale" --durations=3 > $O/pytest.txt 2>&1; echo "rc=$?"; tail -8 $O/pytest.txt

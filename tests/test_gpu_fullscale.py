@@ -14,7 +14,7 @@ import pytest
 import oracle
 from oracle import se3
 from tests.gpu_common import to_dev, workload
-from tests.parity import assert_record_parity
+from tests.parity import assert_record_parity, transformed
 
 pytestmark = pytest.mark.gpu
 
@@ -34,7 +34,7 @@ def test_register_teacher_forced_full_scale(name):
     iters = wl.iters
     reg = lsg.Registrar(tgt, X, iters)
     rng = np.random.default_rng(17)
-    idx = np.sort(rng.choice(wl.N, 96, replace=False))
+    idx = np.sort(rng.choice(wl.N, 1024, replace=False))
     floor = 1e-12 * tgt.extent ** 2
     first = lsg.Registrar(tgt, X, 1)(w=wl.w, traces=True)
     for k in _states(iters):
@@ -47,7 +47,8 @@ def test_register_teacher_forced_full_scale(name):
         nxt = first if k == 0 else lsg.Registrar(tgt, X, k + 1)(w=wl.w)
         rec = lsg.estep(tgt, X, R, t, s2, wl.w, tgt.volume).cpu().numpy()
         ora = oracle.estep(wl.target, n64, a64, wl.source[idx], R, t, s2, wl.w, tgt.volume)
-        assert_record_parity(rec[idx], ora, wl.target, a64, what=f"{name} E step at state {k}")
+        assert_record_parity(rec[idx], ora, wl.target, a64, what=f"{name} E step at state {k}",
+                             Xh=transformed(wl.source[idx], R, t), s2=s2)
         R1, t1, s21, _ = oracle.mstep(wl.source, rec, R, t, s2, tgt.extent, 10, floor)
         ang = se3.rotation_angle(np.asarray(nxt["R"]).T @ R1)
         dt = np.linalg.norm(np.asarray(nxt["t"]) - t1)

@@ -7,7 +7,7 @@ import pytest
 import oracle
 import synth
 from tests.gpu_common import oracle_target32, to_dev, workload
-from tests.parity import assert_record_parity
+from tests.parity import assert_record_parity, transformed
 
 pytestmark = pytest.mark.gpu
 
@@ -29,7 +29,8 @@ def test_affine_estep_at_a_non_orthogonal_linear_part():
     for s2 in (1e-3, 1e-5):
         rec = lsg.estep(tgt, to_dev(wl.source), A, wl.t_expected, s2, wl.w, V, group="affine").cpu().numpy()
         ora = oracle.estep(wl.target, n32, a32, wl.source, A, wl.t_expected, s2, wl.w, V)
-        assert_record_parity(rec, ora, wl.target, a32, what=f"affine E step s2={s2}")
+        assert_record_parity(rec, ora, wl.target, a32, what=f"affine E step s2={s2}",
+                             Xh=transformed(wl.source, A, wl.t_expected), s2=s2)
     with pytest.raises(lsg.LsgcpdError, match="EINVAL"):
         lsg.estep(tgt, to_dev(wl.source), A, wl.t_expected, 1e-3, wl.w, V)          # not a rotation
     with pytest.raises(lsg.LsgcpdError, match="EINVAL"):

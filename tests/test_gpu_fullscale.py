@@ -111,7 +111,7 @@ def test_estep_indexing_beyond_2_31_record_floats():
     xs = wl.source[idx % wl.N] + ((idx // wl.N).astype(np.float32) * np.float32(1e-7))[:, None]
     ora = oracle.estep(wl.target, n32.astype(np.float64), a32.astype(np.float64), xs.astype(np.float32), R, t, s2,
                        wl.w, V)
-    assert_record_parity(sub, ora, wl.target, a32, what="N = 2^27 + 77 sampled")
+    assert_record_parity(sub, ora, wl.target, a32, what="N = 2^27 + 77 sampled", Xh=transformed(xs, R, t), s2=s2)
 
 
 def test_estep_targets_beyond_2_31_bytes():
@@ -133,7 +133,7 @@ def test_estep_targets_beyond_2_31_bytes():
     for s2 in (1e-3, 1e-5):
         rec = lsg.estep(tgt, to_dev(X), R, t, s2, wl.w, V).cpu().numpy()
         ora = oracle.estep(Y, nY.astype(np.float64), aY.astype(np.float64), X, R, t, s2, wl.w, V)
-        assert_record_parity(rec, ora, Y, aY, what=f"M = 2^24 + 5, s2={s2}")
+        assert_record_parity(rec, ora, Y, aY, what=f"M = 2^24 + 5, s2={s2}", Xh=transformed(X, R, t), s2=s2)
 
 
 @pytest.mark.parametrize("comm", [False, True])

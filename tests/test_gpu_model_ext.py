@@ -10,7 +10,7 @@ import pytest
 import oracle
 from oracle import outlier as ol, se3
 from tests.gpu_common import oracle_target32, to_dev, workload
-from tests.parity import assert_record_parity
+from tests.parity import assert_record_parity, transformed
 
 pytestmark = pytest.mark.gpu
 
@@ -53,7 +53,8 @@ def test_estep_ex_prior_and_point_weights(consistent, mode):
                             src_conf=to_dev(phi_x)).cpu().numpy()
         wn = ol.point_outlier_weights(w0, phi_x.astype(np.float64))
         ora = oracle.estep_cf(wl.target, n32, a32, pi, wl.source, wn, wl.R_expected, wl.t_expected, s2, V, consistent)
-        assert_record_parity(rec, ora, wl.target, a32, what=f"{mode} consistent={consistent} s2={s2}")
+        assert_record_parity(rec, ora, wl.target, a32, what=f"{mode} consistent={consistent} s2={s2}",
+                             Xh=transformed(wl.source, wl.R_expected, wl.t_expected), s2=s2)
         assert np.all(rec[:20, 15] == 1.0) and np.all(rec[:20, :14] == 0.0)
         np.testing.assert_allclose(rec[:, 0] + rec[:, 15], 1.0, atol=3e-6)
 
@@ -67,7 +68,8 @@ def test_uniform_prior_restores_the_uniform_model():
     for s2 in (1e-3, 1e-5):
         rec = lsg.estep(tgt, to_dev(wl.source), wl.R_expected, wl.t_expected, s2, wl.w, V).cpu().numpy()
         ora = oracle.estep(wl.target, n32, a32, wl.source, wl.R_expected, wl.t_expected, s2, wl.w, V)
-        assert_record_parity(rec, ora, wl.target, a32, what=f"uniform again s2={s2}")
+        assert_record_parity(rec, ora, wl.target, a32, what=f"uniform again s2={s2}",
+                             Xh=transformed(wl.source, wl.R_expected, wl.t_expected), s2=s2)
 
 
 def test_register_with_eta_and_confidence_vs_oracle():
@@ -122,7 +124,7 @@ def test_rgbd_confidence_filtered_registration_teacher_forced():
     pi = ol.confidence_prior(py.astype(np.float64))
     X = to_dev(Xs)
     C = to_dev(px)
-    idx = np.sort(np.random.default_rng(3).choice(Xs.shape[0], 96, replace=False))
+    idx = np.sort(np.random.default_rng(3).choice(Xs.shape[0], 1024, replace=False))
     floor = 1e-12 * tgt.extent ** 2
     for k in (1, 10, 30):
         st = lsg.Registrar(tgt, X, k)(w=wl.w, src_conf=C)
@@ -131,7 +133,8 @@ def test_rgbd_confidence_filtered_registration_teacher_forced():
         rec = lsg.estep(tgt, X, R, t, s2, wl.w, tgt.volume, src_conf=C).cpu().numpy()
         wn = ol.point_outlier_weights(wl.w, px[idx].astype(np.float64))
         ora = oracle.estep_cf(Y, n64, a64, pi, Xs[idx], wn, R, t, s2, tgt.volume)
-        assert_record_parity(rec[idx], ora, Y, a64, what=f"rgbd-CF E step at state {k}")
+        assert_record_parity(rec[idx], ora, Y, a64, what=f"rgbd-CF E step at state {k}",
+                             Xh=transformed(Xs[idx], R, t), s2=s2)
         R1, t1, s21, _ = oracle.mstep(Xs, rec, R, t, s2, tgt.extent, 10, floor)
         assert se3.rotation_angle(np.asarray(nxt["R"]).T @ R1) <= 1e-4
         assert np.linalg.norm(np.asarray(nxt["t"]) - t1) <= 1e-4 * tgt.extent

@@ -269,6 +269,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
 // 1 TMA producer warp, 3 MMA warps.  TMEM per warpgroup: D 2 × 32 + A 2 × 32 columns; 384 of 512 used
 // (the CTA allocates all 512: one CTA per SM).
 constexpr int kTcFold = 16;
+// consumer-side barrier waits (A buffer free, stage full): a plain try_wait spin — the waits are short and a
+// suspended consumer wakes later than it could issue (+0.8 %, tools/estep_time.py); the producer and MMA warps keep
+// the suspend-time hint so their polling does not take issue slots from the consumers
+#ifndef LSG_CONSUMER_SLEEP
+#define LSG_CWAIT mbar_wait
+#else
+#define LSG_CWAIT mbar_wait_sleep
+#endif
 #ifndef LSG_TC_NWG
 #define LSG_TC_NWG 3
 #define LSG_TC_RB 2
@@ -580,7 +588,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         uint32_t av0[RB][16], av1[RB][16];
         tc_chunk_pairs<kLiteral, decltype(cheapc)::value, RB>(core, 2 * k, xa, xb, nk2, Lt, av0);
         tc_chunk_pairs<kLiteral, decltype(cheapc)::value, RB>(core, 2 * k + 1, xa, xb, nk2, Lt, av1);
-        mbar_wait_sleep(&aempty[wg][0], PAR ^ 1u);   // the MMAs of the previous pair are complete
+        LSG_CWAIT(&aempty[wg][0], PAR ^ 1u);   // the MMAs of the previous pair are complete
         tc_fence_after();
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) tmem_st16(tl + (uint32_t)(32 * RB + rb * 16), av0[rb]);
@@ -598,7 +606,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int64_t grp = 0, pend_g = 0;
     int tig = 0;
     for (int64_t it = 0; it < nunits; ++it) {
-        mbar_wait_sleep(&full_bar[it & 3], (uint32_t)((it >> 2) & 1));
+        LSG_CWAIT(&full_bar[it & 3], (uint32_t)((it >> 2) & 1));
         const float4* core = reinterpret_cast<const float4*>(&tiles_st[it & 3][0]);
         float2 Lt[RB];
 #pragma unroll

@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kBTThreads, 1)
         uint32_t av0[RB][16], av1[RB][16];
         tc_chunk_pairs<kLiteral, decltype(cheapc)::value, RB>(core, 2 * k, xa, xb, nk2, Lt, av0);
         tc_chunk_pairs<kLiteral, decltype(cheapc)::value, RB>(core, 2 * k + 1, xa, xb, nk2, Lt, av1);
-        mbar_wait_sleep(&aempty[wg][0], PAR ^ 1u);
+        LSG_CWAIT(&aempty[wg][0], PAR ^ 1u);
         tc_fence_after();
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) tmem_st16(tl + (uint32_t)(32 * RB + rb * 16), av0[rb]);
@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(kBTThreads, 1)
             load_points(cur_b, cur_j);
         }
         const int s = (int)(it & 3);
-        mbar_wait_sleep(&full_bar[s], (uint32_t)((it >> 2) & 1));
+        LSG_CWAIT(&full_bar[s], (uint32_t)((it >> 2) & 1));
         const float4* core = reinterpret_cast<const float4*>(&tiles_st[s][0]);
         float2 Lt[RB];
 #pragma unroll

@@ -269,14 +269,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
 // 1 TMA producer warp, 3 MMA warps.  TMEM per warpgroup: D 2 × 32 + A 2 × 32 columns; 384 of 512 used
 // (the CTA allocates all 512: one CTA per SM).
 constexpr int kTcFold = 16;
-// consumer-side barrier waits (A buffer free, stage full): a plain try_wait spin — the waits are short and a
-// suspended consumer wakes later than it could issue (+0.8 %, tools/estep_time.py); the producer and MMA warps keep
-// the suspend-time hint so their polling does not take issue slots from the consumers
-#ifndef LSG_CONSUMER_SLEEP
-#define LSG_CWAIT mbar_wait
-#else
-#define LSG_CWAIT mbar_wait_sleep
-#endif
 #ifndef LSG_TC_NWG
 #define LSG_TC_NWG 3
 #define LSG_TC_RB 2

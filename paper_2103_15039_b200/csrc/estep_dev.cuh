@@ -176,6 +176,14 @@ constexpr int kTcChunk = 8;                   // targets per A buffer (one K ste
 #define LSG_MAXNREG 160
 #define LSG_MAXNREG_LO 32
 #endif
+// consumer-side barrier waits (A buffer free, stage full): a plain try_wait spin — the waits are short and a
+// suspended consumer wakes later than it could issue (+0.8 %, tools/estep_time.py); the producer and MMA warps keep
+// the suspend-time hint so their polling does not take issue slots from the consumers
+#ifndef LSG_CONSUMER_SLEEP
+#define LSG_CWAIT mbar_wait
+#else
+#define LSG_CWAIT mbar_wait_sleep
+#endif
 #define LSG_PRAGMA(x) _Pragma(#x)
 #define LSG_UNROLL(n) LSG_PRAGMA(unroll n)
 #ifndef LSG_DRAIN_LAG

@@ -2,6 +2,7 @@
 // τ, e, ex2, Σpτ, TF32 split of p) over broadcast shared-memory targets, no TMEM / MMA / barriers.
 // Reports pairs per clock per SM for several warp counts and points per thread: the ceiling the
 // E-step consumer code can reach on this SM.
+// MODE 3: tile-centred residual (13 lane-ops); MODE 4: expanded residual (11 lane-ops).
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pairloop pairloop.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -14,8 +15,9 @@ constexpr int kReps = 64;
 
 template <int RB, int MODE>
 __global__ void pairloop(const float4* __restrict__ gt, float* out, long long* cyc, float k2) {
-    __shared__ float4 core[kTgt / 2 * 4];
-    for (int i = threadIdx.x; i < kTgt / 2 * 4; i += blockDim.x) core[i] = gt[i];
+    constexpr int kS = MODE == 4 ? 5 : 4;   // float4 per target pair (mode 4: + |y'|², -ñ·y')
+    __shared__ float4 core[kTgt / 2 * 5];
+    for (int i = threadIdx.x; i < kTgt / 2 * kS; i += blockDim.x) core[i] = gt[i];
     __syncthreads();
     float h[RB][3], l[RB][3];
     for (int rb = 0; rb < RB; ++rb)
@@ -28,9 +30,27 @@ __global__ void pairloop(const float4* __restrict__ gt, float* out, long long* c
     for (int rep = 0; rep < kReps; ++rep) {
 #pragma unroll 4
         for (int pr = 0; pr < kTgt / 2; ++pr) {
-            const float4 v0 = core[4 * pr], v1 = core[4 * pr + 1], v2 = core[4 * pr + 2], v3 = core[4 * pr + 3];
+            const float4 v0 = core[kS * pr], v1 = core[kS * pr + 1], v2 = core[kS * pr + 2], v3 = core[kS * pr + 3];
 #pragma unroll
             for (int rb = 0; rb < RB; ++rb) {
+                if (MODE == 4) {   // expanded residual: τ = |x'|² + |y'|² - 2x'·y' + (ñ·x' - ñ·y')², 11 lane-ops
+                    const float4 v4 = core[kS * pr + 4];
+                    float2 s2 = __fadd2_rn(bc(l[rb][0]), make_float2(v4.x, v4.y));
+                    s2 = __ffma2_rn(bc(-2.f * h[rb][0]), make_float2(v0.x, v0.y), s2);
+                    s2 = __ffma2_rn(bc(-2.f * h[rb][1]), make_float2(v0.z, v0.w), s2);
+                    s2 = __ffma2_rn(bc(-2.f * h[rb][2]), make_float2(v1.x, v1.y), s2);
+                    float2 qv = __ffma2_rn(bc(h[rb][0]), make_float2(v2.x, v2.y), make_float2(v4.z, v4.w));
+                    qv = __ffma2_rn(bc(h[rb][1]), make_float2(v2.z, v2.w), qv);
+                    qv = __ffma2_rn(bc(h[rb][2]), make_float2(v3.x, v3.y), qv);
+                    const float2 tau = __ffma2_rn(qv, qv, s2);
+                    const float2 e = __ffma2_rn(nk2, tau, make_float2(v1.z, v1.w));
+                    const float2 p = make_float2(ex2a(e.x), ex2a(e.y));
+                    Lt[rb] = __ffma2_rn(p, tau, Lt[rb]);
+                    const unsigned hx = __float_as_uint(p.x) & 0xFFFFE000u, hy = __float_as_uint(p.y) & 0xFFFFE000u;
+                    const float2 lo = __fadd2_rn(p, make_float2(-__uint_as_float(hx), -__uint_as_float(hy)));
+                    sink ^= hx ^ hy ^ __float_as_uint(lo.x) ^ __float_as_uint(lo.y);
+                    continue;
+                }
                 const float2 rx = MODE == 3 ? __fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y))
                                             : __fadd2_rn(__fadd2_rn(bc(h[rb][0]), make_float2(-v0.x, -v0.y)), bc(l[rb][0]));
                 const float2 ry = MODE == 3 ? __fadd2_rn(bc(h[rb][1]), make_float2(-v0.z, -v0.w))
@@ -143,11 +163,11 @@ int main() {
     int nsm;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     float4* gt; float* out; long long* cyc;
-    cudaMalloc(&gt, kTgt / 2 * 4 * sizeof(float4));
+    cudaMalloc(&gt, kTgt / 2 * 5 * sizeof(float4));
     cudaMalloc(&out, 1024 * 1024 * sizeof(float));
     cudaMalloc(&cyc, 1024 * sizeof(long long));
-    float4 hbuf[kTgt / 2 * 4];
-    for (int i = 0; i < kTgt / 2 * 4; ++i) hbuf[i] = make_float4(0.013f * (i % 17), 0.011f * (i % 13), -0.5f, 0.3f);
+    float4 hbuf[kTgt / 2 * 5];
+    for (int i = 0; i < kTgt / 2 * 5; ++i) hbuf[i] = make_float4(0.013f * (i % 17), 0.011f * (i % 13), -0.5f, 0.3f);
     cudaMemcpy(gt, hbuf, sizeof(hbuf), cudaMemcpyHostToDevice);
     for (int w : {8, 12, 16, 24, 32}) run<2, 0>(w, gt, out, cyc, nsm);
     for (int w : {12, 16, 24}) run<1, 0>(w, gt, out, cyc, nsm);
@@ -160,5 +180,9 @@ int main() {
     for (int w : {8, 12, 16, 20, 24, 32}) run<2, 3>(w, gt, out, cyc, nsm);
     for (int w : {12, 16, 24, 32}) run<1, 3>(w, gt, out, cyc, nsm);
     for (int w : {8, 12, 16}) run<4, 3>(w, gt, out, cyc, nsm);
+    // the expanded residual on very compact tiles (11 FP32 lane-ops per pair + ex2 + TF32 split)
+    for (int w : {8, 12, 16, 24, 32}) run<2, 4>(w, gt, out, cyc, nsm);
+    for (int w : {12, 16, 24}) run<1, 4>(w, gt, out, cyc, nsm);
+    for (int w : {8, 12}) run<4, 4>(w, gt, out, cyc, nsm);
     return 0;
 }

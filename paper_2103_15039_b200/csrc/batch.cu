@@ -293,8 +293,14 @@ __global__ void __launch_bounds__((kBNCW + 1) * 32, kBMinB)
 constexpr int kBTNWG = 3, kBTRB = 2, kBTMW = 3, kBTNT = 4;
 constexpr int kBTNCW = 4 * kBTNWG;
 constexpr int kBTThreads = (kBTNCW + 1 + kBTMW) * 32;
-// register split (setmaxnreg): the producer / MMA warps walk the problem list (BatchCursor) and keep 72
-constexpr int kBTRegHi = LSG_MAXNREG > 0 ? 144 : 0, kBTRegLo = 72;
+// register split (setmaxnreg): the producer / MMA warps walk the problem list (BatchCursor) with 48 registers
+// (a few spills outside their waits), each consumer thread gets 152 (tools/batch_speed.py: 144/72 → 152/48
+// +1.5 %, 160/32 +1.3 %; gpurun_out/r04f)
+#ifndef LSG_BT_REG_HI
+#define LSG_BT_REG_HI 152
+#define LSG_BT_REG_LO 48
+#endif
+constexpr int kBTRegHi = LSG_MAXNREG > 0 ? LSG_BT_REG_HI : 0, kBTRegLo = LSG_BT_REG_LO;
 static_assert(kBTRegHi == 0 || (kBTThreads == 512 && 384 * kBTRegHi + 128 * kBTRegLo <= 65536),
               "register split: 3 consumer warpgroups + warpgroup 3");
 constexpr int kBTWGCols = 64 * kBTRB;

@@ -33,8 +33,7 @@ constexpr int kFineRings = LSG_KNN_RMAX;        // fine rings searched before th
 
 // ---- reductions over the raw cloud -------------------------------------------------------------
 // stats1: [max(-x), max(-y), max(-z), max x, max y, max z, Σx, Σy, Σz]
-__global__ void __launch_bounds__(kRedThreads)
-    cloud_stats_kernel(const float* __restrict__ xyz, int64_t M, double* blockpart, double* out, unsigned* counter) {
+__device__ __forceinline__ void cloud_stats_body(const float* __restrict__ xyz, int64_t M, double* blockpart, double* out, unsigned* counter) {
     double v[12] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
@@ -47,6 +46,10 @@ __global__ void __launch_bounds__(kRedThreads)
         }
     }
     block_reduce_store<12, 6, kRedThreads>(v, blockpart, out, counter);
+}
+__global__ void __launch_bounds__(kRedThreads)
+    cloud_stats_kernel(const float* __restrict__ xyz, int64_t M, double* blockpart, double* out, unsigned* counter) {
+    cloud_stats_body(xyz, M, blockpart, out, counter);
 }
 
 // The model of target m as packed: y, the unit normal n = n_in/|n_in| and α.  A zero or non-finite normal
@@ -67,8 +70,7 @@ __device__ __forceinline__ double model_of(const float* __restrict__ nrm, const 
 }
 
 // stats2 (after the model is built): [max ω, Σ α, Σ ||y - ȳ||², Σ nn-distance, n_degenerate, Σ √(1+α)]
-__global__ void __launch_bounds__(kRedThreads)
-    model_stats_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm, const float* __restrict__ alpha,
+__device__ __forceinline__ void model_stats_body(const float* __restrict__ xyz, const float* __restrict__ nrm, const float* __restrict__ alpha,
                        const float* __restrict__ nnd, const int* __restrict__ degen, int64_t M,
                        const double* __restrict__ stats1, double* blockpart, double* out, unsigned* counter) {
     double v[6] = {-INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -89,10 +91,16 @@ __global__ void __launch_bounds__(kRedThreads)
     }
     block_reduce_store<6, 1, kRedThreads>(v, blockpart, out, counter);
 }
+__global__ void __launch_bounds__(kRedThreads)
+    model_stats_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm, const float* __restrict__ alpha,
+                       const float* __restrict__ nnd, const int* __restrict__ degen, int64_t M,
+                       const double* __restrict__ stats1, double* blockpart, double* out, unsigned* counter) {
+    model_stats_body(xyz, nrm, alpha, nnd, degen, M, stats1, blockpart, out, counter);
+}
 
 // Header: AABB, centroid, V (margin per side; a zero-extent axis is floored at the mean
 // nearest-neighbour spacing when known, else at sqrt(area/M) of the other two axes), extent.
-__global__ void header_kernel(TargetHeader* hdr, int64_t M, const double* stats1, const double* stats2,
+__device__ __forceinline__ void header_body(TargetHeader* hdr, int64_t M, const double* stats1, const double* stats2,
                               double margin, int have_nn) {
     TargetHeader h;
     h.M = M;
@@ -132,6 +140,10 @@ __global__ void header_kernel(TargetHeader* hdr, int64_t M, const double* stats1
     uint32_t* tail = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(hdr) + sizeof(TargetHeader));
     for (size_t i = 0; i < (kHeaderBytes - sizeof(TargetHeader)) / 4; ++i) tail[i] = 0u;
 }
+__global__ void header_kernel(TargetHeader* hdr, int64_t M, const double* stats1, const double* stats2,
+                              double margin, int have_nn) {
+    header_body(hdr, M, stats1, stats2, margin, have_nn);
+}
 
 // ---- slot order: a Morton (Z-order) curve over the AABB ----------------------------------------------
 // 21 bits per axis of the AABB's enclosing cube; ties (one cell) keep the input order (stable radix sort).
@@ -144,7 +156,7 @@ __device__ __forceinline__ uint64_t morton_spread(uint64_t x) {
     x = (x | (x << 2)) & 0x1249249249249249ull;
     return x;
 }
-__global__ void morton_keys_kernel(const float* __restrict__ xyz, int64_t M, const double* __restrict__ stats1,
+__device__ __forceinline__ void morton_keys_body(const float* __restrict__ xyz, int64_t M, const double* __restrict__ stats1,
                                    uint64_t* __restrict__ keys, int* __restrict__ ids) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M) return;
@@ -161,15 +173,22 @@ __global__ void morton_keys_kernel(const float* __restrict__ xyz, int64_t M, con
     keys[m] = k;
     ids[m] = (int)m;
 }
+__global__ void morton_keys_kernel(const float* __restrict__ xyz, int64_t M, const double* __restrict__ stats1,
+                                   uint64_t* __restrict__ keys, int* __restrict__ ids) {
+    morton_keys_body(xyz, M, stats1, keys, ids);
+}
 // slot_of[perm[s]] = s (the inverse permutation, kept in the target for lsgcpd_target_set_prior)
-__global__ void slot_inverse_kernel(const int* __restrict__ perm, int64_t M, int64_t M_pad, int32_t* __restrict__ slot_of) {
+__device__ __forceinline__ void slot_inverse_body(const int* __restrict__ perm, int64_t M, int64_t M_pad, int32_t* __restrict__ slot_of) {
     const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s < M) slot_of[perm[s]] = (int32_t)s;
     else if (s < M_pad) slot_of[s] = -1;
 }
+__global__ void slot_inverse_kernel(const int* __restrict__ perm, int64_t M, int64_t M_pad, int32_t* __restrict__ slot_of) {
+    slot_inverse_body(perm, M, M_pad, slot_of);
+}
 
 // Packed per-target record in slot order (FP64 arithmetic, FP32 storage); padding targets contribute nothing.
-__global__ void pack_body_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm,
+__device__ __forceinline__ void pack_record_body(const float* __restrict__ xyz, const float* __restrict__ nrm,
                                  const float* __restrict__ alpha, const int* __restrict__ perm, int64_t M,
                                  int64_t M_pad, const double* __restrict__ stats2, float* __restrict__ body) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // slot
@@ -199,6 +218,11 @@ __global__ void pack_body_kernel(const float* __restrict__ xyz, const float* __r
 #pragma unroll
     for (int i = 0; i < kTgtFloats; ++i) o[2 * i] = f[i];
 }
+__global__ void pack_body_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm,
+                                 const float* __restrict__ alpha, const int* __restrict__ perm, int64_t M,
+                                 int64_t M_pad, const double* __restrict__ stats2, float* __restrict__ body) {
+    pack_record_body(xyz, nrm, alpha, perm, M, M_pad, stats2, body);
+}
 
 // Tensor-core section: core fields (tile-centred) and the hi/lo TF32 feature blocks (see common.cuh).
 __device__ __forceinline__ float tf32_rna(float x) {
@@ -215,8 +239,7 @@ __device__ __forceinline__ bool exact_diff_f32(float y, float c) {
     return err == 0.0 && (double)(float)s == s;
 }
 // One CTA of kTcTile threads per tile, one thread per slot.
-__global__ void __launch_bounds__(kTcTile)
-    pack_tc_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm, const float* __restrict__ alpha,
+__device__ __forceinline__ void pack_tc_body(const float* __restrict__ xyz, const float* __restrict__ nrm, const float* __restrict__ alpha,
                    const int* __restrict__ perm, int64_t M, const double* __restrict__ stats2, float* __restrict__ tc) {
     __shared__ float s_lo[3][kTcTile], s_hi[3][kTcTile];
     __shared__ int s_bad[3];
@@ -308,6 +331,11 @@ __global__ void __launch_bounds__(kTcTile)
         *reinterpret_cast<float*>(base + off + 512) = tf32_rna(F[f] - hi);
     }
 }
+__global__ void __launch_bounds__(kTcTile)
+    pack_tc_kernel(const float* __restrict__ xyz, const float* __restrict__ nrm, const float* __restrict__ alpha,
+                   const int* __restrict__ perm, int64_t M, const double* __restrict__ stats2, float* __restrict__ tc) {
+    pack_tc_body(xyz, nrm, alpha, perm, M, stats2, tc);
+}
 
 // ---- grid kNN ------------------------------------------------------------------------------------
 struct Grid {
@@ -321,7 +349,7 @@ __device__ __forceinline__ int cell_coord(double p, double lo, double h, int dim
     return c < 0 ? 0 : (c >= dim ? dim - 1 : c);
 }
 
-__global__ void cell_keys_kernel(const float* __restrict__ xyz, int64_t M, Grid g, int* keys, int* ids) {
+__device__ __forceinline__ void cell_keys_body(const float* __restrict__ xyz, int64_t M, Grid g, int* keys, int* ids) {
     const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= M) return;
     const int cx = cell_coord(xyz[3 * m], g.lo[0], g.h, g.dim[0]);
@@ -330,22 +358,32 @@ __global__ void cell_keys_kernel(const float* __restrict__ xyz, int64_t M, Grid 
     keys[m] = (cx * g.dim[1] + cy) * g.dim[2] + cz;
     ids[m] = (int)m;
 }
+__global__ void cell_keys_kernel(const float* __restrict__ xyz, int64_t M, Grid g, int* keys, int* ids) {
+    cell_keys_body(xyz, M, g, keys, ids);
+}
 
 // A grid's points in its cell order, padded to 16 B: the searches read a cell's points contiguously.
-__global__ void gather_pts_kernel(const float* __restrict__ xyz, const int* __restrict__ sids, int64_t M,
+__device__ __forceinline__ void gather_pts_body(const float* __restrict__ xyz, const int* __restrict__ sids, int64_t M,
                                   float4* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= M) return;
     const int64_t j = sids[i];
     out[i] = make_float4(xyz[3 * j], xyz[3 * j + 1], xyz[3 * j + 2], 0.f);
 }
+__global__ void gather_pts_kernel(const float* __restrict__ xyz, const int* __restrict__ sids, int64_t M,
+                                  float4* __restrict__ out) {
+    gather_pts_body(xyz, sids, M, out);
+}
 
-__global__ void cell_ranges_kernel(const int* __restrict__ skeys, int64_t M, int* cstart, int* cend) {
+__device__ __forceinline__ void cell_ranges_body(const int* __restrict__ skeys, int64_t M, int* cstart, int* cend) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= M) return;
     const int k = skeys[i];
     if (i == 0 || skeys[i - 1] != k) cstart[k] = (int)i;
     if (i == M - 1 || skeys[i + 1] != k) cend[k] = (int)i + 1;
+}
+__global__ void cell_ranges_kernel(const int* __restrict__ skeys, int64_t M, int* cstart, int* cend) {
+    cell_ranges_body(skeys, M, cstart, cend);
 }
 
 // One thread per target point: exact k nearest (self included), ties → lower id, by ring search
@@ -522,8 +560,7 @@ __device__ __noinline__ void finish_point(const float* __restrict__ xyz, int64_t
 // order, giving up on the first two after kFineRings rings; points in sparse regions (isolated outliers, far
 // LiDAR returns) thus end on the coarse grid instead of scanning O(r³) fine cells.  Every search is exact,
 // so the result does not depend on which one finished.
-__global__ void __launch_bounds__(128)
-    knn_surface_kernel(const float* __restrict__ xyz, int64_t M, Grid g, const int* __restrict__ sids,
+__device__ __forceinline__ void knn_surface_body(const float* __restrict__ xyz, int64_t M, Grid g, const int* __restrict__ sids,
                        const int* __restrict__ cstart, const int* __restrict__ cend, Grid gc,
                        const int* __restrict__ sids_c, const int* __restrict__ cstart_c,
                        const int* __restrict__ cend_c, Grid gb, const int* __restrict__ sids_b,
@@ -549,6 +586,19 @@ __global__ void __launch_bounds__(128)
     }
     finish_point(xyz, m, bd, bi, k, alpha_max, lambda, nrm_out, kappa_out, alpha_out, knn_out, nnd_out, degen_out);
 }
+__global__ void __launch_bounds__(128)
+    knn_surface_kernel(const float* __restrict__ xyz, int64_t M, Grid g, const int* __restrict__ sids,
+                       const int* __restrict__ cstart, const int* __restrict__ cend, Grid gc,
+                       const int* __restrict__ sids_c, const int* __restrict__ cstart_c,
+                       const int* __restrict__ cend_c, Grid gb, const int* __restrict__ sids_b,
+                       const int* __restrict__ cstart_b, const int* __restrict__ cend_b, int use_bulk, int k,
+                       float alpha_max, float lambda,
+                       float* __restrict__ nrm_out, float* __restrict__ kappa_out, float* __restrict__ alpha_out,
+                       int* __restrict__ knn_out, float* __restrict__ nnd_out, int* __restrict__ degen_out,
+                       int* __restrict__ hard, int* __restrict__ nhard, const float4* __restrict__ pts_f,
+                       const float4* __restrict__ pts_b) {
+    knn_surface_body(xyz, M, g, sids, cstart, cend, gc, sids_c, cstart_c, cend_c, gb, sids_b, cstart_b, cend_b, use_bulk, k, alpha_max, lambda, nrm_out, kappa_out, alpha_out, knn_out, nnd_out, degen_out, hard, nhard, pts_f, pts_b);
+}
 
 // The points whose search left the first two grids (isolated outliers, far returns): one warp per point on the
 // coarse grid.  Ring by ring, the lanes split the shell's points (cell by cell, each cell's points strided over
@@ -556,8 +606,7 @@ __global__ void __launch_bounds__(128)
 // the warp then merges the 32 lists (k rounds of a warp-wide lexicographic minimum) into the ring's k best,
 // whose k-th distance prunes the next rings' cells and decides the stop exactly as ring_search does.  Lane 0
 // finishes the point.  Same result as the one-thread search (exact k nearest, ties → lower id).
-__global__ void __launch_bounds__(128)
-    knn_hard_kernel(const float* __restrict__ xyz, Grid g, const int* __restrict__ sids, const int* __restrict__ cstart,
+__device__ __forceinline__ void knn_hard_body(const float* __restrict__ xyz, Grid g, const int* __restrict__ sids, const int* __restrict__ cstart,
                     const int* __restrict__ cend, int k, float alpha_max, float lambda, float* __restrict__ nrm_out,
                     float* __restrict__ kappa_out, float* __restrict__ alpha_out, int* __restrict__ knn_out,
                     float* __restrict__ nnd_out, int* __restrict__ degen_out, const int* __restrict__ hard,
@@ -686,6 +735,14 @@ __global__ void __launch_bounds__(128)
         }
         __syncwarp();
     }
+}
+__global__ void __launch_bounds__(128)
+    knn_hard_kernel(const float* __restrict__ xyz, Grid g, const int* __restrict__ sids, const int* __restrict__ cstart,
+                    const int* __restrict__ cend, int k, float alpha_max, float lambda, float* __restrict__ nrm_out,
+                    float* __restrict__ kappa_out, float* __restrict__ alpha_out, int* __restrict__ knn_out,
+                    float* __restrict__ nnd_out, int* __restrict__ degen_out, const int* __restrict__ hard,
+                    const int* __restrict__ nhard, const float4* __restrict__ pts) {
+    knn_hard_body(xyz, g, sids, cstart, cend, k, alpha_max, lambda, nrm_out, kappa_out, alpha_out, knn_out, nnd_out, degen_out, hard, nhard, pts);
 }
 
 // ---- host side -------------------------------------------------------------------------------------
@@ -847,11 +904,15 @@ int pack_target_impl(const float* d_xyz, const float* d_nrm, const float* d_alph
 
 // kNN grids, sorts, the searches, the surface fit and the packed model of one target, from its cloud statistics
 // s1 (host copy) and st1 (device copy).  Async: no host synchronisation.
-static int prep_build(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p, const double* s1, const double* st1,
-                      void* d_target, char* ws, const PrepLayout& L, const lsgcpd_annotations* ann,
-                      cudaStream_t stream) {
+// The three kNN grids of a target from its cloud statistics s1 (host copy), and the host checks.
+struct GridPlan {
+    Grid g, gc, gb;
+    int use_bulk;
+    int64_t ncells, ncells_c, ncells_b;
+};
+static int plan_grids(const double* s1, int64_t M, GridPlan& P) {
     // grid: cell size from the AABB volume per point (≈ 1 point per cell for a volume-filling cloud)
-    Grid g;
+    Grid& g = P.g;
     double ext[3], ext_b[3], maxe = 0.0;
     for (int a = 0; a < 3; ++a) {
         g.lo[a] = -s1[a];
@@ -878,7 +939,8 @@ static int prep_build(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p
     // clamped into its border cells, which keeps every search exact).  Used first when that box is under a
     // quarter of the AABB volume — a cloud whose AABB is inflated by sparse outliers (the LiDAR config's
     // 100 m box), where AABB-sized cells would hold hundreds of the dense points.
-    Grid gb = g;
+    P.gb = g;
+    Grid& gb = P.gb;
     double vb = 1.0, va = 1.0;
     for (int a = 0; a < 3; ++a) {
         const double mean = s1[6 + a] / (double)M;
@@ -889,8 +951,8 @@ static int prep_build(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p
         vb *= ext_b[a];
         va *= fmax(ext[a], floor_e);
     }
-    const int use_bulk = (vb * 4.0 < va) ? 1 : 0;
-    if (use_bulk) {
+    P.use_bulk = (vb * 4.0 < va) ? 1 : 0;
+    if (P.use_bulk) {
         double hb = cbrt(vb / (double)M) / LSG_KNN_FINE;
         for (;;) {
             int64_t cells = 1;
@@ -903,6 +965,25 @@ static int prep_build(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p
         }
         gb.h = hb;
     }
+    P.gc = g;
+    P.gc.h = g.h * kCoarse;
+    for (int a = 0; a < 3; ++a) P.gc.dim[a] = (g.dim[a] + kCoarse - 1) / kCoarse;
+    P.ncells = (int64_t)g.dim[0] * g.dim[1] * g.dim[2];
+    P.ncells_c = (int64_t)P.gc.dim[0] * P.gc.dim[1] * P.gc.dim[2];
+    P.ncells_b = P.use_bulk ? (int64_t)gb.dim[0] * gb.dim[1] * gb.dim[2] : 0;
+    LSG_CHECK(P.ncells_c <= cell_cap_coarse(M), LSGCPD_EINVAL, "coarse grid too large (%lld cells)",
+              (long long)P.ncells_c);
+    return 0;
+}
+
+static int prep_build(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p, const double* s1, const double* st1,
+                      void* d_target, char* ws, const PrepLayout& L, const lsgcpd_annotations* ann,
+                      cudaStream_t stream) {
+    GridPlan P;
+    const int prc = plan_grids(s1, M, P);
+    if (prc) return prc;
+    const Grid &g = P.g, &gc = P.gc, &gb = P.gb;
+    const int use_bulk = P.use_bulk;
     int* keys = reinterpret_cast<int*>(ws + L.keys);
     int* ids = reinterpret_cast<int*>(ws + L.ids);
     int* skeys = reinterpret_cast<int*>(ws + L.skeys);
@@ -920,9 +1001,6 @@ static int prep_build(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p
     float4* pts_f = reinterpret_cast<float4*>(ws + L.pts_f);
     gather_pts_kernel<<<nb, 256, 0, stream>>>(d_xyz, sids, M, pts_f);
     // the coarse grid (keys and ids scratch reused: the fine sort has consumed them)
-    Grid gc = g;
-    gc.h = g.h * kCoarse;
-    for (int a = 0; a < 3; ++a) gc.dim[a] = (g.dim[a] + kCoarse - 1) / kCoarse;
     int* skeys_c = reinterpret_cast<int*>(ws + L.skeys_c);
     int* sids_c = reinterpret_cast<int*>(ws + L.sids_c);
     int* cstart_c = reinterpret_cast<int*>(ws + L.cstart_c);
@@ -931,8 +1009,7 @@ static int prep_build(const float* d_xyz, int64_t M, const lsgcpd_prep_params& p
     cub_bytes = L.cub_bytes;
     LSG_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.cub_tmp, cub_bytes, keys, skeys_c, ids, sids_c, (int)M, 0, 22,
                                              stream));
-    const int64_t ncells_c = (int64_t)gc.dim[0] * gc.dim[1] * gc.dim[2];
-    LSG_CHECK(ncells_c <= cell_cap_coarse(M), LSGCPD_EINVAL, "coarse grid too large (%lld cells)", (long long)ncells_c);
+    const int64_t ncells_c = P.ncells_c;
     LSG_CUDA(cudaMemsetAsync(cstart_c, 0xff, sizeof(int) * ncells_c, stream));
     LSG_CUDA(cudaMemsetAsync(cend_c, 0xff, sizeof(int) * ncells_c, stream));
     cell_ranges_kernel<<<nb, 256, 0, stream>>>(skeys_c, M, cstart_c, cend_c);
@@ -994,67 +1071,312 @@ int prepare_target_impl(const float* d_xyz, int64_t M, const lsgcpd_prep_params&
     return info_from_header(h, M, true, info);
 }
 
-// B targets in one call (NEXT-3 workloads): every cloud's statistics, one host synchronisation, then every
-// target's grids, searches and packing on kPrepStreams streams (each with a workspace region sized for the
-// largest cloud), then one copy of all headers.  Two host synchronisations instead of two per target, and the
-// small targets' kernel chains overlap.
-constexpr int kPrepStreams = 8;   // concurrent target builds in lsgcpd_prepare_batch
-size_t prepare_batch_ws_bytes(const int64_t* M, int B) {
+// ---- lsgcpd_prepare_batch (NEXT-3 workloads): every stage launched once per wave of targets ------------
+// The per-target chain above is ~35 launches and memsets; for hundreds of small clouds the host launch rate, not
+// the GPU, set the time (550 clouds of 3,500 points: 70 ms, tools/prep_batch_time.py).  Here every stage runs
+// once per wave of targets, blockIdx.y = the target within the wave, through the same device
+// bodies with the same block decomposition per target (gridDim.x, blockIdx.x and thread roles unchanged), and the
+// radix sorts become segmented sorts of the wave's concatenated keys (stable: the same permutations).  So each
+// target is built byte for byte as lsgcpd_prepare_target builds it (tests/test_gpu_prepare.py).  A wave holds up
+// to 64 targets (wave_size), each with a job region of the largest cloud's PrepLayout.
+struct PrepJob {
+    const float* xyz;
+    int64_t M, M_pad;
+    Grid g, gc, gb;
+    int use_bulk;
+    int64_t ncells, ncells_c, ncells_b;
+    int64_t off;               // first entry of this target in its wave's concatenated sort buffers
+    char* ws;                  // its workspace region (the PrepLayout of the largest cloud)
+    const double* st1;         // its cloud statistics (device)
+    TargetHeader* hdr;         // the target's sections
+    float* body;
+    float* tc;
+    int32_t* slots;
+};
+struct WaveBufs {              // concatenated over a wave's targets: wave_span entries each
+    int *kin, *vin;            // cell keys / point ids of the grid being built
+    int *ks[3], *vs[3];        // sorted (keys, ids) of the fine, coarse and bulk grids
+    uint64_t *mkin, *mkout;    // Morton keys
+    int *mvin, *mvout;         // Morton ids → slot permutation
+};
+// targets per wave: up to 64, their job regions within ~512 MB of workspace (a 3,500-point cloud's region is
+// ≈ 7.7 MB, dominated by the dense cell arrays), and a wave's sort buffers indexable by int
+static int wave_size(int64_t mmax) {
+    const size_t region = al(prep_layout(mmax, true).total);
+    int64_t P = (int64_t)((size_t)512 << 20) / (int64_t)region;
+    P = P < 1 ? 1 : (P > 64 ? 64 : P);
+    while (P > 1 && P * mmax >= ((int64_t)1 << 31)) --P;
+    return (int)P;
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+    cloud_stats_batch(const float* const* xyz, const int64_t* M, int b0, double* part, double* out, unsigned* ctr) {
+    const int b = b0 + blockIdx.y;
+    cloud_stats_body(xyz[b], M[b], part + (int64_t)b * kRedBlocks * 16, out + 16 * (int64_t)b, ctr + 4 * b);
+}
+// which: 0 fine, 1 coarse, 2 bulk grid
+__device__ __forceinline__ const Grid& job_grid(const PrepJob& j, int which) {
+    return which == 0 ? j.g : (which == 1 ? j.gc : j.gb);
+}
+__device__ __forceinline__ int* job_cstart(const PrepJob& j, const PrepLayout& L, int which) {
+    return reinterpret_cast<int*>(j.ws + (which == 0 ? L.cstart : (which == 1 ? L.cstart_c : L.cstart_b)));
+}
+__device__ __forceinline__ int* job_cend(const PrepJob& j, const PrepLayout& L, int which) {
+    return reinterpret_cast<int*>(j.ws + (which == 0 ? L.cend : (which == 1 ? L.cend_c : L.cend_b)));
+}
+__device__ __forceinline__ float4* job_pts(const PrepJob& j, const PrepLayout& L, int which) {
+    return reinterpret_cast<float4*>(j.ws + (which == 0 ? L.pts_f : (which == 1 ? L.pts_c : L.pts_b)));
+}
+__global__ void cell_keys_batch(const PrepJob* __restrict__ J, WaveBufs W, int which) {
+    const PrepJob& j = J[blockIdx.y];
+    if (which == 2 && !j.use_bulk) return;
+    cell_keys_body(j.xyz, j.M, job_grid(j, which), W.kin + j.off, W.vin + j.off);
+}
+// the dense cell arrays to -1 (the memset 0xff of the single-target chain); also clears the hard-point count and
+// the model-statistics counter of the job region (the single-target chain zeroes it before its cloud statistics;
+// block_reduce_store leaves it at 0 after each use)
+__global__ void fill_cells_batch(const PrepJob* __restrict__ J, PrepLayout L, int which) {
+    const PrepJob& j = J[blockIdx.y];
+    if (which == 2 && !j.use_bulk) return;
+    const int64_t n = which == 0 ? j.ncells : (which == 1 ? j.ncells_c : j.ncells_b);
+    int* cs = job_cstart(j, L, which);
+    int* ce = job_cend(j, L, which);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        cs[i] = -1;
+        ce[i] = -1;
+    }
+    if (which == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+        *reinterpret_cast<int*>(j.ws + L.hard) = 0;
+        *reinterpret_cast<unsigned*>(j.ws + L.counter) = 0u;
+    }
+}
+__global__ void cell_ranges_batch(const PrepJob* __restrict__ J, PrepLayout L, WaveBufs W, int which) {
+    const PrepJob& j = J[blockIdx.y];
+    if (which == 2 && !j.use_bulk) return;
+    cell_ranges_body(W.ks[which] + j.off, j.M, job_cstart(j, L, which), job_cend(j, L, which));
+}
+__global__ void gather_pts_batch(const PrepJob* __restrict__ J, PrepLayout L, WaveBufs W, int which) {
+    const PrepJob& j = J[blockIdx.y];
+    if (which == 2 && !j.use_bulk) return;
+    gather_pts_body(j.xyz, W.vs[which] + j.off, j.M, job_pts(j, L, which));
+}
+__global__ void __launch_bounds__(128)
+    knn_surface_batch(const PrepJob* __restrict__ J, PrepLayout L, WaveBufs W, int k, float alpha_max, float lambda) {
+    const PrepJob& j = J[blockIdx.y];
+    if ((int64_t)blockIdx.x * blockDim.x >= j.M) return;
+    char* ws = j.ws;
+    int* nhard = reinterpret_cast<int*>(ws + L.hard);
+    knn_surface_body(j.xyz, j.M, j.g, W.vs[0] + j.off, job_cstart(j, L, 0), job_cend(j, L, 0), j.gc,
+                     W.vs[1] + j.off, job_cstart(j, L, 1), job_cend(j, L, 1), j.gb, W.vs[2] + j.off,
+                     job_cstart(j, L, 2), job_cend(j, L, 2), j.use_bulk, k, alpha_max, lambda,
+                     reinterpret_cast<float*>(ws + L.nrm), reinterpret_cast<float*>(ws + L.kappa),
+                     reinterpret_cast<float*>(ws + L.alpha), nullptr, reinterpret_cast<float*>(ws + L.nnd),
+                     reinterpret_cast<int*>(ws + L.degen), nhard + 1, nhard, job_pts(j, L, 0), job_pts(j, L, 2));
+}
+__global__ void __launch_bounds__(128)
+    knn_hard_batch(const PrepJob* __restrict__ J, PrepLayout L, WaveBufs W, int k, float alpha_max, float lambda) {
+    const PrepJob& j = J[blockIdx.y];
+    char* ws = j.ws;
+    const int* nhard = reinterpret_cast<const int*>(ws + L.hard);
+    knn_hard_body(j.xyz, j.gc, W.vs[1] + j.off, job_cstart(j, L, 1), job_cend(j, L, 1), k, alpha_max, lambda,
+                  reinterpret_cast<float*>(ws + L.nrm), reinterpret_cast<float*>(ws + L.kappa),
+                  reinterpret_cast<float*>(ws + L.alpha), nullptr, reinterpret_cast<float*>(ws + L.nnd),
+                  reinterpret_cast<int*>(ws + L.degen), nhard + 1, nhard, job_pts(j, L, 1));
+}
+__global__ void __launch_bounds__(kRedThreads) model_stats_batch(const PrepJob* __restrict__ J, PrepLayout L) {
+    const PrepJob& j = J[blockIdx.y];
+    char* ws = j.ws;
+    model_stats_body(j.xyz, reinterpret_cast<const float*>(ws + L.nrm), reinterpret_cast<const float*>(ws + L.alpha),
+                     reinterpret_cast<const float*>(ws + L.nnd), reinterpret_cast<const int*>(ws + L.degen), j.M,
+                     j.st1, reinterpret_cast<double*>(ws + L.blockpart), reinterpret_cast<double*>(ws + L.stats2),
+                     reinterpret_cast<unsigned*>(ws + L.counter));
+}
+__global__ void header_batch(const PrepJob* __restrict__ J, PrepLayout L, double margin) {
+    const PrepJob& j = J[blockIdx.y];
+    header_body(j.hdr, j.M, j.st1, reinterpret_cast<const double*>(j.ws + L.stats2), margin, 1);
+}
+__global__ void morton_keys_batch(const PrepJob* __restrict__ J, WaveBufs W) {
+    const PrepJob& j = J[blockIdx.y];
+    morton_keys_body(j.xyz, j.M, j.st1, W.mkin + j.off, W.mvin + j.off);
+}
+__global__ void slot_inverse_batch(const PrepJob* __restrict__ J, WaveBufs W) {
+    const PrepJob& j = J[blockIdx.y];
+    slot_inverse_body(W.mvout + j.off, j.M, j.M_pad, j.slots);
+}
+__global__ void pack_record_batch(const PrepJob* __restrict__ J, PrepLayout L, WaveBufs W) {
+    const PrepJob& j = J[blockIdx.y];
+    pack_record_body(j.xyz, reinterpret_cast<const float*>(j.ws + L.nrm), reinterpret_cast<const float*>(j.ws + L.alpha),
+                     W.mvout + j.off, j.M, j.M_pad, reinterpret_cast<const double*>(j.ws + L.stats2), j.body);
+}
+__global__ void __launch_bounds__(kTcTile) pack_tc_batch(const PrepJob* __restrict__ J, PrepLayout L, WaveBufs W) {
+    const PrepJob& j = J[blockIdx.y];
+    if ((int64_t)blockIdx.x >= j.M_pad / kTcTile) return;   // the whole CTA: no thread reaches the body's barriers
+    pack_tc_body(j.xyz, reinterpret_cast<const float*>(j.ws + L.nrm), reinterpret_cast<const float*>(j.ws + L.alpha),
+                 W.mvout + j.off, j.M, reinterpret_cast<const double*>(j.ws + L.stats2), j.tc);
+}
+
+// Workspace of lsgcpd_prepare_batch: [stats B×16 | cloud partials B×kRedBlocks×16 | counters B×4 | jobs B |
+// segment offsets 3×B | cloud pointers + sizes B | wave sort buffers | cub temp | wave job regions]
+struct BatchWs {
+    size_t stats, part, ctr, jobs, seg, xyzp, msz, wave, cub, regions, total;
+    int P;
+    int64_t span;              // entries per wave sort buffer (P × largest cloud)
+    size_t cub_bytes;
+};
+static BatchWs batch_ws(const int64_t* M, int B) {
     int64_t mmax = 1;
     for (int b = 0; b < B; ++b) mmax = M[b] > mmax ? M[b] : mmax;
-    return (size_t)kPrepStreams * al(prep_layout(mmax, true).total) + al(sizeof(double) * 16 * (size_t)B);
+    BatchWs w;
+    w.P = wave_size(mmax);
+    if (w.P > B) w.P = B;
+    w.span = (int64_t)w.P * mmax;
+    size_t c1 = 0, c2 = 0;
+    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, c1, (const int*)nullptr, (int*)nullptr, (const int*)nullptr,
+                                             (int*)nullptr, (int)w.span, w.P, (const int*)nullptr, (const int*)nullptr,
+                                             0, 22);
+    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, c2, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                             (const int*)nullptr, (int*)nullptr, (int)w.span, w.P, (const int*)nullptr,
+                                             (const int*)nullptr, 0, 63);
+    w.cub_bytes = c1 > c2 ? c1 : c2;
+    size_t o = 0;
+    w.stats = o; o += al(sizeof(double) * 16 * (size_t)B);
+    w.part = o; o += al(sizeof(double) * kRedBlocks * 16 * (size_t)B);
+    w.ctr = o; o += al(sizeof(unsigned) * 4 * (size_t)B);
+    w.jobs = o; o += al(sizeof(PrepJob) * (size_t)B);
+    w.seg = o; o += al(sizeof(int) * 3 * (size_t)B);
+    w.xyzp = o; o += al(sizeof(float*) * (size_t)B);
+    w.msz = o; o += al(sizeof(int64_t) * (size_t)B);
+    w.wave = o; o += al((sizeof(int) * 8 + sizeof(uint64_t) * 2 + sizeof(int) * 2) * (size_t)w.span);
+    w.cub = o; o += al(w.cub_bytes);
+    w.regions = o; o += (size_t)w.P * al(prep_layout(mmax, true).total);
+    w.total = o;
+    return w;
 }
+size_t prepare_batch_ws_bytes(const int64_t* M, int B) { return batch_ws(M, B).total; }
 
 int prepare_batch_impl(const float* const* xyz, const int64_t* M, int B, const lsgcpd_prep_params& p,
                        void* const* targets, void* d_ws, lsgcpd_target_info* info, cudaStream_t stream) {
+    const BatchWs w = batch_ws(M, B);
     int64_t mmax = 1;
     for (int b = 0; b < B; ++b) mmax = M[b] > mmax ? M[b] : mmax;
     const PrepLayout L = prep_layout(mmax, true);
-    const int S = B < kPrepStreams ? B : kPrepStreams;
     char* ws = static_cast<char*>(d_ws);
-    double* stats = reinterpret_cast<double*>(ws + (size_t)kPrepStreams * al(L.total));   // [B][16]
-    double* bp = reinterpret_cast<double*>(ws + L.blockpart);
-    unsigned* ctr = reinterpret_cast<unsigned*>(ws + L.counter);
-    for (int r = 0; r < S; ++r)
-        LSG_CUDA(cudaMemsetAsync(ws + (size_t)r * al(L.total) + L.counter, 0, sizeof(unsigned) * 4, stream));
-    for (int b = 0; b < B; ++b)
-        cloud_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(xyz[b], M[b], bp, stats + 16 * (size_t)b, ctr);
+    double* stats = reinterpret_cast<double*>(ws + w.stats);
+    // 1. every cloud's statistics in one launch per 65,535 clouds; one host synchronisation
+    LSG_CUDA(cudaMemsetAsync(ws + w.ctr, 0, sizeof(unsigned) * 4 * (size_t)B, stream));
+    LSG_CUDA(cudaMemcpyAsync(ws + w.xyzp, xyz, sizeof(float*) * (size_t)B, cudaMemcpyHostToDevice, stream));
+    LSG_CUDA(cudaMemcpyAsync(ws + w.msz, M, sizeof(int64_t) * (size_t)B, cudaMemcpyHostToDevice, stream));
+    for (int b0 = 0; b0 < B; b0 += 65535) {
+        const int nb = B - b0 < 65535 ? B - b0 : 65535;
+        cloud_stats_batch<<<dim3(kRedBlocks, nb), kRedThreads, 0, stream>>>(
+            reinterpret_cast<const float* const*>(ws + w.xyzp), reinterpret_cast<const int64_t*>(ws + w.msz), b0,
+            reinterpret_cast<double*>(ws + w.part), stats, reinterpret_cast<unsigned*>(ws + w.ctr));
+    }
     std::vector<double> hs(16 * (size_t)B);
     LSG_CUDA(cudaMemcpyAsync(hs.data(), stats, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost, stream));
     LSG_CUDA(cudaStreamSynchronize(stream));
-    // the targets' builds are chains of small kernels: S streams, each with its own workspace region, overlap them
-    struct Streams {
-        std::vector<cudaStream_t> s;
-        std::vector<cudaEvent_t> e;
-        ~Streams() {
-            for (auto x : s)
-                if (x) cudaStreamDestroy(x);
-            for (auto x : e)
-                if (x) cudaEventDestroy(x);
-        }
-    } sub;
-    sub.s.assign(S, nullptr);
-    sub.e.assign(S, nullptr);
-    for (int r = 0; r < S; ++r) {
-        LSG_CUDA(cudaStreamCreateWithFlags(&sub.s[r], cudaStreamNonBlocking));
-        LSG_CUDA(cudaEventCreateWithFlags(&sub.e[r], cudaEventDisableTiming));
-    }
+    // 2. every target's grids (host checks, naming the problem), its wave slot and segment
+    std::vector<PrepJob> jobs(B);
+    std::vector<int> seg(3 * (size_t)B);   // [begin | end | end of the bulk segment (empty without a bulk grid)]
+    int64_t off = 0;
     for (int b = 0; b < B; ++b) {
-        const int r = b % S;
-        const int rc = prep_build(xyz[b], M[b], p, hs.data() + 16 * (size_t)b, stats + 16 * (size_t)b, targets[b],
-                                  ws + (size_t)r * al(L.total), L, nullptr, sub.s[r]);
+        GridPlan P;
+        const int rc = plan_grids(hs.data() + 16 * (size_t)b, M[b], P);
         if (rc) {
             char msg[1024];
             snprintf(msg, sizeof(msg), "problem %d: %s", b, lsgcpd_last_error());
-            for (int q = 0; q < S; ++q) cudaStreamSynchronize(sub.s[q]);
             set_error("%s", msg);
             return rc;
         }
+        if (b % w.P == 0) off = 0;
+        PrepJob& j = jobs[b];
+        j.xyz = xyz[b];
+        j.M = M[b];
+        j.M_pad = pad_targets(M[b]);
+        j.g = P.g;
+        j.gc = P.gc;
+        j.gb = P.gb;
+        j.use_bulk = P.use_bulk;
+        j.ncells = P.ncells;
+        j.ncells_c = P.ncells_c;
+        j.ncells_b = P.ncells_b;
+        j.off = off;
+        j.ws = ws + w.regions + (size_t)(b % w.P) * al(L.total);
+        j.st1 = stats + 16 * (size_t)b;
+        j.hdr = reinterpret_cast<TargetHeader*>(targets[b]);
+        j.body = target_body(targets[b]);
+        j.tc = target_tc(targets[b], j.M_pad);
+        j.slots = target_slots(targets[b], j.M_pad);
+        seg[b] = (int)off;
+        seg[B + b] = (int)(off + M[b]);
+        seg[2 * (size_t)B + b] = (int)(P.use_bulk ? off + M[b] : off);
+        off += M[b];
     }
-    for (int r = 0; r < S; ++r) {
-        LSG_CUDA(cudaEventRecord(sub.e[r], sub.s[r]));
-        LSG_CUDA(cudaStreamWaitEvent(stream, sub.e[r], 0));
+    PrepJob* d_jobs = reinterpret_cast<PrepJob*>(ws + w.jobs);
+    int* d_seg = reinterpret_cast<int*>(ws + w.seg);
+    LSG_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), sizeof(PrepJob) * (size_t)B, cudaMemcpyHostToDevice, stream));
+    LSG_CUDA(cudaMemcpyAsync(d_seg, seg.data(), sizeof(int) * seg.size(), cudaMemcpyHostToDevice, stream));
+    WaveBufs W;
+    {
+        char* q = ws + w.wave;
+        auto take = [&](size_t elem) { char* r = q; q += elem * (size_t)w.span; return r; };
+        W.kin = reinterpret_cast<int*>(take(sizeof(int)));
+        W.vin = reinterpret_cast<int*>(take(sizeof(int)));
+        for (int g = 0; g < 3; ++g) {
+            W.ks[g] = reinterpret_cast<int*>(take(sizeof(int)));
+            W.vs[g] = reinterpret_cast<int*>(take(sizeof(int)));
+        }
+        W.mkin = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t)));
+        W.mkout = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t)));
+        W.mvin = reinterpret_cast<int*>(take(sizeof(int)));
+        W.mvout = reinterpret_cast<int*>(take(sizeof(int)));
     }
+    // 3. the waves: every stage once per wave (stream order separates the waves' uses of the job regions)
+    for (int b0 = 0; b0 < B; b0 += w.P) {
+        const int n = B - b0 < w.P ? B - b0 : w.P;
+        const PrepJob* J = d_jobs + b0;
+        int64_t wm = 1, wspan = 0, wcells = 1, wpad = kTcTile;
+        for (int b = b0; b < b0 + n; ++b) {
+            wm = M[b] > wm ? M[b] : wm;
+            wspan += M[b];
+            wcells = jobs[b].ncells > wcells ? jobs[b].ncells : wcells;
+            wpad = jobs[b].M_pad > wpad ? jobs[b].M_pad : wpad;
+        }
+        const unsigned nb = (unsigned)((wm + 255) / 256);
+        const unsigned nfill = (unsigned)std::min<int64_t>((wcells + 255) / 256, 1024);
+        const int* beg = d_seg + b0;
+        const int* end = d_seg + B + b0;
+        const int* endb = d_seg + 2 * (size_t)B + b0;
+        for (int g = 0; g < 3; ++g) {
+            if (g == 2) {
+                bool any = false;
+                for (int b = b0; b < b0 + n; ++b) any = any || jobs[b].use_bulk;
+                if (!any) break;
+            }
+            cell_keys_batch<<<dim3(nb, n), 256, 0, stream>>>(J, W, g);
+            size_t cb = w.cub_bytes;
+            LSG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(ws + w.cub, cb, W.kin, W.ks[g], W.vin, W.vs[g], (int)wspan,
+                                                              n, beg, g == 2 ? endb : end, 0, 22, stream));
+            fill_cells_batch<<<dim3(nfill, n), 256, 0, stream>>>(J, L, g);
+            cell_ranges_batch<<<dim3(nb, n), 256, 0, stream>>>(J, L, W, g);
+            gather_pts_batch<<<dim3(nb, n), 256, 0, stream>>>(J, L, W, g);
+        }
+        knn_surface_batch<<<dim3((unsigned)((wm + 127) / 128), n), 128, 0, stream>>>(J, L, W, p.knn_k, p.alpha_max,
+                                                                                    p.lambda);
+        knn_hard_batch<<<dim3(8, n), 128, 0, stream>>>(J, L, W, p.knn_k, p.alpha_max, p.lambda);
+        model_stats_batch<<<dim3(kRedBlocks, n), kRedThreads, 0, stream>>>(J, L);
+        header_batch<<<dim3(1, n), 1, 0, stream>>>(J, L, p.volume_margin);
+        morton_keys_batch<<<dim3(nb, n), 256, 0, stream>>>(J, W);
+        size_t cb = w.cub_bytes;
+        LSG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(ws + w.cub, cb, W.mkin, W.mkout, W.mvin, W.mvout, (int)wspan,
+                                                          n, beg, end, 0, 63, stream));
+        const unsigned np = (unsigned)((wpad + 255) / 256);
+        slot_inverse_batch<<<dim3(np, n), 256, 0, stream>>>(J, W);
+        pack_record_batch<<<dim3(np, n), 256, 0, stream>>>(J, L, W);
+        pack_tc_batch<<<dim3((unsigned)(wpad / kTcTile), n), kTcTile, 0, stream>>>(J, L, W);
+        LSG_CUDA(cudaGetLastError());
+    }
+    // 4. every header, one host synchronisation
     std::vector<TargetHeader> hh(B);
     for (int b = 0; b < B; ++b)
         LSG_CUDA(cudaMemcpyAsync(&hh[b], targets[b], sizeof(TargetHeader), cudaMemcpyDeviceToHost, stream));

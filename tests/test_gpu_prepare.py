@@ -103,6 +103,9 @@ def test_prepare_batch_equals_single_prepares():
     clouds.append(np.concatenate([rng.normal(0, 0.02, (800, 3)), rng.uniform(-20, 20, (60, 3))]).astype(np.float32))
     clouds.append(workload("tiny").target)
     dev = [to_dev(c) for c in clouds]
+    import torch
+    junk = torch.full((256 << 20,), 0x5A, dtype=torch.uint8, device="cuda")   # the workspace is recycled, dirty
+    del junk
     batch = lsg.prepare_batch(dev, 10)
     for c, tb in zip(dev, batch):
         ts = lsg.prepare_target(c, 10)

@@ -7,13 +7,19 @@ import paper_2103_15039_b200 as lsg
 B = int(os.environ.get("B", "550")); n = int(os.environ.get("NPTS", "3500")); iters = int(os.environ.get("ITERS", "50"))
 wls = synth.make_batch(B, n)
 clouds = [torch.from_numpy(w.target).cuda() for w in wls]
-[lsg.prepare_target(c, w.knn_k) for c, w in zip(clouds, wls)]; lsg.prepare_batch(clouds, wls[0].knn_k)   # warm-up
+# each variant timed after a warm-up of itself, the previous variant's targets freed first (allocator state)
+tgts = [lsg.prepare_target(c, w.knn_k) for c, w in zip(clouds, wls)]
+del tgts
 torch.cuda.synchronize(); t0 = time.perf_counter()
 tgts = [lsg.prepare_target(c, w.knn_k) for c, w in zip(clouds, wls)]
+torch.cuda.synchronize(); t_each = time.perf_counter() - t0
+del tgts
+tgts = lsg.prepare_batch(clouds, wls[0].knn_k)
+del tgts
 torch.cuda.synchronize(); t1 = time.perf_counter()
 tgts = lsg.prepare_batch(clouds, wls[0].knn_k)
 torch.cuda.synchronize(); t2 = time.perf_counter()
-print(f"prepare {B} targets: {(t1 - t0) * 1e3:.1f} ms one call each, {(t2 - t1) * 1e3:.1f} ms in one lsgcpd_prepare_batch",
+print(f"prepare {B} targets: {t_each * 1e3:.1f} ms one call each, {(t2 - t1) * 1e3:.1f} ms in one lsgcpd_prepare_batch",
       flush=True)
 srcs = [torch.from_numpy(w.source).cuda() for w in wls]
 reg = lsg.BatchRegistrar(tgts, srcs, iters)

@@ -115,6 +115,24 @@ def test_prepare_batch_equals_single_prepares():
         lsg.prepare_batch([to_dev(np.zeros((2, 3), np.float32))], 10)
 
 
+def test_prepare_batch_several_waves_equal_single_prepares():
+    # more targets than one wave holds: 70 small clouds (waves of 64 + 6), and a batch whose largest cloud (the
+    # scale config's target) leaves room for only a few targets per wave; every target byte-identical to its
+    # lsgcpd_prepare_target build, the workspace dirty
+    import torch
+    import paper_2103_15039_b200 as lsg
+    import synth
+    small = [to_dev(w.target) for w in synth.make_batch(70, 600, seed=9, ragged=True)]
+    big = [to_dev(workload("scale").target)] + small[:7]
+    for clouds, check in ((small, [0, 1, 63, 64, 65, 69]), (big, list(range(8)))):
+        junk = torch.full((512 << 20,), 0xA5, dtype=torch.uint8, device="cuda")
+        del junk
+        batch = lsg.prepare_batch(clouds, 10)
+        for b in check:
+            ts = lsg.prepare_target(clouds[b], 10)
+            assert torch_equal(batch[b].buf, ts.buf), f"target {b} of {len(clouds)}"
+
+
 def torch_equal(a, b):
     import torch
     return bool(torch.equal(a, b))

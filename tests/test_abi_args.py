@@ -113,6 +113,18 @@ def test_prepare_register_and_model_extensions_refuse_bad_arguments(L):
     assert L.lsgcpd_depth_confidence(FAKE, 10, 0.0, 0.0, 0.4, FAKE, None) == EINVAL
 
 
+def test_prepare_batch_workspace_is_bounded(L):
+    # waves of up to 64 targets within ~512 MB of job regions: 550 paper-scale clouds stay under 1 GiB, and a
+    # batch holding a 2^29-point cloud gets one target per wave (no int overflow in the wave's sort offsets)
+    M = (ctypes.c_int64 * 550)(*([3500] * 550))
+    ws = L.lsgcpd_prepare_batch_workspace_bytes(M, 550, 10)
+    assert 0 < ws < (1 << 30)
+    M1 = (ctypes.c_int64 * 1)(3500)
+    assert L.lsgcpd_prepare_batch_workspace_bytes(M1, 1, 10) < ws   # one target: one job region
+    big = (ctypes.c_int64 * 2)(1 << 29, 5)
+    assert L.lsgcpd_prepare_batch_workspace_bytes(big, 2, 10) >= L.lsgcpd_prepare_workspace_bytes(1 << 29, 10)
+
+
 def test_prepare_batch_refuses_bad_arguments(L):
     M = (ctypes.c_int64 * 2)(100, 2)
     assert L.lsgcpd_prepare_batch_workspace_bytes(M, 2, 10) == 0          # a cloud with M < 3

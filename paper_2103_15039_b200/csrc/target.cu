@@ -3,6 +3,7 @@
 // the packed 64-B-per-target model the E step streams through TMA.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"

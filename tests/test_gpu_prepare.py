@@ -149,3 +149,7 @@ def test_prepare_batch_edge_cases():
     good = workload("tiny").target
     with pytest.raises(lsg.LsgcpdError, match="problem 1"):
         lsg.prepare_batch([to_dev(good), to_dev(np.ones((50, 3), np.float32))], 10)
+    # a degenerate cloud in the second wave (64 targets per wave): refused before any wave runs, named
+    clouds = [to_dev(good)] * 69 + [to_dev(np.ones((50, 3), np.float32))]
+    with pytest.raises(lsg.LsgcpdError, match="problem 69"):
+        lsg.prepare_batch(clouds, 10)

@@ -715,12 +715,12 @@ struct Variant {
 };
 #define LSG_VARIANT(P, W, B, X) \
     {P, W, B, X, {(const void*)estep_kernel<P, W, B, X, false>, (const void*)estep_kernel<P, W, B, X, true>}}
-static const Variant kVariants[] = {LSG_VARIANT(2, kTcNCW, 1, true), LSG_VARIANT(2, 8, 1, true),
+static const Variant kVariants[] = {LSG_VARIANT(kTcBlk / (kTcNCW * 32), kTcNCW, 1, true), LSG_VARIANT(2, 8, 1, true),
                                     LSG_VARIANT(2, 1, 8, true)};
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 constexpr int kBigVariant = 0, kMidVariant = 1, kSmallVariant = 2;
 constexpr int kMidBlk = 2 * 8 * 32;
-static_assert(2 * kTcNCW * 32 == kTcBlk, "the running-max partner of the tensor-core kernel uses its block size");
+static_assert(kTcBlk % (kTcNCW * 32) == 0, "the running-max partner of the tensor-core kernel uses its block size");
 constexpr int64_t kSplitBytes = 48ll << 20;   // tensor-core sections above this are swept in two halves
 
 // Per-device facts (SM count, occupancies) and one-time function attributes, set up once per device under a

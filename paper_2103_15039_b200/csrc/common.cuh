@@ -172,6 +172,23 @@ __device__ __forceinline__ double warp_max(double v) {
 // Deterministic grid reduction: entries [0, KMAX) by max, [KMAX, K) by sum.  Each block writes a
 // partial; the last block to finish (atomic ticket) combines the partials in block order and
 // writes `out`, then re-arms the counter.  blockDim.x must equal NT.
+// The last CTA's fold of the per-CTA partials p[0], p[stride], … p[(n-1)·stride] in CTA order (max or sum):
+// loaded 16 at a time from L2 (ld.global.cg, after the writers' __threadfence and the atomic ticket), then
+// combined in the same order as a plain loop — the same result, without n dependent L2 round trips.
+template <bool kMax>
+__device__ __forceinline__ double ordered_reduce_l2(const double* __restrict__ p, int64_t stride, unsigned n) {
+    double s = __ldcg(p);
+    for (unsigned b0 = 1; b0 < n; b0 += 16) {
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = (b0 + u < n) ? __ldcg(p + (int64_t)(b0 + u) * stride) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (b0 + u < n) s = kMax ? fmax(s, v[u]) : s + v[u];
+    }
+    return s;
+}
+
 template <int K, int KMAX, int NT>
 __device__ void block_reduce_store(double (&v)[K], double* blockpart, double* out, unsigned int* counter) {
     __shared__ double sm[NT / 32][K];
@@ -194,12 +211,9 @@ __device__ void block_reduce_store(double (&v)[K], double* blockpart, double* ou
     __syncthreads();
     if (last) {
         __threadfence();
-        for (int f = threadIdx.x; f < K; f += NT) {
-            const volatile double* bp = blockpart;
-            double s = bp[f];
-            for (unsigned b = 1; b < gridDim.x; ++b) s = f < KMAX ? fmax(s, bp[(int64_t)b * K + f]) : s + bp[(int64_t)b * K + f];
-            out[f] = s;
-        }
+        for (int f = threadIdx.x; f < K; f += NT)
+            out[f] = f < KMAX ? ordered_reduce_l2<true>(blockpart + f, K, gridDim.x)
+                              : ordered_reduce_l2<false>(blockpart + f, K, gridDim.x);
         if (threadIdx.x == 0) *counter = 0u;
     }
 }

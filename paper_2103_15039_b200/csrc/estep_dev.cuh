@@ -413,21 +413,33 @@ __device__ inline void merge_tile32(const float* __restrict__ part, int64_t N, i
     }
     double mustar = -INFINITY, a = 0.0;
     if (ok) {
-        for (int h = 0; h < sc.halves; ++h) {   // the segments of every half of the targets (Sched::halves)
-            const float* bh = blk + h * sc.hstride;
+        if (st->fixed) {
+            // fixed-max mode: every segment's max is 0 and so is the reference (max(0, min(L_o, 0)) = 0), every
+            // scale factor is 1 — the plain sum, as the general path computes it, without the pass over the maxima
+            mustar = 0.0;
+            if (f < kAcc)
+                for (int h = 0; h < sc.halves; ++h) {
+                    const float* bh = blk + h * sc.hstride;
 #pragma unroll 4
-            for (int k = 0; k < nk; ++k) mustar = fmax(mustar, (double)bh[(int64_t)k * kPartF * kB + 14 * kB]);
-        }
-        if (wn > 0.0) mustar = fmax(mustar, fmin(Lon, 0.0));
-        if (f < kAcc) {
-            for (int h = 0; h < sc.halves; ++h) {
+                    for (int k = 0; k < nk; ++k) a = fma(1.0, (double)bh[(int64_t)k * kPartF * kB + f * kB], a);
+                }
+        } else {
+            for (int h = 0; h < sc.halves; ++h) {   // the segments of every half of the targets (Sched::halves)
                 const float* bh = blk + h * sc.hstride;
 #pragma unroll 4
-                for (int k = 0; k < nk; ++k) {
-                    const float* base = bh + (int64_t)k * kPartF * kB;
-                    const double muk = (double)base[14 * kB];
-                    const double sc_k = (muk == mustar) ? 1.0 : exp2(muk - mustar);
-                    a = fma(sc_k, (double)base[f * kB], a);
+                for (int k = 0; k < nk; ++k) mustar = fmax(mustar, (double)bh[(int64_t)k * kPartF * kB + 14 * kB]);
+            }
+            if (wn > 0.0) mustar = fmax(mustar, fmin(Lon, 0.0));
+            if (f < kAcc) {
+                for (int h = 0; h < sc.halves; ++h) {
+                    const float* bh = blk + h * sc.hstride;
+#pragma unroll 4
+                    for (int k = 0; k < nk; ++k) {
+                        const float* base = bh + (int64_t)k * kPartF * kB;
+                        const double muk = (double)base[14 * kB];
+                        const double sc_k = (muk == mustar) ? 1.0 : exp2(muk - mustar);
+                        a = fma(sc_k, (double)base[f * kB], a);
+                    }
                 }
             }
         }

@@ -639,12 +639,7 @@ __global__ void __launch_bounds__(kTailThreads)
     __syncthreads();
     if (!last) return;
     __threadfence();
-    if (threadIdx.x < kMom) {
-        const volatile double* bp = blockpart;
-        double v = bp[threadIdx.x];
-        for (unsigned b = 1; b < gridDim.x; ++b) v += bp[(int64_t)b * kMom + threadIdx.x];
-        mom[threadIdx.x] = v;
-    }
+    if (threadIdx.x < kMom) mom[threadIdx.x] = ordered_reduce_l2<false>(blockpart + threadIdx.x, kMom, gridDim.x);
     if (threadIdx.x == 0) *counter = 0u;
     __syncthreads();
     if (run_newton && threadIdx.x < 32) {

@@ -119,11 +119,13 @@ int lsgcpd_prepare_target(const float* d_xyz, int64_t M, const lsgcpd_prep_param
                           lsgcpd_target_info* h_info, const lsgcpd_annotations* annotations,
                           lsgcpd_stream_t stream);
 
-/* B targets in one call (many small registrations, §8(f) NEXT-3): the same model as B calls of
+/* B targets in one call (many small registrations, §8(f) NEXT-3): byte for byte the targets of B calls of
  * lsgcpd_prepare_target (no annotations), with two host synchronisations in all instead of two per
- * target.  h_d_xyz[b] / h_d_target[b]: HOST arrays of B DEVICE pointers (cloud b [M_b][3], target b of
- * lsgcpd_target_bytes(M_b) bytes); h_M: HOST [B]; h_info: HOST [B] or NULL.  One workspace of
- * lsgcpd_prepare_batch_workspace_bytes() bytes serves all targets.  sync.
+ * target; every stage runs once per wave of up to 64 targets.  h_d_xyz[b] / h_d_target[b]: HOST arrays of
+ * B DEVICE pointers (cloud b [M_b][3], target b of lsgcpd_target_bytes(M_b) bytes); h_M: HOST [B];
+ * h_info: HOST [B] or NULL.  One workspace of lsgcpd_prepare_batch_workspace_bytes() bytes serves all
+ * targets: about 512 MB of per-target regions for a wave plus O(B) bookkeeping (smaller for few targets).
+ * sync.
  * Errors: as lsgcpd_prepare_target, the message naming the problem; EINVAL also for B < 1. */
 size_t lsgcpd_prepare_batch_workspace_bytes(const int64_t* h_M, int B, int knn_k);
 int lsgcpd_prepare_batch(const float* const* h_d_xyz, const int64_t* h_M, int B,

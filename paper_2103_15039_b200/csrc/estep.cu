@@ -420,29 +420,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
             }
 #else
-            static_assert(kWPer == 1, "the per-K-step hand-off assumes one MMA warp per warpgroup");
-            const int w = w0;
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 const int ab = c & 1;
                 const uint64_t bhi = bdesc(bbase + 1024 * c), blo = bdesc(bbase + 1024 * c + 512);
-                if (c == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
-                mbar_wait_sleep(&afull[w][ab], (uint32_t)((c >> 1) & 1));
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
-                    const uint32_t colA = (uint32_t)(w * kWGCols + 32 * RB + ab * 16 * RB);
 #pragma unroll
-                    for (int rb = 0; rb < RB; ++rb) {
-                        mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, (c == 0 && first) ? 0u : 1u);
-                        mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
-                        mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
+                for (int wi = 0; wi < kWPer; ++wi) {
+                    const int w = w0 + wi;
+                    if (c == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
+                    mbar_wait_sleep(&afull[w][ab], (uint32_t)((c >> 1) & 1));
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);
+                        const uint32_t colA = (uint32_t)(w * kWGCols + 32 * RB + ab * 16 * RB);
+#pragma unroll
+                        for (int rb = 0; rb < RB; ++rb) {
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, bhi, kTcIdesc16, (c == 0 && first) ? 0u : 1u);
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16 + 8, bhi, kTcIdesc16, 1u);
+                            mma_tf32_ts(colD + rb * 16, colA + rb * 16, blo, kTcIdesc16, 1u);
+                        }
+                        mma_commit(&aempty[w][ab]);
+                        if (c == kChunks - 1 && last) mma_commit(&dfull[w][db]);
+                        // stage s's B operand read by this warp's MMAs
+                        if (c == kChunks - 1 && wi == kWPer - 1) mma_commit(&empty_bar[s]);
                     }
-                    mma_commit(&aempty[w][ab]);
-                    if (c == kChunks - 1 && last) mma_commit(&dfull[w][db]);
-                    if (c == kChunks - 1) mma_commit(&empty_bar[s]);   // stage s's B operand read
+                    __syncwarp();
                 }
-                __syncwarp();
             }
 #endif
             if (last) {

@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             int64_t tile = u0 % sc.T;
             for (int64_t it = 0; it < nunits; ++it) {
                 const int s = (int)(it & 3);
-                mbar_wait_sleep(&empty_bar[s], (uint32_t)(((it >> 2) & 1) ^ 1));
+                LSG_PWAIT(&empty_bar[s], (uint32_t)(((it >> 2) & 1) ^ 1));
                 mbar_arrive_expect_tx(&full_bar[s], kTcTileBytes);
                 bulk_g2s(&tiles_st[s][0], tc + tile * (int64_t)kTcTileBytes, kTcTileBytes, &full_bar[s]);
                 if (++tile == sc.T) tile = 0;
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const bool first = tig == 0;
             const bool last = tig + 1 == NT || tile + 1 == sc.T || it + 1 == nunits;
             const uint32_t dpar = (uint32_t)(((grp >> 1) & 1) ^ 1);   // completion (grp>>1) - 1 of dfree[db]
-            mbar_wait_sleep(&full_bar[s], (uint32_t)((it >> 2) & 1));
+            LSG_MWAIT(&full_bar[s], (uint32_t)((it >> 2) & 1));
             const uint32_t bbase = tiles0 + (uint32_t)s * kTcTileBytes;
 #if LSG_PAIRED
             // one hand-off per pair of K steps (both A buffers): afull[w][0] / aempty[w][0], parity k & 1
@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                 for (int wi = 0; wi < kWPer; ++wi) {
                     const int w = w0 + wi;
-                    if (k == 0 && first) mbar_wait_sleep(&dfree[w][db], dpar);
-                    mbar_wait_sleep(&afull[w][0], (uint32_t)(k & 1));
+                    if (k == 0 && first) LSG_MWAIT(&dfree[w][db], dpar);
+                    LSG_MWAIT(&afull[w][0], (uint32_t)(k & 1));
                     tc_fence_after();
                     if (elect_one()) {
                         const uint32_t colD = (uint32_t)(w * kWGCols + db * 16 * RB);

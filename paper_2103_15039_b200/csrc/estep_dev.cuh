@@ -147,6 +147,36 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         "r"(parity), "r"(1000000u)
         : "memory");
 }
+// Diagnostic: helper-warp waits with a fixed back-off instead of the suspend-time hint (LSG_PROD_NS: the TMA
+// producer; LSG_MMA_NS: the MMA warps).  Test the phase, else sleep NS nanoseconds, repeat.
+template <int NS>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) break;
+        __nanosleep(NS);
+    }
+}
+#ifdef LSG_PROD_NS
+#define LSG_PWAIT mbar_wait_backoff<LSG_PROD_NS>
+#else
+#define LSG_PWAIT mbar_wait_sleep
+#endif
+#ifdef LSG_MMA_NS
+#define LSG_MWAIT mbar_wait_backoff<LSG_MMA_NS>
+#else
+#define LSG_MWAIT mbar_wait_sleep
+#endif
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

@@ -280,6 +280,9 @@ int lsgcpd_register_shards(const void* d_target, int64_t M, double volume, const
  *   "graph_cache"   0: no cached EM-iteration graphs
  *   "no_graph"      1: plain launches instead of a captured EM iteration
  *   "tile_gate"     G: tile-centred residual on tiles with E_tile ≤ G·σ (≤ 0: never)
+ *   "far_rule"      1 (default): also for a warp whose points are all ≥ 2 R_tile from the tile centre; 0: off
+ *   "sort_source"   1 (default): lsgcpd_register / _shards run on a Morton-ordered copy of sources of ≥ 4,096
+ *                   points (kept in the workspace; only the FP summation order changes); 0: the given order
  * Errors: EINVAL (unknown name, value out of range). */
 int lsgcpd_set_option(const char* name, double value);
 int lsgcpd_get_option(const char* name, double* value);

@@ -197,7 +197,12 @@ static int estep_layout(int64_t M_pad, int64_t N, EstepLayout* L, Sched* sc) {
 
 struct RegLayout {
     size_t state, mom, sums, blockpart, counters, nll, sig2, iters, part, rec, total;
+    size_t srt, sphi, ssort;   // the Morton-ordered source copy and its sort scratch (0: sources not reordered)
+    int sorted;
 };
+// Sources of at least this many points are registered in Morton order (DESIGN §8 "far points"); below it the
+// sort's launches cost more than the E steps gain
+constexpr int64_t kSortMinN = 4096;
 static int reg_layout(int64_t M_pad, int64_t N, int max_iters, RegLayout* L, Sched* sc) {
     const int rc = estep_plan(M_pad, N, sc);
     if (rc) return rc;
@@ -212,7 +217,28 @@ static int reg_layout(int64_t M_pad, int64_t N, int max_iters, RegLayout* L, Sch
     L->iters = o; o += al(sizeof(int) * 4);
     L->part = o; o += al(estep_partial_bytes(*sc));
     L->rec = o; o += al(sizeof(float) * LSGCPD_REC * (size_t)N);
+    L->sorted = N >= kSortMinN && N < ((int64_t)1 << 31);
+    if (L->sorted) {
+        L->srt = o; o += al(sizeof(float) * 3 * (size_t)N);
+        L->sphi = o; o += al(sizeof(float) * (size_t)N);
+        L->ssort = o; o += al(source_sort_ws_bytes(N));
+    } else {
+        L->srt = L->sphi = L->ssort = 0;
+    }
     L->total = o;
+    return 0;
+}
+// The source the EM iterations read: a Morton-ordered copy in the workspace when the layout has one and the
+// sort_source option is on (the confidences φ reordered with it), else the caller's arrays.
+static int order_source(const float** src, const float** phi, int64_t N, char* ws, const RegLayout& L,
+                        cudaStream_t s) {
+    if (!L.sorted || options().sort_source.load() == 0) return 0;
+    float* out = reinterpret_cast<float*>(ws + L.srt);
+    float* phi_out = *phi ? reinterpret_cast<float*>(ws + L.sphi) : nullptr;
+    const int rc = source_sort_launch(*src, *phi, N, out, phi_out, ws + L.ssort, s);
+    if (rc) return rc;
+    *src = out;
+    if (*phi) *phi = phi_out;
     return 0;
 }
 
@@ -294,7 +320,7 @@ using namespace lsg;
 // =============================================================================================
 // exported C ABI
 // =============================================================================================
-LSG_EXPORT int lsgcpd_version(void) { return 10300; }
+LSG_EXPORT int lsgcpd_version(void) { return 10400; }
 LSG_EXPORT const char* lsgcpd_last_error(void) { return g_err; }
 
 LSG_EXPORT void lsgcpd_prep_params_default(lsgcpd_prep_params* p) {
@@ -598,7 +624,10 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     IterState* st = reinterpret_cast<IterState*>(ws + L.state);
     double* mom = reinterpret_cast<double*>(ws + L.mom);
     double* sums = reinterpret_cast<double*>(ws + L.sums);
-    const RegParams rp = reg_params(p, h, V, M);
+    RegParams rp = reg_params(p, h, V, M);
+    const float* d_src = d_src_local;
+    rc = order_source(&d_src, &rp.phi, N_local, ws, L, s);
+    if (rc) return rc;
 
     LSG_CUDA(cudaMemsetAsync(ws + L.counters, 0, sizeof(unsigned) * 8, s));
     LSG_CUDA(cudaMemsetAsync(ws + L.iters, 0, sizeof(int) * 4, s));
@@ -606,7 +635,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
     LSG_CUDA(cudaMemsetAsync(ws + L.sig2, 0, sizeof(double) * (p.max_iters + 2), s));
     // initial pose, then σ²₀ (CPD closed form over all ranks' points)
     estep_launch_setup(st, d_target, R, t, 1.0, rp.w, V, M, rp.consistent, rp.eta, s);
-    sigma2_sums_launch(d_src_local, N_local, st, d_target, reinterpret_cast<double*>(ws + L.blockpart), sums,
+    sigma2_sums_launch(d_src, N_local, st, d_target, reinterpret_cast<double*>(ws + L.blockpart), sums,
                        reinterpret_cast<unsigned*>(ws + L.counters), s);
     if (c) {
         const ncclResult_t r = g_nccl.AllReduce(sums, sums, 2, kNcclFloat64, kNcclSum, c->nc, s);
@@ -636,7 +665,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
         key_put(topo, nofuse);
         key = topo;
         key_put(key, d_target);
-        key_put(key, d_src_local);
+        key_put(key, d_src);
         key_put(key, ws);
         key_put(key, L);
         key_put(key, rp);
@@ -650,7 +679,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
             if (!cap) LSG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
             LSG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
             cudaGraph_t graph = nullptr;
-            rc = enqueue_iteration(d_target, d_src_local, N_local, ws, L, sc, rp, c, cap);
+            rc = enqueue_iteration(d_target, d_src, N_local, ws, L, sc, rp, c, cap);
             cudaError_t ce = cudaStreamEndCapture(cap, &graph);
             if (rc || ce != cudaSuccess) {
                 if (graph) cudaGraphDestroy(graph);
@@ -687,7 +716,7 @@ LSG_EXPORT int lsgcpd_register(const void* d_target, int64_t M, double volume, c
         LSG_CUDA(cudaStreamSynchronize(s));
     } else {
         for (int k = 0; k < p.max_iters; ++k) {
-            rc = enqueue_iteration(d_target, d_src_local, N_local, ws, L, sc, rp, c, s);
+            rc = enqueue_iteration(d_target, d_src, N_local, ws, L, sc, rp, c, s);
             if (rc) return rc;
         }
         LSG_CUDA(cudaGetLastError());
@@ -764,6 +793,13 @@ LSG_EXPORT int lsgcpd_register_shards(const void* d_target, int64_t M, double vo
         sums.p[g] = reinterpret_cast<double*>(ws[g] + L[g].sums);
     }
     NvtxRange r("lsgcpd_register_shards");
+    std::vector<const float*> src(G);
+    for (int g = 0; g < G; ++g) {   // each shard in Morton order, as lsgcpd_register orders its source
+        src[g] = h_d_src[g];
+        const float* no_phi = nullptr;
+        rc = order_source(&src[g], &no_phi, h_N[g], ws[g], L[g], s);
+        if (rc) return rc;
+    }
     for (int g = 0; g < G; ++g) {
         char* w = ws[g];
         LSG_CUDA(cudaMemsetAsync(w + L[g].counters, 0, sizeof(unsigned) * 8, s));
@@ -772,7 +808,7 @@ LSG_EXPORT int lsgcpd_register_shards(const void* d_target, int64_t M, double vo
         LSG_CUDA(cudaMemsetAsync(w + L[g].sig2, 0, sizeof(double) * (p.max_iters + 2), s));
         estep_launch_setup(reinterpret_cast<IterState*>(w + L[g].state), d_target, R, t, 1.0, rp.w, V, M,
                            rp.consistent, rp.eta, s);
-        sigma2_sums_launch(h_d_src[g], h_N[g], reinterpret_cast<IterState*>(w + L[g].state), d_target,
+        sigma2_sums_launch(src[g], h_N[g], reinterpret_cast<IterState*>(w + L[g].state), d_target,
                            reinterpret_cast<double*>(w + L[g].blockpart), sums.p[g],
                            reinterpret_cast<unsigned*>(w + L[g].counters), s);
     }
@@ -783,7 +819,7 @@ LSG_EXPORT int lsgcpd_register_shards(const void* d_target, int64_t M, double vo
     LSG_CUDA(cudaGetLastError());
     for (int k = 0; k < p.max_iters; ++k) {
         for (int g = 0; g < G; ++g) {
-            rc = enqueue_moments(d_target, h_d_src[g], h_N[g], ws[g], L[g], sc[g], rp, false, s);
+            rc = enqueue_moments(d_target, src[g], h_N[g], ws[g], L[g], sc[g], rp, false, s);
             if (rc) return rc;
         }
         shard_allreduce_kernel<<<(kMomentCount + 127) / 128, 128, 0, s>>>(mom, G, kMomentCount);
@@ -835,6 +871,10 @@ LSG_EXPORT int lsgcpd_set_option(const char* name, double value) {
         o.no_graph.store(iv);
     } else if (!strcmp(name, "tile_gate")) {
         o.tile_gate.store((float)value);
+    } else if (!strcmp(name, "far_rule")) {
+        o.far_rule.store(iv ? 1 : 0);
+    } else if (!strcmp(name, "sort_source")) {
+        o.sort_source.store(iv ? 1 : 0);
     } else {
         set_error("unknown option '%s'", name);
         return LSGCPD_EINVAL;
@@ -852,6 +892,8 @@ LSG_EXPORT int lsgcpd_get_option(const char* name, double* value) {
     else if (!strcmp(name, "graph_cache")) *value = o.graph_cache.load();
     else if (!strcmp(name, "no_graph")) *value = o.no_graph.load();
     else if (!strcmp(name, "tile_gate")) *value = o.tile_gate.load();
+    else if (!strcmp(name, "far_rule")) *value = o.far_rule.load();
+    else if (!strcmp(name, "sort_source")) *value = o.sort_source.load();
     else {
         set_error("unknown option '%s'", name);
         return LSGCPD_EINVAL;
@@ -961,6 +1003,7 @@ static int batch_layout(const lsgcpd_problem* P, int B, int max_iters, BatchLayo
     memset(&sc, 0, sizeof(sc));
     sc.halves = 1;
     sc.gate_g = options().tile_gate.load();
+    sc.far_rule = options().far_rule.load() ? 1 : 0;
     sc.U = units;
     const int64_t slots = (int64_t)nsm;       // one CTA per SM (both batched E-step kernels)
     sc.G = units < slots ? units : slots;

@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(kBTThreads, 1)
             }
 #endif
         };
-        if (tile_cheap(tm, gate)) run_tile(std::true_type());
+        if (tile_cheap(tm, gate) || (sc.far_rule && warp_far<RB>(h, l, tm))) run_tile(std::true_type());
         else run_tile(std::false_type());
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[s]);

@@ -60,7 +60,7 @@ struct TargetHeader {
     uint32_t pad_[2];
 };
 static_assert(sizeof(TargetHeader) <= kHeaderBytes, "header too big");
-constexpr uint32_t kTargetMagic = 0x4c534744u;  // "LSGD": layout 2 (slot order, tile-centred core)
+constexpr uint32_t kTargetMagic = 0x4c534745u;  // "LSGE": layout 3 (slot order, tile-centred core, R_tile)
 
 inline int64_t pad_targets(int64_t M) { return (M + kTgtPadMultiple - 1) / kTgtPadMultiple * kTgtPadMultiple; }
 inline const float* target_body(const void* t) { return reinterpret_cast<const float*>(static_cast<const char*>(t) + kHeaderBytes); }
@@ -74,8 +74,8 @@ inline float* target_body(void* t) { return reinterpret_cast<float*>(static_cast
 //   [0, 2048)     core: 32 target pairs × 64 B, field f of targets (2i, 2i+1) adjacent, f = y'0, y'1, y'2,
 //                 ω̄, ñ0, ñ1, ñ2, meta.  y' = y - c_tile, exact in FP32 (c_a = 0 on an axis where it would
 //                 not be); the CUDA-core part of the pair math, two targets per f32x2 instruction.
-//                 meta of targets 0, 1, 2, 3 = c_0, c_1, c_2, E_tile = R_tile·√(1 + max α) with R_tile =
-//                 max ||y'|| over the tile's real targets (the E step's per-tile precision gate).
+//                 meta of targets 0, 1, 2, 3, 4 = c_0, c_1, c_2, E_tile = R_tile·√(1 + max α), R_tile (rounded
+//                 up) with R_tile = max ||y'|| over the tile's real targets (the E step's precision gates).
 //   [2048, 10240) 8 K-steps × 1024 B: the 32×8 B operand [F_hi; F_lo] of one K step, where
 //                 F[f][m] = (1, y, W, b, 0,0,0) (original coordinates), F_hi = F rounded to TF32 (nearest),
 //                 F_lo = F - F_hi (exact in FP32, read as TF32 by the MMA); UMMA K-major, no swizzle:
@@ -249,6 +249,7 @@ struct Sched {
     int tc_variant;   // tensor-core kernel configuration
     int halves;       // 2: the targets are swept as two halves, one launch each (T = tiles per half); else 1
     float gate_g;     // tile-centred residual when E_tile ≤ gate_g·σ, else the hi/lo residual
+    int far_rule;     // 1: also the centred residual for a warp whose points are all ≥ 2 R_tile from the centre
     int64_t hstride;  // floats between the two halves' partial sets
 };
 __host__ __device__ inline int64_t sched_start(const Sched& s, int64_t g) { return g * s.U / s.G; }

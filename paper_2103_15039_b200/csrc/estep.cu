@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
 #endif
         };
-        if (tile_cheap(tm, gate)) run_tile(std::true_type());
+        if (tile_cheap(tm, gate) || (sc.far_rule && warp_far<RB>(h, l, tm))) run_tile(std::true_type());
         else run_tile(std::false_type());
         __syncwarp();   // this warp is done reading the stage's core data
         if (lane == 0) mbar_arrive(&empty_bar[it & 3]);
@@ -802,6 +802,7 @@ int estep_plan(int64_t M_pad, int64_t N, Sched* sc) {
     const bool split = tc && (M_pad / kTT) * (int64_t)kTcTileBytes > kSplitBytes && hv != 1;
     s.halves = split ? 2 : 1;
     s.gate_g = op.tile_gate.load();
+    s.far_rule = op.far_rule.load() ? 1 : 0;
     s.T = M_pad / kTT / s.halves;
     s.U = s.nblk * s.T;
     const int64_t slots = (int64_t)di->nsm * (tc ? 1 : di->occ[vi]);   // the TC kernel holds all TMEM: 1 CTA/SM
@@ -871,6 +872,8 @@ Options::Options() {
     no_graph.store(env_int("LSGCPD_NO_GRAPH", 0));
     const char* g = getenv("LSGCPD_TILE_GATE");
     tile_gate.store(g && *g ? (float)atof(g) : kDefaultTileGate);
+    far_rule.store(env_int("LSGCPD_FAR_RULE", 1));
+    sort_source.store(env_int("LSGCPD_SORT_SOURCE", 1));
 }
 Options& options() {
     static Options o;   // thread-safe one-time initialisation (C++11 magic static)

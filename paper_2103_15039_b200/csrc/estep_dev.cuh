@@ -290,10 +290,11 @@ __device__ __forceinline__ uint64_t bdesc(uint32_t saddr) {
 struct TileMeta {
     float c[3];
     float E;
+    float R;
 };
 __device__ __forceinline__ TileMeta tile_meta(const float4* core) {
-    const float4 a = core[3], b = core[7];   // spare fields of targets 0..3 (see common.cuh)
-    return {{a.z, a.w, b.z}, b.w};
+    const float4 a = core[3], b = core[7], e = core[11];   // spare fields of targets 0..4 (see common.cuh)
+    return {{a.z, a.w, b.z}, b.w, e.z};
 }
 template <bool kCheap, int RB>
 __device__ __forceinline__ void tile_points(const float (&h)[RB][3], const float (&l)[RB][3], const TileMeta& tm,
@@ -351,6 +352,24 @@ __device__ __forceinline__ void tc_chunk_pairs(const float4* __restrict__ core, 
 }
 // the tile's residual mode: centred when E_tile ≤ gate (gate = gate_g·σ, uniform over the CTA)
 __device__ __forceinline__ bool tile_cheap(const TileMeta& tm, float gate) { return tm.E <= gate; }
+// ... or, per warp, when every point of the warp is at least 2 R_tile from the tile centre (DESIGN §8 "far
+// points"): then |r| ≥ |x'| - R_tile ≥ |x'|/2 for every pair, so the centred residual's extra rounding
+// ε|x'| is at most 2ε|r| — the hi/lo residual's relative accuracy up to a small factor, whatever σ is
+template <int RB>
+__device__ __forceinline__ bool warp_far(const float (&h)[RB][3], const float (&l)[RB][3], const TileMeta& tm) {
+    bool far = true;
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb) {
+        float d2 = 0.f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float x = __fadd_rn(__fsub_rn(h[rb][a], tm.c[a]), l[rb][a]);
+            d2 = __fmaf_rn(x, x, d2);
+        }
+        far = far && d2 >= 4.01f * tm.R * tm.R;
+    }
+    return __all_sync(0xffffffffu, far);
+}
 
 // One point of the split-M merge: the nk partials of its source block start at `blk` (slot stride
 // kPartF·kB floats, field stride kB, point index b), `phi` → φ(x_n) or NULL, record row `r`.

@@ -8,7 +8,7 @@ namespace lsg {
 
 // Run-time knobs (diagnostics and tests; the defaults are the product configuration).  Initialised once from
 // the environment (LSGCPD_TC, LSGCPD_ESTEP_VARIANT, LSGCPD_HALVES, LSGCPD_NO_FUSE, LSGCPD_GRAPH_CACHE,
-// LSGCPD_NO_GRAPH, LSGCPD_TILE_GATE); lsgcpd_set_option changes them.  Atomic: calls on other threads see a
+// LSGCPD_NO_GRAPH, LSGCPD_TILE_GATE, LSGCPD_FAR_RULE, LSGCPD_SORT_SOURCE); lsgcpd_set_option changes them.  Atomic: calls on other threads see a
 // consistent value per field.
 constexpr float kDefaultTileGate = 24.f;   // E_tile ≤ gate·σ → tile-centred residual
 struct Options {
@@ -19,6 +19,8 @@ struct Options {
     std::atomic<int> graph_cache;     // 0: no cached EM-iteration graphs
     std::atomic<int> no_graph;        // 1: plain launches instead of a captured EM iteration
     std::atomic<float> tile_gate;     // gate_g of Sched (≤ 0: hi/lo residual on every tile)
+    std::atomic<int> far_rule;        // far_rule of Sched (0: the tile gate alone picks the residual)
+    std::atomic<int> sort_source;     // 1: lsgcpd_register runs on a Morton-ordered copy of the source
     Options();
 };
 Options& options();
@@ -91,6 +93,9 @@ constexpr int64_t kTailMaxN = 1 << 17;   // above this the separate merge / mome
 
 // target.cu
 size_t prepare_ws_bytes(int64_t M);
+size_t source_sort_ws_bytes(int64_t N);
+int source_sort_launch(const float* src, const float* phi, int64_t N, float* out, float* phi_out, void* d_ws,
+                       cudaStream_t stream);
 size_t pack_ws_bytes(int64_t M);
 int pack_target_impl(const float* d_xyz, const float* d_nrm, const float* d_alpha, int64_t M, double margin,
                      void* d_target, void* d_ws, lsgcpd_target_info* info, cudaStream_t stream);

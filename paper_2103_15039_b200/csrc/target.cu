@@ -320,7 +320,9 @@ __device__ __forceinline__ void pack_tc_body(const float* __restrict__ xyz, cons
         F[7] = (float)(a * n[1] * n[1]); F[8] = (float)(a * n[1] * n[2]); F[9] = (float)(a * n[2] * n[2]);
         F[10] = (float)(a * ny * n[0]); F[11] = (float)(a * ny * n[1]); F[12] = (float)(a * ny * n[2]);
     }
-    cf[7] = jt < 3 ? c[jt] : (jt == 3 ? E : 0.f);   // tile meta in the spare field of targets 0..3
+    // tile meta in the spare field of targets 0..4: c_0, c_1, c_2, E_tile, R_tile (rounded up)
+    const float Rt = __double2float_ru(s_r[0]);
+    cf[7] = jt < 3 ? c[jt] : (jt == 3 ? E : (jt == 4 ? Rt : 0.f));
     for (int f = 0; f < 8; ++f) core[2 * f] = cf[f];
     const int s = jt / 8, j = jt % 8;
     for (int f = 0; f < 16; ++f) {
@@ -830,6 +832,62 @@ static PrepLayout prep_layout(int64_t M, bool with_knn) {
 }
 
 size_t prepare_ws_bytes(int64_t M) { return prep_layout(M, true).total; }
+
+// ---- source order for the E step (DESIGN §8 "far points") ---------------------------------------------
+// lsgcpd_register runs on a Morton-ordered copy of the source (and of its confidences): a warp's points are
+// then spatially compact, so for most target tiles all of them are far from the tile and the warp takes the
+// cheaper centred residual.  The registration is a sum over points: the order changes only FP summation.
+// Device-side only (no host synchronisation): the source box from cloud_stats, keys, a stable radix sort, gather.
+__global__ void source_gather_kernel(const float* __restrict__ src, const float* __restrict__ phi,
+                                     const int* __restrict__ perm, int64_t N, float* __restrict__ out,
+                                     float* __restrict__ phi_out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const int64_t j = perm[i];
+    out[3 * i] = src[3 * j];
+    out[3 * i + 1] = src[3 * j + 1];
+    out[3 * i + 2] = src[3 * j + 2];
+    if (phi) phi_out[i] = phi[j];
+}
+struct SrcSortLayout {
+    size_t keys, keys_s, ids, perm, part, stats, ctr, cub, total;
+    size_t cub_bytes;
+};
+static SrcSortLayout src_sort_layout(int64_t N) {
+    SrcSortLayout L;
+    size_t o = 0;
+    L.keys = o; o += al(sizeof(uint64_t) * N);
+    L.keys_s = o; o += al(sizeof(uint64_t) * N);
+    L.ids = o; o += al(sizeof(int) * N);
+    L.perm = o; o += al(sizeof(int) * N);
+    L.part = o; o += al(sizeof(double) * kRedBlocks * 16);
+    L.stats = o; o += al(sizeof(double) * 16);
+    L.ctr = o; o += al(sizeof(unsigned) * 4);
+    L.cub_bytes = cub_morton_bytes(N);
+    L.cub = o; o += al(L.cub_bytes);
+    L.total = o;
+    return L;
+}
+size_t source_sort_ws_bytes(int64_t N) { return src_sort_layout(N).total; }
+int source_sort_launch(const float* src, const float* phi, int64_t N, float* out, float* phi_out, void* d_ws,
+                       cudaStream_t stream) {
+    const SrcSortLayout L = src_sort_layout(N);
+    char* ws = static_cast<char*>(d_ws);
+    unsigned* ctr = reinterpret_cast<unsigned*>(ws + L.ctr);
+    double* stats = reinterpret_cast<double*>(ws + L.stats);
+    LSG_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned) * 4, stream));
+    cloud_stats_kernel<<<kRedBlocks, kRedThreads, 0, stream>>>(src, N, reinterpret_cast<double*>(ws + L.part), stats, ctr);
+    uint64_t* k = reinterpret_cast<uint64_t*>(ws + L.keys);
+    int* ids = reinterpret_cast<int*>(ws + L.ids);
+    int* perm = reinterpret_cast<int*>(ws + L.perm);
+    morton_keys_kernel<<<(unsigned)((N + 255) / 256), 256, 0, stream>>>(src, N, stats, k, ids);
+    size_t cb = L.cub_bytes;
+    LSG_CUDA(cub::DeviceRadixSort::SortPairs(ws + L.cub, cb, k, reinterpret_cast<uint64_t*>(ws + L.keys_s), ids, perm,
+                                             (int)N, 0, 63, stream));
+    source_gather_kernel<<<(unsigned)((N + 255) / 256), 256, 0, stream>>>(src, phi, perm, N, out, phi_out);
+    LSG_CUDA(cudaGetLastError());
+    return 0;
+}
 size_t pack_ws_bytes(int64_t M) { return prep_layout(M, false).total; }
 
 // Model statistics, header and the two packed sections of one target (async; st1 = its cloud statistics).

@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_version_and_pure_host_queries(L):
-    assert L.lsgcpd_version() == 10300
+    assert L.lsgcpd_version() == 10400
     assert L.lsgcpd_last_error() is not None
     # header + body + tensor-core section + slot section (original index -> Morton slot)
     assert L.lsgcpd_target_bytes(1000) == 256 + 1024 * 64 + (1024 // 64) * 10240 + 1024 * 4

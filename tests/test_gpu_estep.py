@@ -306,6 +306,48 @@ def test_tile_centres_exact_on_zero_crossing_and_offset_axes():
                 _check(rec, ora, Y, a32, X, R, t, s2, f"zero-crossing/offset {gate} s2={s2}")
 
 
+def _morton_order(X):
+    # a plain Z-order of the points (test-side, independent of the library's own source ordering)
+    lo, hi = X.min(0), X.max(0)
+    q = np.floor((X - lo) / max(float((hi - lo).max()), 1e-30) * 1023.0).astype(np.uint64)
+    key = np.zeros(len(X), np.uint64)
+    for b in range(10):
+        for a in range(3):
+            key |= ((q[:, a] >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + a)
+    return np.argsort(key, kind="stable")
+
+
+@pytest.mark.parametrize("name", ["object", "lidar"])
+def test_estep_far_rule_on_spatially_ordered_sources(name):
+    # the far-point rule (a warp whose points are all >= 2 R_tile from a tile's centre takes the centred residual)
+    # only fires when a warp's points are close together: Z-ordered sources.  Checked with the tile gate off, so
+    # that every centred tile comes from the rule, and with the product gates; object full records, lidar
+    # sampled, at the initial, intermediate and converged σ²
+    wl, n32, a32, V, ext = oracle_target32(name)
+    X = wl.source[_morton_order(wl.source)]
+    R, t = wl.R_expected, wl.t_expected
+    tgt = _gpu_target(wl.target, n32, a32)
+    idx = np.arange(len(X)) if name == "object" else np.sort(np.random.default_rng(8).choice(len(X), 3000, replace=False))
+    import paper_2103_15039_b200 as lsg
+    Xd = to_dev(X)
+    for s2 in (oracle.sigma2_init(X, wl.target, R, t), 1e-3, 1e-4):
+        ora = oracle.estep(wl.target, n32.astype(np.float64), a32.astype(np.float64), X[idx], R, t, s2, wl.w, V)
+        for opts in ({"tile_gate": 0.0, "far_rule": 1}, {"far_rule": 1}):
+            with lsg.options(tc=1, **opts):
+                rec = lsg.estep(tgt, Xd, R, t, s2, wl.w, V).cpu().numpy()[idx]
+            assert_record_parity(rec, ora, wl.target, a32, what=f"{name} far rule {opts} s2={s2:.1e}",
+                                 Xh=transformed(X[idx], R, t), s2=s2)
+        if s2 == 1e-3 and name == "lidar":   # the rule fires: with the gate off it changes some records' rounding
+            # (object's tiles around the origin often keep c_a = 0 on an axis — y - c would not be exact — so
+            # their R_tile is large and the rule rarely holds there)
+            with lsg.options(tc=1, tile_gate=0.0, far_rule=0):
+                hilo = lsg.estep(tgt, Xd, R, t, s2, wl.w, V).cpu().numpy()
+            with lsg.options(tc=1, tile_gate=0.0, far_rule=1):
+                far = lsg.estep(tgt, Xd, R, t, s2, wl.w, V).cpu().numpy()
+            assert not np.array_equal(hilo, far), "the far-point rule never fired"
+
+
+
 def test_estep_literal_normaliser_with_the_centred_residual():
     # the Eq. 9-10 literal normaliser (kLiteral instantiation) on tiles that take the tile-centred residual:
     # object at σ²₀ and σ² = 0.05, where E_tile / σ is under the default gate

@@ -1,6 +1,6 @@
-"""Max scaled E-step error vs the oracle per tile-gate value (DESIGN §8 "tile-centred residual"): object and rgbd
-(full records), tiny, and scale (4,096 sampled points), at σ²₀, 1e-3, 1e-4 and the converged σ² of the goldens.
-Diagnostic (imports the oracle).
+"""Max scaled E-step error vs the oracle per tile-gate value (DESIGN §8 "tile-centred residual"), without and with
+the far-point rule: object and rgbd (full records), tiny, lidar and scale (4,096 sampled points), at σ²₀, 1e-3,
+1e-4 and the converged σ² of the goldens.  Diagnostic (imports the oracle).
 python tests/tools/gate_sweep.py [config ...]"""
 import json
 import os
@@ -16,8 +16,9 @@ import paper_2103_15039_b200 as lsg  # noqa: E402
 from tests.gpu_common import oracle_target32  # noqa: E402
 from tests.parity import record_errors, transformed  # noqa: E402
 
-SWEEPS = [("G", "tile_gate", [0.0, 4.0, 8.0, 12.0, 16.0, 24.0, 32.0, 48.0, 1e30], {})]
-for name in sys.argv[1:] or ["tiny", "object", "rgbd", "scale"]:
+SWEEPS = [("G", "tile_gate", [0.0, 8.0, 16.0, 24.0, 32.0, 48.0, 1e30], {"far_rule": 0}),
+          ("G+far", "tile_gate", [0.0, 24.0, 48.0], {"far_rule": 1})]
+for name in sys.argv[1:] or ["tiny", "object", "rgbd", "lidar", "scale"]:
     wl, n32, a32, V, ext = oracle_target32(name)
     tgt = lsg.pack_target(torch.from_numpy(wl.target).cuda(), torch.from_numpy(n32).cuda(), torch.from_numpy(a32).cuda())
     X = torch.from_numpy(wl.source).cuda()

@@ -251,3 +251,23 @@ def test_concurrent_calls_on_two_threads_and_streams():
             np.testing.assert_array_equal(r["R"], alone[i]["R"])
             np.testing.assert_array_equal(r["t"], alone[i]["t"])
             assert r["sigma2"] == alone[i]["sigma2"]
+
+
+@pytest.mark.parametrize("name", ["rgbd", "lidar"])
+def test_register_source_order_and_far_rule_do_not_change_the_result(name):
+    # lsgcpd_register runs on a Morton-ordered copy of the source and lets far warps take the centred residual
+    # (DESIGN §8 "far points"): against the given order with the rule off, only the FP summation order and the
+    # residual's rounding differ, so the poses agree far inside the 1e-4 rad bar and σ² to the E step's FP32
+    # rounding; with the same options the result is bit-for-bit repeatable
+    import paper_2103_15039_b200 as lsg
+    wl = workload(name)
+    tgt = lsg.prepare_target(to_dev(wl.target), wl.knn_k)
+    X = to_dev(wl.source)
+    out = {}
+    for key, opts in (("plain", {"sort_source": 0, "far_rule": 0}), ("product", {}), ("again", {})):
+        with lsg.options(**opts):
+            out[key] = lsg.register(tgt, X, wl.iters, w=wl.w)
+    a, b = out["plain"], out["product"]
+    _close(b["R"], b["t"], a["R"], a["t"], float(np.linalg.norm(wl.target.max(0) - wl.target.min(0))), tol=1e-6)
+    assert abs(b["sigma2"] / a["sigma2"] - 1.0) <= 1e-5, (b["sigma2"], a["sigma2"])
+    assert np.array_equal(out["again"]["R"], b["R"]) and out["again"]["sigma2"] == b["sigma2"]

@@ -355,6 +355,9 @@ __device__ __forceinline__ bool tile_cheap(const TileMeta& tm, float gate) { ret
 // ... or, per warp, when every point of the warp is at least 2 R_tile from the tile centre (DESIGN §8 "far
 // points"): then |r| ≥ |x'| - R_tile ≥ |x'|/2 for every pair, so the centred residual's extra rounding
 // ε|x'| is at most 2ε|r| — the hi/lo residual's relative accuracy up to a small factor, whatever σ is
+#ifndef LSG_FAR_K2
+#define LSG_FAR_K2 4.01f   // (2 R_tile)² with a margin: |r| ≥ |x'| - R_tile ≥ |x'|/2
+#endif
 template <int RB>
 __device__ __forceinline__ bool warp_far(const float (&h)[RB][3], const float (&l)[RB][3], const TileMeta& tm) {
     bool far = true;
@@ -366,7 +369,7 @@ __device__ __forceinline__ bool warp_far(const float (&h)[RB][3], const float (&
             const float x = __fadd_rn(__fsub_rn(h[rb][a], tm.c[a]), l[rb][a]);
             d2 = __fmaf_rn(x, x, d2);
         }
-        far = far && d2 >= 4.01f * tm.R * tm.R;
+        far = far && d2 >= LSG_FAR_K2 * tm.R * tm.R;
     }
     return __all_sync(0xffffffffu, far);
 }

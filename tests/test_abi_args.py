@@ -167,3 +167,4 @@ def test_register_shards_shard_count_refused(L, G):
     rc = L.lsgcpd_register_shards(FAKE, 100, 0.0, ptrs, Ns, G, None, R0, t0, R.ctypes.data_as(dp),
                                   t.ctypes.data_as(dp), s2.ctypes.data_as(dp), it, FAKE, 1 << 20, None)
     assert rc == EINVAL and "out of range" in _err(L)
+

@@ -271,3 +271,13 @@ def test_register_source_order_and_far_rule_do_not_change_the_result(name):
     _close(b["R"], b["t"], a["R"], a["t"], float(np.linalg.norm(wl.target.max(0) - wl.target.min(0))), tol=1e-6)
     assert abs(b["sigma2"] / a["sigma2"] - 1.0) <= 1e-5, (b["sigma2"], a["sigma2"])
     assert np.array_equal(out["again"]["R"], b["R"]) and out["again"]["sigma2"] == b["sigma2"]
+
+
+def test_register_workspace_holds_the_ordered_source_from_4096_points():
+    # sources of >= 4,096 points are registered on a Morton-ordered copy kept in the workspace: the workspace
+    # grows by at least the copy, its φ and the sort's keys and ids at that size (the query needs the device)
+    import paper_2103_15039_b200 as lsg
+    L = lsg.lib()
+    below = L.lsgcpd_register_workspace_bytes(10000, 4095, 50)
+    at = L.lsgcpd_register_workspace_bytes(10000, 4096, 50)
+    assert below > 0 and at - below >= 4096 * (12 + 4 + 8 + 8 + 4 + 4)
